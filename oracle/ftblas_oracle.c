@@ -1,0 +1,373 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of online ABFT DGEMM as
+ * described in FT-BLAS (arXiv 2104.00897).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference leg may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2104_00897_b200/csrc); neither side includes or links the other.
+ *
+ * Arithmetic: IEEE fp64, round-to-nearest, compiled WITHOUT -ffast-math and with
+ * -ffp-contract=off so every `x*y + z` below is two roundings, exactly as written.
+ *
+ * What it computes (citations are PAPER.md line numbers and sections):
+ *   - Checksum encoding A^c = [A; e^T A], B^r = [B, B e]        PAPER.md:90 §II.A
+ *   - Outer-product maintenance C^f = sum_s A^c(:,s) B^r(s,:)   PAPER.md:93-95 §II.A
+ *     restricted to one verification unit (row block I, column block J,
+ *     k-interval of length Kc): the carried checksums are (e^T A_I) B_J and A_I (B_J e).
+ *   - Reference checksums from the computed C, compare, locate    PAPER.md:258 §V.A
+ *   - One error per verification interval, no checkpoint/rollback PAPER.md:95 §II.A
+ *   - Correction ("subtracting the error magnitude from the erroneous position")
+ *     PAPER.md:445 §VI.C is the optional `subtract` mode; the default `recompute`
+ *     mode restores C_ij from a fresh dot product (reading R4).
+ *   - Detection threshold: the paper says only "round-off threshold"
+ *     (PAPER.md:91); the reading used is the rigorous per-unit bound R1:
+ *       tau_col = 2*gamma(kt+bm)*kt*bm*amax*bmax,  tau_row = 2*gamma(kt+bn)*kt*bn*amax*bmax
+ *     with gamma(n) = n*u/(1-n*u), u = 2^-53, kt = k accumulated so far.
+ *   - Multi-flag units (out of the paper's one-error model) are recomputed once
+ *     without re-verification (reading R6/R13).
+ *   - Injected faults: acc_ij += delta after step_q rank-1 updates, with
+ *     step_q = floor(step/BK)*BK (reading R8; "an element of matrix C
+ *     is randomly selected for modification when an injection point is reached").
+ *
+ * Parity pins: tests/test_oracle.py (run with -m "not gpu").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct { int64_t i, j, step; double delta; } or_fault_t;
+typedef struct {
+  int64_t i, j;
+  int32_t kind;      /* 1 = corrected at (i,j); 2 = recomputed unit with origin (i,j) */
+  int32_t interval;  /* verification interval index t */
+  double residual_row, residual_col;
+} or_event_t;
+
+enum { OR_UNITS_CHECKED = 0, OR_DETECTED, OR_CORRECTED, OR_RECOMPUTED, OR_N_EVENTS, OR_NCOUNTERS };
+
+static const double U = 0x1p-53; /* unit roundoff of binary64 */
+
+/* gamma(n) = n u / (1 - n u)  (standard rounding-error constant; R1). */
+double oracle_gamma(int64_t n) {
+  double nu = (double)n * U;
+  return nu / (1.0 - nu);
+}
+
+/* tau = 2 * gamma(kt + len) * kt * len * amax * bmax  (R1), evaluated
+ * left to right exactly as written. */
+double oracle_tau(int64_t kt, int64_t len, double amax, double bmax) {
+  return 2.0 * oracle_gamma(kt + len) * (double)kt * (double)len * amax * bmax;
+}
+
+/* op(A)(r, c) for a column-major matrix with leading dimension ld;
+ * trans 'N' reads M[r + c*ld], 'T'/'C' reads M[c + r*ld] (real data: C == T). */
+static double op_at(const double *M, int64_t ld, int trans, int64_t r, int64_t c) {
+  return trans ? M[c + r * ld] : M[r + c * ld];
+}
+
+static int is_trans(char t) { return t == 'T' || t == 't' || t == 'C' || t == 'c'; }
+
+/* ---------------------------------------------------------------------------
+ * Plain definitions used by the pins (each one a formula written out).
+ * ------------------------------------------------------------------------- */
+
+/* Column sums e^T M of an r x c column-major matrix (e^T A). */
+void oracle_col_sums(int64_t r, int64_t c, const double *M, int64_t ld, double *out) {
+  for (int64_t j = 0; j < c; ++j) {
+    double s = 0.0;
+    for (int64_t i = 0; i < r; ++i) s += M[i + j * ld];
+    out[j] = s;
+  }
+}
+
+/* Row sums M e of an r x c column-major matrix (B e). */
+void oracle_row_sums(int64_t r, int64_t c, const double *M, int64_t ld, double *out) {
+  for (int64_t i = 0; i < r; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j < c; ++j) s += M[i + j * ld];
+    out[i] = s;
+  }
+}
+
+/* Plain product C = alpha*op(A)*op(B) + beta*C, triple loop, p ascending,
+ * no ABFT (the DGEMM definition; PAPER.md:182 routine).  beta == 0: C0 not read. */
+void oracle_gemm_plain(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
+                       const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                       double *C, int64_t ldc) {
+  int tA = is_trans(ta), tB = is_trans(tb);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t j = 0; j < n; ++j) {
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int64_t p = 0; p < k; ++p) acc += op_at(A, lda, tA, i, p) * op_at(B, ldb, tB, p, j);
+      double out = alpha * acc;
+      if (beta != 0.0) out = out + beta * C[i + j * ldc];
+      C[i + j * ldc] = out;
+    }
+  }
+}
+
+/* Selected elements of the plain product: out[e] = alpha*sum_p opA(i,p)opB(p,j) + beta*C0[e]
+ * (C0 given per element, ignored when beta == 0).  Used for sampled parity at full size. */
+void oracle_gemm_elements(char ta, char tb, int64_t k, double alpha, const double *A, int64_t lda,
+                          const double *B, int64_t ldb, double beta, int64_t ne, const int64_t *ii,
+                          const int64_t *jj, const double *c0, double *out) {
+  int tA = is_trans(ta), tB = is_trans(tb);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < ne; ++e) {
+    double acc = 0.0;
+    for (int64_t p = 0; p < k; ++p) acc += op_at(A, lda, tA, ii[e], p) * op_at(B, ldb, tB, p, jj[e]);
+    double o = alpha * acc;
+    if (beta != 0.0) o = o + beta * c0[e];
+    out[e] = o;
+  }
+}
+
+/* |C - C_ref| bound helper: S_ij = sum_p |opA(i,p)| |opB(p,j)| for selected elements. */
+void oracle_abs_product_elements(char ta, char tb, int64_t k, const double *A, int64_t lda,
+                                 const double *B, int64_t ldb, int64_t ne, const int64_t *ii,
+                                 const int64_t *jj, double *out) {
+  int tA = is_trans(ta), tB = is_trans(tb);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < ne; ++e) {
+    double s = 0.0;
+    for (int64_t p = 0; p < k; ++p)
+      s += fabs(op_at(A, lda, tA, ii[e], p)) * fabs(op_at(B, ldb, tB, p, jj[e]));
+    out[e] = s;
+  }
+}
+
+/* ---------------------------------------------------------------------------
+ * One verification unit: rows [i0, i0+bm), columns [j0, j0+bn), all intervals.
+ * Follows PAPER.md:93-95 (outer-product maintenance) and 258 (verify/locate),
+ * step by step, in the paper's order: for every rank-Kc step, update C, update
+ * the checksums, then verify.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int tA, tB;
+  int64_t k, Kc, BK;
+  const double *A, *B;
+  int64_t lda, ldb;
+  int subtract_mode;
+} unit_ctx_t;
+
+typedef struct {
+  int64_t detected, corrected, recomputed, checked;
+} unit_counts_t;
+
+/* Fresh dot product over p in [0, pe), p ascending. */
+static double dot_upto(const unit_ctx_t *x, int64_t i, int64_t j, int64_t pe) {
+  double s = 0.0;
+  for (int64_t p = 0; p < pe; ++p) s += op_at(x->A, x->lda, x->tA, i, p) * op_at(x->B, x->ldb, x->tB, p, j);
+  return s;
+}
+
+static void apply_faults_at(double *acc, int64_t bm, int64_t i0, int64_t j0, const or_fault_t *f,
+                            int64_t nf, int64_t BK, int64_t step_q_wanted) {
+  for (int64_t e = 0; e < nf; ++e) {
+    int64_t step_q = (f[e].step / BK) * BK; /* reading R8: quantised to BK */
+    if (step_q == step_q_wanted) acc[(f[e].i - i0) + (f[e].j - j0) * bm] += f[e].delta;
+  }
+}
+
+/* Returns number of events written into ev (at most ev_cap). */
+static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t j0, int64_t bn,
+                           const or_fault_t *f, int64_t nf, double *acc /* bm*bn, out */,
+                           or_event_t *ev, int64_t ev_cap, unit_counts_t *cnt) {
+  const int64_t k = x->k, Kc = x->Kc;
+  const int64_t T = (k + Kc - 1) / Kc;
+  double *cs_col = calloc((size_t)bn, sizeof(double)); /* (e^T A_I) B_J, carried */
+  double *cs_row = calloc((size_t)bm, sizeof(double)); /* A_I (B_J e), carried   */
+  double *r_col = malloc((size_t)bn * sizeof(double));
+  double *r_row = malloc((size_t)bm * sizeof(double));
+  double *d_col = malloc((size_t)bn * sizeof(double));
+  double *d_row = malloc((size_t)bm * sizeof(double));
+  double amax = 0.0, bmax = 0.0;
+  int64_t nev = 0;
+  memset(acc, 0, (size_t)(bm * bn) * sizeof(double));
+
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t ps = t * Kc, pe = (ps + Kc < k) ? ps + Kc : k;
+    for (int64_t p = ps; p < pe; ++p) {
+      /* Injection point: faults whose quantised step equals p land before update p. */
+      apply_faults_at(acc, bm, i0, j0, f, nf, x->BK, p);
+
+      /* Encode: a_sum = sum_{i in I} opA(i,p)  (e^T A column p),
+       *                       b_sum = sum_{j in J} opB(p,j)  (B e row p);
+       * running maxima for the threshold (R1). */
+      double a_sum = 0.0, b_sum = 0.0;
+      for (int64_t i = 0; i < bm; ++i) {
+        double a = op_at(x->A, x->lda, x->tA, i0 + i, p);
+        a_sum += a;
+        if (fabs(a) > amax) amax = fabs(a);
+      }
+      for (int64_t j = 0; j < bn; ++j) {
+        double b = op_at(x->B, x->ldb, x->tB, p, j0 + j);
+        b_sum += b;
+        if (fabs(b) > bmax) bmax = fabs(b);
+      }
+
+      /* Rank-1 update of C (C_s = A(:,s) B(s,:)). */
+      for (int64_t j = 0; j < bn; ++j) {
+        double b = op_at(x->B, x->ldb, x->tB, p, j0 + j);
+        for (int64_t i = 0; i < bm; ++i) acc[i + j * bm] += op_at(x->A, x->lda, x->tA, i0 + i, p) * b;
+      }
+
+      /* Checksum maintenance: C^c += (e^T A(:,p)) B(p,:),
+       * C^r += A(:,p) (B(p,:) e). */
+      for (int64_t j = 0; j < bn; ++j) cs_col[j] += a_sum * op_at(x->B, x->ldb, x->tB, p, j0 + j);
+      for (int64_t i = 0; i < bm; ++i) cs_row[i] += op_at(x->A, x->lda, x->tA, i0 + i, p) * b_sum;
+    }
+    if (t == T - 1) apply_faults_at(acc, bm, i0, j0, f, nf, x->BK, k); /* step_q == k */
+
+    /* Reference checksums from the computed C: r_col = e^T C_IJ, r_row = C_IJ e. */
+    for (int64_t j = 0; j < bn; ++j) {
+      double s = 0.0;
+      for (int64_t i = 0; i < bm; ++i) s += acc[i + j * bm];
+      r_col[j] = s;
+    }
+    for (int64_t i = 0; i < bm; ++i) {
+      double s = 0.0;
+      for (int64_t j = 0; j < bn; ++j) s += acc[i + j * bm];
+      r_row[i] = s;
+    }
+
+    /* Compare against the maintained checksums; flag where not |d| <= tau (NaN flags; R13). */
+    const double tau_col = oracle_tau(pe, bm, amax, bmax);
+    const double tau_row = oracle_tau(pe, bn, amax, bmax);
+    int64_t nfr = 0, nfc = 0, fr = -1, fc = -1;
+    for (int64_t i = 0; i < bm; ++i) {
+      d_row[i] = r_row[i] - cs_row[i];
+      if (!(fabs(d_row[i]) <= tau_row)) { if (fr < 0) fr = i; ++nfr; }
+    }
+    for (int64_t j = 0; j < bn; ++j) {
+      d_col[j] = r_col[j] - cs_col[j];
+      if (!(fabs(d_col[j]) <= tau_col)) { if (fc < 0) fc = j; ++nfc; }
+    }
+    cnt->checked += 1;
+    if (nfr == 0 && nfc == 0) continue; /* clean */
+    cnt->detected += 1;
+
+    or_event_t e;
+    e.interval = (int32_t)t;
+    e.residual_row = fr >= 0 ? d_row[fr] : 0.0;
+    e.residual_col = fc >= 0 ? d_col[fc] : 0.0;
+    if (nfr == 1 && nfc == 1) {
+      /* Locate: the single error sits at the intersection, correct it in place. */
+      if (x->subtract_mode) acc[fr + fc * bm] -= d_col[fc];
+      else acc[fr + fc * bm] = dot_upto(x, i0 + fr, j0 + fc, pe);     /* reading R4 */
+      cnt->corrected += 1;
+      e.kind = 1; e.i = i0 + fr; e.j = j0 + fc;
+    } else {
+      /* Out of the one-error model (R6): recompute the whole unit once, no re-verify. */
+      for (int64_t j = 0; j < bn; ++j)
+        for (int64_t i = 0; i < bm; ++i) acc[i + j * bm] = dot_upto(x, i0 + i, j0 + j, pe);
+      cnt->recomputed += 1;
+      e.kind = 2; e.i = i0; e.j = j0;
+    }
+    if (nev < ev_cap) ev[nev] = e;
+    ++nev;
+  }
+  free(cs_col); free(cs_row); free(r_col); free(r_row); free(d_col); free(d_row);
+  return nev;
+}
+
+static int cmp_event(const void *a, const void *b) {
+  const or_event_t *x = a, *y = b;
+  if (x->interval != y->interval) return x->interval < y->interval ? -1 : 1;
+  if (x->i != y->i) return x->i < y->i ? -1 : 1;
+  if (x->j != y->j) return x->j < y->j ? -1 : 1;
+  return 0;
+}
+
+/*
+ * ABFT DGEMM over a set of units.  units == NULL means every unit (full oracle);
+ * otherwise `units` lists (ti, tj) tile indices (2 entries per unit) and only
+ * those units are computed and stored (sampled oracle at full size).
+ *
+ * C holds C0 on entry (read only when beta != 0) and C_out on exit for the
+ * computed units.  counters[OR_NCOUNTERS] out.  events sorted by (interval, i, j).
+ * Returns 0, or -1 on bad arguments.
+ */
+int oracle_dgemm_abft_units(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
+                            const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                            double *C, int64_t ldc, int64_t BM, int64_t BN, int64_t BK, int64_t Kc,
+                            int subtract_mode, const or_fault_t *faults, int64_t nfaults,
+                            const int64_t *units, int64_t nunits, int64_t *counters,
+                            or_event_t *events, int64_t events_cap) {
+  for (int c = 0; c < OR_NCOUNTERS; ++c) counters[c] = 0;
+  if (m < 0 || n < 0 || k < 0 || BM <= 0 || BN <= 0 || BK <= 0) return -1;
+  if (Kc <= 0 || Kc > k) Kc = k;
+  if (m == 0 || n == 0) return 0;
+  /* alpha == 0 or k == 0: C = beta*C with no ABFT (BLAS semantics). */
+  if (alpha == 0.0 || k == 0) {
+    if (beta == 1.0) return 0;
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < m; ++i) C[i + j * ldc] = (beta == 0.0) ? 0.0 : beta * C[i + j * ldc];
+    return 0;
+  }
+  const int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
+  const int64_t nu = units ? nunits : tm * tn;
+  unit_ctx_t x = {is_trans(ta), is_trans(tb), k, Kc, BK, A, B, lda, ldb, subtract_mode};
+
+  int64_t det = 0, cor = 0, rec = 0, chk = 0, nev_total = 0;
+  int64_t ev_used = 0;
+
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : det, cor, rec, chk)
+  for (int64_t u = 0; u < nu; ++u) {
+    int64_t ti = units ? units[2 * u] : u % tm;
+    int64_t tj = units ? units[2 * u + 1] : u / tm;
+    int64_t i0 = ti * BM, j0 = tj * BN;
+    int64_t bm = (i0 + BM <= m) ? BM : m - i0;
+    int64_t bn = (j0 + BN <= n) ? BN : n - j0;
+    /* Faults that fall in this unit (list order preserved). */
+    or_fault_t *uf = malloc((size_t)(nfaults > 0 ? nfaults : 1) * sizeof(or_fault_t));
+    int64_t nf = 0;
+    for (int64_t e = 0; e < nfaults; ++e)
+      if (faults[e].i >= i0 && faults[e].i < i0 + bm && faults[e].j >= j0 && faults[e].j < j0 + bn)
+        uf[nf++] = faults[e];
+    double *acc = malloc((size_t)(bm * bn) * sizeof(double));
+    int64_t T = (k + Kc - 1) / Kc;
+    or_event_t *ev = malloc((size_t)T * sizeof(or_event_t));
+    unit_counts_t cnt = {0, 0, 0, 0};
+    int64_t nev = verify_unit(&x, i0, bm, j0, bn, uf, nf, acc, ev, T, &cnt);
+    det += cnt.detected; cor += cnt.corrected; rec += cnt.recomputed; chk += cnt.checked;
+
+    /* Output: C = alpha*acc + beta*C0; C0 not read when beta == 0. */
+    for (int64_t j = 0; j < bn; ++j)
+      for (int64_t i = 0; i < bm; ++i) {
+        double o = alpha * acc[i + j * bm];
+        if (beta != 0.0) o = o + beta * C[(i0 + i) + (j0 + j) * ldc];
+        C[(i0 + i) + (j0 + j) * ldc] = o;
+      }
+#pragma omp critical
+    {
+      for (int64_t e = 0; e < nev; ++e) {
+        if (ev_used < events_cap) events[ev_used++] = ev[e];
+      }
+      nev_total += nev;
+    }
+    free(uf); free(acc); free(ev);
+  }
+  if (ev_used > 1) qsort(events, (size_t)ev_used, sizeof(or_event_t), cmp_event);
+  counters[OR_UNITS_CHECKED] = chk;
+  counters[OR_DETECTED] = det;
+  counters[OR_CORRECTED] = cor;
+  counters[OR_RECOMPUTED] = rec;
+  counters[OR_N_EVENTS] = nev_total;
+  return 0;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
