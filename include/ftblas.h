@@ -1,0 +1,154 @@
+/*
+ * ftblas.h — C ABI of the B200-native online ABFT DGEMM library (libftblas.so).
+ *
+ * The operation is the paper's Level-3 hot path, FT-BLAS (arXiv 2104.00897):
+ *
+ *     C = alpha * op(A) * op(B) + beta * C          (DGEMM, §III.C.2)
+ *
+ * protected online by algorithm-based fault tolerance (ABFT):
+ *   - checksum encoding e^T A and B e                        PAPER.md:90   §II.A
+ *   - outer-product checksum maintenance (e^T A)B, A(Be)      PAPER.md:93-95 §II.A
+ *   - encoding fused into operand loads, reference checksums
+ *     fused into the kernel ("purely computational")          PAPER.md:276  §V.B
+ *   - verify e^T C / C e against the maintained checksums,
+ *     locate the single corrupted C_ij from the intersecting
+ *     row and column residuals, correct it in place           PAPER.md:258 §V.A, 445 §VI.C
+ *   - one correctable error per verification interval         PAPER.md:95  §II.A
+ *
+ * Conventions (all entry points):
+ *   - Matrices are column-major, BLAS style: element (r, c) of a matrix with leading
+ *     dimension ld is at ptr[r + c*ld].  op(A) is m x k, op(B) is k x n, C is m x n.
+ *     trans = 'N'/'n' (op(X) = X) or 'T'/'t'/'C'/'c' (op(X) = X^T; real data, so C == T).
+ *     A is m x k (lda >= max(1,m)) for 'N' and k x m (lda >= max(1,k)) otherwise;
+ *     B is k x n (ldb >= max(1,k)) for 'N' and n x k (ldb >= max(1,n)) otherwise.
+ *   - A, B, C are caller-owned DEVICE pointers on the current CUDA device (e.g. the
+ *     data_ptr() of torch float64 tensors) unless the function name ends in _host.
+ *     C must not alias A or B (BLAS rule; undefined otherwise).  The library never
+ *     frees or retains caller pointers.
+ *   - beta == 0: C is not read on input (NaN in C is ignored).  alpha == 0 or k == 0:
+ *     C = beta*C, no ABFT, no units checked.  m == 0 or n == 0: quick return.
+ *   - Work is enqueued on the calling thread's stream (ftblas_set_stream; default: the
+ *     legacy default stream 0).
+ *   - The library owns lazily allocated per-device scratch (report counters, event ring,
+ *     fault lists, host-API staging buffers); ftblas_finalize() releases it.
+ *
+ * Status codes (return value of every int function):
+ *     0  success — INCLUDING when soft errors were detected and corrected; detection is
+ *        reported through the error report, never through the status.
+ *    -p  argument p is invalid (LAPACK INFO style): 1 transA, 2 transB, 3 m, 4 n, 5 k,
+ *        7 A == NULL, 8 lda, 9 B == NULL, 10 ldb, 12 C == NULL, 13 ldc
+ *        (positions in the ftblas_dgemm argument list; NULL checks only when the
+ *        operand is read: A and B when alpha != 0 and k > 0, C when m, n > 0).
+ *     1  CUDA error (the CUDA error string is kept for ftblas_status_string(1)),
+ *     2  out of memory,  3  bad fault list (i outside [0,m), j outside [0,n), step
+ *        outside [0,k], or count < 0), 4 bad option value.
+ */
+#ifndef FTBLAS_H
+#define FTBLAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One error event (one per flagged verification unit). */
+typedef struct {
+  int64_t i, j;        /* kind 1: row/column of the corrected element (global, 0-based);
+                          kind 2: first row/column of the recomputed unit */
+  int32_t kind;        /* 1 = CORRECTED at (i, j); 2 = RECOMPUTED unit (flag pattern other
+                          than exactly one row and one column; reading R6/R13) */
+  int32_t interval;    /* verification interval index t (0 when Kc == k) */
+  double residual_row; /* d_row = (C e)_i - (A(Be))_i at the (first) flagged row, else 0 */
+  double residual_col; /* d_col = (e^T C)_j - ((e^T A)B)_j at the (first) flagged col, else 0 */
+} ftblas_event_t;
+
+/* Error report of one protected call.  Counters are totals over the call. */
+typedef struct {
+  int64_t units_checked; /* out: verification units (tile x interval) verified */
+  int64_t detected;      /* out: units with any flagged row or column */
+  int64_t corrected;     /* out: units with exactly one flagged row and column (fixed in place) */
+  int64_t recomputed;    /* out: units recomputed once (any other flag pattern) */
+  int64_t n_events;      /* out: events produced (may exceed events_capacity) */
+  int32_t unit_rows;     /* out: BM, rows per verification unit */
+  int32_t unit_cols;     /* out: BN, columns per verification unit */
+  int32_t unit_k;        /* out: Kc, k-length of a verification interval (== k today) */
+  int32_t step_quantum;  /* out: BK; an injected fault's step is applied at floor(step/BK)*BK */
+  ftblas_event_t *events;  /* in: caller-owned HOST array (may be NULL), filled with the
+                              first min(n_events, events_capacity) events sorted by
+                              (interval, i, j) */
+  int64_t events_capacity; /* in */
+} ftblas_err_report_t;
+
+/* One injected soft error: after `step` of the k rank-1 updates have been accumulated
+ * into acc(i, j) (quantised down to a multiple of step_quantum), add `delta` to it.
+ * Models PAPER.md:445 §VI.C: "An element of matrix C is randomly selected for
+ * modification when an injection point is reached." */
+typedef struct {
+  int64_t i, j, step;
+  double delta;
+} ftblas_fault_t;
+
+/* Protected DGEMM.  Stream-ordered; synchronises the stream only when err != NULL (to
+ * fill the report).  Consumes (and disarms) any faults armed on this thread. */
+int ftblas_dgemm(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                 double *C, int64_t ldc, ftblas_err_report_t *err);
+
+/* Unprotected twin (same mainloop and epilogue, no checksums): the overhead baseline.
+ * Fully asynchronous.  Armed faults are also consumed here and injected silently (the
+ * negative control: the corruption reaches C undetected). */
+int ftblas_dgemm_noft(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                      double *C, int64_t ldc);
+
+/* Same as ftblas_dgemm / ftblas_dgemm_noft but A, B, C are HOST pointers (pinned memory
+ * recommended).  Copies op inputs host->device, computes, copies C device->host and
+ * synchronises the stream before returning.  Device staging is library-owned. */
+int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                      double *C, int64_t ldc, ftblas_err_report_t *err);
+int ftblas_dgemm_noft_host(char transA, char transB, int64_t m, int64_t n, int64_t k,
+                           double alpha, const double *A, int64_t lda, const double *B,
+                           int64_t ldb, double beta, double *C, int64_t ldc);
+
+/* Fault injection (test / benchmark hook).  ftblas_inject_arm copies n faults (host
+ * array) to this thread's armed list; the next dgemm call on this thread consumes them.
+ * Validation against m, n, k happens at that call (status 3). */
+int ftblas_inject_arm(const ftblas_fault_t *faults, int64_t n);
+int ftblas_inject_disarm(void);
+
+/* Seeded fault generator: SplitMix64 (Steele, Lea, Flood 2014) seeded with `seed`; per
+ * fault draw u0..u4 in [0,1) from the top 53 bits and set i = floor(u0*m),
+ * j = floor(u1*n), step = floor(u2*k) (each clamped to the last index),
+ * |delta| = 10^(log10_lo + (log10_hi - log10_lo)*u3), sign negative iff u4 < 0.5.
+ * Writes `count` entries to the caller-owned `out`. */
+int ftblas_inject_seeded(uint64_t seed, int64_t count, int64_t m, int64_t n, int64_t k,
+                         double log10_lo, double log10_hi, ftblas_fault_t *out);
+
+/* Thread-local stream for subsequent calls (a cudaStream_t; NULL = legacy stream). */
+int ftblas_set_stream(void *cuda_stream);
+
+/* Correction mode for single errors: 0 = recompute C_ij from a fresh k-long dot product
+ * (default, reading R4), 1 = subtract the located error magnitude. */
+#define FTBLAS_CORRECT_RECOMPUTE 0
+#define FTBLAS_CORRECT_SUBTRACT 1
+int ftblas_set_correction(int mode);
+
+/* Verification-unit geometry the kernels use: BM x BN tiles, step quantum BK. */
+int ftblas_get_geometry(int32_t *unit_rows, int32_t *unit_cols, int32_t *step_quantum);
+
+/* Number of kernel launches enqueued by this thread since the last call (for the
+ * benchmark's launch accounting); resets the counter. */
+int64_t ftblas_take_launch_count(void);
+
+const char *ftblas_status_string(int status);
+
+/* Free per-device scratch on every device touched.  Not safe while calls are in flight. */
+int ftblas_finalize(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FTBLAS_H */

@@ -1,0 +1,384 @@
+// ftblas.cu — host side of libftblas.so: the C ABI declared in include/ftblas.h.
+//
+// Argument checking (BLAS INFO convention), quick returns, fault bucketing, kernel
+// dispatch over (transA, transB, FT, 16-byte vector path), the error-report path and the
+// seeded fault generator.  All arithmetic of the method runs in the kernels of
+// dgemm_abft.cuh; this file only marshals.
+#include "../../include/ftblas.h"
+#include "dgemm_abft.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local cudaStream_t tl_stream = nullptr;
+thread_local std::vector<ftblas_fault_t> tl_armed;
+thread_local bool tl_have_armed = false;
+thread_local int tl_correct = FTBLAS_CORRECT_RECOMPUTE;
+thread_local int64_t tl_launches = 0;
+thread_local std::string tl_cuda_error;
+
+std::mutex g_init_mu;
+bool g_init_done[64] = {false};
+
+int cuda_fail(cudaError_t e) {
+  tl_cuda_error = cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? 2 : 1;
+}
+#define CUDA_TRY(x)                          \
+  do {                                       \
+    cudaError_t e_ = (x);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_); \
+  } while (0)
+
+bool is_n(char c) { return c == 'N' || c == 'n'; }
+bool is_t(char c) { return c == 'T' || c == 't' || c == 'C' || c == 'c'; }
+
+template <bool AKM, bool BKM, bool FT, bool V16>
+int launch_one(const ftk::Params &p, dim3 grid, cudaStream_t st) {
+  auto kfn = ftk::dgemm_abft_kernel<AKM, BKM, FT, V16>;
+  static bool attr_set[64] = {false};  // per instantiation and device
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ftk::SMEM_BYTES));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  kfn<<<grid, ftk::NTHREADS, ftk::SMEM_BYTES, st>>>(p);
+  ++tl_launches;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <bool FT>
+int dispatch(bool akm, bool bkm, bool v16, const ftk::Params &p, dim3 grid, cudaStream_t st) {
+  if (v16) {
+    if (akm) return bkm ? launch_one<true, true, FT, true>(p, grid, st) : launch_one<true, false, FT, true>(p, grid, st);
+    return bkm ? launch_one<false, true, FT, true>(p, grid, st) : launch_one<false, false, FT, true>(p, grid, st);
+  }
+  if (akm) return bkm ? launch_one<true, true, FT, false>(p, grid, st) : launch_one<true, false, FT, false>(p, grid, st);
+  return bkm ? launch_one<false, true, FT, false>(p, grid, st) : launch_one<false, false, FT, false>(p, grid, st);
+}
+
+int ensure_device_init() {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (dev >= 0 && dev < 64 && !g_init_done[dev]) {
+    // Keep stream-ordered scratch cached in the device's default pool.
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_init_done[dev] = true;
+  }
+  return 0;
+}
+
+int check_args(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A,
+               int64_t lda, const double *B, int64_t ldb, const double *C, int64_t ldc) {
+  if (!is_n(ta) && !is_t(ta)) return -1;
+  if (!is_n(tb) && !is_t(tb)) return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  const int64_t nrowa = is_n(ta) ? m : k, nrowb = is_n(tb) ? k : n;
+  const bool reads_ab = alpha != 0.0 && k > 0 && m > 0 && n > 0;
+  if (reads_ab && A == nullptr) return -7;
+  if (lda < std::max<int64_t>(1, nrowa)) return -8;
+  if (reads_ab && B == nullptr) return -9;
+  if (ldb < std::max<int64_t>(1, nrowb)) return -10;
+  if (m > 0 && n > 0 && C == nullptr) return -12;
+  if (ldc < std::max<int64_t>(1, m)) return -13;
+  // Index arithmetic inside the kernels uses int for tile coordinates.
+  if ((m + ftk::BM - 1) / ftk::BM > 0x7fffffff) return -3;
+  if ((n + ftk::BN - 1) / ftk::BN > 65535) return -4;
+  return 0;
+}
+
+void fill_geometry(ftblas_err_report_t *err, int64_t k) {
+  err->unit_rows = ftk::BM;
+  err->unit_cols = ftk::BN;
+  err->unit_k = (int32_t)std::min<int64_t>(k, INT32_MAX);
+  err->step_quantum = ftk::BK;
+}
+
+void zero_report(ftblas_err_report_t *err, int64_t k) {
+  if (!err) return;
+  err->units_checked = err->detected = err->corrected = err->recomputed = err->n_events = 0;
+  fill_geometry(err, k);
+}
+
+// The core entry: device pointers, protected (FT) or not.
+int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
+               const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+               int64_t ldc, ftblas_err_report_t *err) {
+  std::vector<ftblas_fault_t> faults;
+  if (tl_have_armed) { faults.swap(tl_armed); tl_have_armed = false; }
+  const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
+  if (rc) return rc;
+  zero_report(err, k);
+  if (m == 0 || n == 0) return 0;
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  if (alpha == 0.0 || k == 0) {
+    if (beta == 1.0) return 0;
+    const int64_t total = m * n;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    ftk::scale_kernel<<<blocks, 256, 0, st>>>(m, n, beta, C, ldc);
+    ++tl_launches;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  for (const auto &f : faults)
+    if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step > k) return 3;
+
+  ftk::Params p{};
+  p.m = m; p.n = n; p.k = k; p.alpha = alpha; p.beta = beta;
+  p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
+  p.tiles_m = (int)((m + ftk::BM - 1) / ftk::BM);
+  p.tiles_n = (int)((n + ftk::BN - 1) / ftk::BN);
+  p.nk = (int)((k + ftk::BK - 1) / ftk::BK);
+  p.correct_mode = tl_correct;
+
+  // Bucket faults by (tile, stage); stable so same-stage faults keep the caller's order.
+  std::vector<ftk::FaultDev> fd;
+  fd.reserve(faults.size());
+  for (const auto &f : faults) {
+    const int64_t ti = f.i / ftk::BM, tj = f.j / ftk::BN;
+    fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m), (int32_t)(f.step / ftk::BK),
+                               (int32_t)(f.i - ti * ftk::BM), (int32_t)(f.j - tj * ftk::BN), f.delta});
+  }
+  std::stable_sort(fd.begin(), fd.end(), [](const ftk::FaultDev &a, const ftk::FaultDev &b) {
+    return a.tile != b.tile ? a.tile < b.tile : a.stage < b.stage;
+  });
+
+  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
+  const size_t cnt_bytes = sizeof(unsigned long long) * ftk::CNT_N;
+  const size_t ev_bytes = sizeof(ftk::EventDev) * (size_t)ev_cap;
+  const size_t f_bytes = sizeof(ftk::FaultDev) * fd.size();
+  char *scratch = nullptr;
+  CUDA_TRY(cudaMallocAsync((void **)&scratch, cnt_bytes + ev_bytes + f_bytes + 64, st));
+  p.counters = reinterpret_cast<unsigned long long *>(scratch);
+  p.events = reinterpret_cast<ftk::EventDev *>(scratch + cnt_bytes);
+  p.ev_cap = ev_cap;
+  p.faults = fd.empty() ? nullptr : reinterpret_cast<const ftk::FaultDev *>(scratch + cnt_bytes + ev_bytes);
+  p.nfaults = (int)fd.size();
+  CUDA_TRY(cudaMemsetAsync(scratch, 0, cnt_bytes, st));
+  if (!fd.empty())  // pageable source: the call returns once the source has been staged
+    CUDA_TRY(cudaMemcpyAsync(scratch + cnt_bytes + ev_bytes, fd.data(), f_bytes, cudaMemcpyHostToDevice, st));
+
+  const bool akm = is_t(ta), bkm = is_n(tb);
+  const bool v16 = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+                   (lda % 2) == 0 && (ldb % 2) == 0;
+  const dim3 grid(p.tiles_m, p.tiles_n);
+  int lrc = ft ? dispatch<true>(akm, bkm, v16, p, grid, st) : dispatch<false>(akm, bkm, v16, p, grid, st);
+  if (lrc) { cudaFreeAsync(scratch, st); return lrc; }
+
+  if (err) {
+    unsigned long long cnt[ftk::CNT_N];
+    CUDA_TRY(cudaMemcpyAsync(cnt, p.counters, cnt_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t nev = (int64_t)cnt[ftk::CNT_EVENTS];
+    const int64_t nstore = std::min<int64_t>(nev, ev_cap);
+    std::vector<ftk::EventDev> ev((size_t)nstore);
+    if (nstore > 0) {
+      CUDA_TRY(cudaMemcpyAsync(ev.data(), p.events, sizeof(ftk::EventDev) * nstore, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    std::sort(ev.begin(), ev.end(), [](const ftk::EventDev &a, const ftk::EventDev &b) {
+      if (a.interval != b.interval) return a.interval < b.interval;
+      if (a.i != b.i) return a.i < b.i;
+      return a.j < b.j;
+    });
+    err->units_checked = ft ? (int64_t)p.tiles_m * p.tiles_n : 0;
+    err->detected = (int64_t)cnt[ftk::CNT_DETECTED];
+    err->corrected = (int64_t)cnt[ftk::CNT_CORRECTED];
+    err->recomputed = (int64_t)cnt[ftk::CNT_RECOMPUTED];
+    err->n_events = nev;
+    if (err->events && err->events_capacity > 0) {
+      const int64_t ncopy = std::min<int64_t>(nstore, err->events_capacity);
+      for (int64_t e = 0; e < ncopy; ++e) {
+        err->events[e].i = ev[e].i;
+        err->events[e].j = ev[e].j;
+        err->events[e].kind = ev[e].kind;
+        err->events[e].interval = ev[e].interval;
+        err->events[e].residual_row = ev[e].residual_row;
+        err->events[e].residual_col = ev[e].residual_col;
+      }
+    }
+  }
+  CUDA_TRY(cudaFreeAsync(scratch, st));
+  return 0;
+}
+
+// Host-buffer variant: stage op inputs into stream-ordered device buffers.
+int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
+                    const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                    double *C, int64_t ldc, ftblas_err_report_t *err) {
+  const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
+  if (rc) {
+    if (tl_have_armed) { tl_armed.clear(); tl_have_armed = false; }
+    return rc;
+  }
+  if (m == 0 || n == 0) {
+    if (tl_have_armed) { tl_armed.clear(); tl_have_armed = false; }
+    zero_report(err, k);
+    return 0;
+  }
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  const bool reads_ab = alpha != 0.0 && k > 0;
+  const int64_t ar = is_n(ta) ? m : k, ac = is_n(ta) ? k : m;
+  const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
+  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+  if (reads_ab) {
+    CUDA_TRY(cudaMallocAsync((void **)&dA, sizeof(double) * ar * ac, st));
+    CUDA_TRY(cudaMallocAsync((void **)&dB, sizeof(double) * br * bc, st));
+    CUDA_TRY(cudaMemcpy2DAsync(dA, sizeof(double) * ar, A, sizeof(double) * lda, sizeof(double) * ar, ac,
+                               cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync(dB, sizeof(double) * br, B, sizeof(double) * ldb, sizeof(double) * br, bc,
+                               cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(cudaMallocAsync((void **)&dC, sizeof(double) * m * n, st));
+  if (beta != 0.0)
+    CUDA_TRY(cudaMemcpy2DAsync(dC, sizeof(double) * m, C, sizeof(double) * ldc, sizeof(double) * m, n,
+                               cudaMemcpyHostToDevice, st));
+  int r = dgemm_impl(ft, ta, tb, m, n, k, alpha, reads_ab ? dA : nullptr, reads_ab ? std::max<int64_t>(ar, 1) : lda,
+                     reads_ab ? dB : nullptr, reads_ab ? std::max<int64_t>(br, 1) : ldb, beta, dC, m, err);
+  if (r == 0 && !(reads_ab == false && beta == 1.0))
+    r = (cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
+                           cudaMemcpyDeviceToHost, st) == cudaSuccess) ? 0 : 1;
+  if (dA) cudaFreeAsync(dA, st);
+  if (dB) cudaFreeAsync(dB, st);
+  cudaFreeAsync(dC, st);
+  const cudaError_t se = cudaStreamSynchronize(st);
+  if (r == 0 && se != cudaSuccess) return cuda_fail(se);
+  return r;
+}
+
+uint64_t splitmix_next(uint64_t &state) {
+  state += 0x9E3779B97F4A7C15ull;
+  uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+double splitmix_uniform(uint64_t &state) { return (double)(splitmix_next(state) >> 11) * 0x1p-53; }
+
+}  // namespace
+
+extern "C" {
+
+int ftblas_dgemm(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                 int64_t ldc, ftblas_err_report_t *err) {
+  return dgemm_impl(true, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err);
+}
+
+int ftblas_dgemm_noft(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                      double *C, int64_t ldc) {
+  return dgemm_impl(false, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, nullptr);
+}
+
+int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                      double *C, int64_t ldc, ftblas_err_report_t *err) {
+  return dgemm_host_impl(true, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err);
+}
+
+int ftblas_dgemm_noft_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                           const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                           double *C, int64_t ldc) {
+  return dgemm_host_impl(false, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, nullptr);
+}
+
+int ftblas_inject_arm(const ftblas_fault_t *faults, int64_t n) {
+  if (n < 0 || (n > 0 && faults == nullptr)) return 3;
+  tl_armed.assign(faults, faults + n);
+  tl_have_armed = true;
+  return 0;
+}
+
+int ftblas_inject_disarm(void) {
+  tl_armed.clear();
+  tl_have_armed = false;
+  return 0;
+}
+
+int ftblas_inject_seeded(uint64_t seed, int64_t count, int64_t m, int64_t n, int64_t k,
+                         double log10_lo, double log10_hi, ftblas_fault_t *out) {
+  if (count < 0 || m <= 0 || n <= 0 || k < 0 || (count > 0 && out == nullptr)) return 3;
+  uint64_t st = seed;
+  for (int64_t e = 0; e < count; ++e) {
+    double u[5];
+    for (int q = 0; q < 5; ++q) u[q] = splitmix_uniform(st);
+    out[e].i = std::min<int64_t>((int64_t)std::floor(u[0] * (double)m), m - 1);
+    out[e].j = std::min<int64_t>((int64_t)std::floor(u[1] * (double)n), n - 1);
+    out[e].step = std::min<int64_t>((int64_t)std::floor(u[2] * (double)k), std::max<int64_t>(k - 1, 0));
+    const double mag = std::pow(10.0, log10_lo + (log10_hi - log10_lo) * u[3]);
+    out[e].delta = u[4] < 0.5 ? -mag : mag;
+  }
+  return 0;
+}
+
+int ftblas_set_stream(void *cuda_stream) {
+  tl_stream = static_cast<cudaStream_t>(cuda_stream);
+  return 0;
+}
+
+int ftblas_set_correction(int mode) {
+  if (mode != FTBLAS_CORRECT_RECOMPUTE && mode != FTBLAS_CORRECT_SUBTRACT) return 4;
+  tl_correct = mode;
+  return 0;
+}
+
+int ftblas_get_geometry(int32_t *unit_rows, int32_t *unit_cols, int32_t *step_quantum) {
+  if (unit_rows) *unit_rows = ftk::BM;
+  if (unit_cols) *unit_cols = ftk::BN;
+  if (step_quantum) *step_quantum = ftk::BK;
+  return 0;
+}
+
+int64_t ftblas_take_launch_count(void) {
+  const int64_t v = tl_launches;
+  tl_launches = 0;
+  return v;
+}
+
+const char *ftblas_status_string(int status) {
+  if (status < 0) {
+    static thread_local char buf[64];
+    std::snprintf(buf, sizeof buf, "invalid argument %d", -status);
+    return buf;
+  }
+  switch (status) {
+    case 0: return "success";
+    case 1: return tl_cuda_error.empty() ? "CUDA error" : tl_cuda_error.c_str();
+    case 2: return "out of device memory";
+    case 3: return "bad fault list";
+    case 4: return "bad option value";
+    default: return "unknown status";
+  }
+}
+
+int ftblas_finalize(void) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  for (int d = 0; d < ndev && d < 64; ++d) {
+    if (!g_init_done[d]) continue;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+"""Thin Python binding of libftblas.so (include/ftblas.h) — argument marshalling only.
+
+Every step of the ABFT DGEMM runs in the library's CUDA kernels; this module only
+converts Python/torch arguments to the C ABI.  It raises loudly when the native
+library is missing: there is no CPU fallback.
+
+Function names mirror the C ABI (``ftblas_dgemm``, ``ftblas_dgemm_noft``,
+``ftblas_inject_arm`` ...).  Matrix arguments are device pointers: pass a torch
+float64 CUDA tensor (its data_ptr() is used) or an int address.  Matrices are
+column-major with explicit leading dimensions, exactly as in BLAS.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libftblas.so")
+
+
+class FtblasError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn} returned {status}: {msg}")
+        self.status = status
+
+
+class Event(ctypes.Structure):
+    _fields_ = [("i", ctypes.c_int64), ("j", ctypes.c_int64), ("kind", ctypes.c_int32),
+                ("interval", ctypes.c_int32), ("residual_row", ctypes.c_double),
+                ("residual_col", ctypes.c_double)]
+
+
+class ErrReport(ctypes.Structure):
+    _fields_ = [("units_checked", ctypes.c_int64), ("detected", ctypes.c_int64),
+                ("corrected", ctypes.c_int64), ("recomputed", ctypes.c_int64),
+                ("n_events", ctypes.c_int64), ("unit_rows", ctypes.c_int32),
+                ("unit_cols", ctypes.c_int32), ("unit_k", ctypes.c_int32),
+                ("step_quantum", ctypes.c_int32), ("events", ctypes.POINTER(Event)),
+                ("events_capacity", ctypes.c_int64)]
+
+
+class Fault(ctypes.Structure):
+    _fields_ = [("i", ctypes.c_int64), ("j", ctypes.c_int64), ("step", ctypes.c_int64),
+                ("delta", ctypes.c_double)]
+
+
+@dataclass
+class Report:
+    units_checked: int
+    detected: int
+    corrected: int
+    recomputed: int
+    n_events: int
+    unit_rows: int
+    unit_cols: int
+    unit_k: int
+    step_quantum: int
+    events: list = field(default_factory=list)  # (interval, i, j, kind, residual_row, residual_col)
+
+
+_lib = None
+
+
+def load():
+    """Load libftblas.so (built by paper_2104_00897_b200.build); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    c, i64, d, P, i32 = ctypes.c_char, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
+    gemm = [c, c, i64, i64, i64, d, P, i64, P, i64, d, P, i64]
+    L.ftblas_dgemm.argtypes = gemm + [ctypes.POINTER(ErrReport)]
+    L.ftblas_dgemm_noft.argtypes = gemm
+    L.ftblas_dgemm_host.argtypes = gemm + [ctypes.POINTER(ErrReport)]
+    L.ftblas_dgemm_noft_host.argtypes = gemm
+    L.ftblas_inject_arm.argtypes = [ctypes.POINTER(Fault), i64]
+    L.ftblas_inject_disarm.argtypes = []
+    L.ftblas_inject_seeded.argtypes = [ctypes.c_uint64, i64, i64, i64, i64, d, d,
+                                       ctypes.POINTER(Fault)]
+    L.ftblas_set_stream.argtypes = [P]
+    L.ftblas_set_correction.argtypes = [i32]
+    L.ftblas_get_geometry.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 3
+    L.ftblas_take_launch_count.restype = i64
+    L.ftblas_take_launch_count.argtypes = []
+    L.ftblas_status_string.restype = ctypes.c_char_p
+    L.ftblas_status_string.argtypes = [i32]
+    L.ftblas_finalize.argtypes = []
+    for fn in ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
+               "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
+               "ftblas_set_stream", "ftblas_set_correction", "ftblas_get_geometry",
+               "ftblas_finalize"):
+        getattr(L, fn).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
+            "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
+            "ftblas_set_stream", "ftblas_set_correction", "ftblas_get_geometry",
+            "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize")
+
+
+def _check(fn, status):
+    if status != 0:
+        raise FtblasError(fn, status, load().ftblas_status_string(status).decode())
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):  # torch tensor
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):  # numpy array
+        return x.ctypes.data
+    raise TypeError(type(x))
+
+
+def _c(t: str) -> bytes:
+    return t.encode() if isinstance(t, str) else t
+
+
+def _report(r: ErrReport, evbuf) -> Report:
+    n = min(r.n_events, r.events_capacity)
+    ev = [(evbuf[e].interval, evbuf[e].i, evbuf[e].j, evbuf[e].kind, evbuf[e].residual_row,
+           evbuf[e].residual_col) for e in range(n)]
+    return Report(r.units_checked, r.detected, r.corrected, r.recomputed, r.n_events, r.unit_rows,
+                  r.unit_cols, r.unit_k, r.step_quantum, ev)
+
+
+def ftblas_dgemm(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *, report=True,
+                 events_capacity=4096, raw_status=False):
+    """Protected DGEMM on device pointers.  Returns a Report (synchronises the stream) or,
+    with report=False, None (asynchronous)."""
+    L = load()
+    if report:
+        evbuf = (Event * max(events_capacity, 1))()
+        r = ErrReport()
+        r.events = evbuf
+        r.events_capacity = events_capacity
+        st = L.ftblas_dgemm(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb,
+                            beta, _ptr(C), ldc, ctypes.byref(r))
+    else:
+        st = L.ftblas_dgemm(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb,
+                            beta, _ptr(C), ldc, None)
+    if raw_status:
+        return st
+    _check("ftblas_dgemm", st)
+    return _report(r, evbuf) if report else None
+
+
+def ftblas_dgemm_noft(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *,
+                      raw_status=False):
+    st = load().ftblas_dgemm_noft(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B),
+                                  ldb, beta, _ptr(C), ldc)
+    if raw_status:
+        return st
+    _check("ftblas_dgemm_noft", st)
+
+
+def ftblas_dgemm_host(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *,
+                      report=True, events_capacity=4096):
+    """Protected DGEMM on HOST buffers (numpy arrays / host addresses); C updated in place."""
+    L = load()
+    evbuf = (Event * max(events_capacity, 1))()
+    r = ErrReport()
+    r.events = evbuf
+    r.events_capacity = events_capacity
+    st = L.ftblas_dgemm_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb,
+                             beta, _ptr(C), ldc, ctypes.byref(r) if report else None)
+    _check("ftblas_dgemm_host", st)
+    return _report(r, evbuf) if report else None
+
+
+def ftblas_dgemm_noft_host(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc):
+    st = load().ftblas_dgemm_noft_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda,
+                                       _ptr(B), ldb, beta, _ptr(C), ldc)
+    _check("ftblas_dgemm_noft_host", st)
+
+
+def ftblas_inject_arm(faults):
+    faults = list(faults)
+    arr = (Fault * max(len(faults), 1))()
+    for e, (i, j, s, d) in enumerate(faults):
+        arr[e] = Fault(int(i), int(j), int(s), float(d))
+    _check("ftblas_inject_arm", load().ftblas_inject_arm(arr, len(faults)))
+
+
+def ftblas_inject_disarm():
+    _check("ftblas_inject_disarm", load().ftblas_inject_disarm())
+
+
+def ftblas_inject_seeded(seed, count, m, n, k, log10_lo, log10_hi):
+    arr = (Fault * max(count, 1))()
+    _check("ftblas_inject_seeded",
+           load().ftblas_inject_seeded(seed, count, m, n, k, log10_lo, log10_hi, arr))
+    return [(arr[e].i, arr[e].j, arr[e].step, arr[e].delta) for e in range(count)]
+
+
+def ftblas_set_stream(stream):
+    """stream: torch.cuda.Stream, raw cudaStream_t int, or None (legacy default stream)."""
+    h = None if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    _check("ftblas_set_stream", load().ftblas_set_stream(h))
+
+
+def ftblas_set_correction(mode: int):
+    _check("ftblas_set_correction", load().ftblas_set_correction(mode))
+
+
+def ftblas_get_geometry():
+    a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check("ftblas_get_geometry", load().ftblas_get_geometry(ctypes.byref(a), ctypes.byref(b),
+                                                            ctypes.byref(c)))
+    return a.value, b.value, c.value
+
+
+def ftblas_take_launch_count() -> int:
+    return int(load().ftblas_take_launch_count())
+
+
+def ftblas_status_string(status: int) -> str:
+    return load().ftblas_status_string(status).decode()
+
+
+def ftblas_finalize():
+    _check("ftblas_finalize", load().ftblas_finalize())
+
+
+CORRECT_RECOMPUTE = 0
+CORRECT_SUBTRACT = 1
