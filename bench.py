@@ -146,13 +146,16 @@ def oracle_sample(W, rank_rows, seed, units_wanted, torch, A_dev, B_dev, lda, ld
         u = (i // BM, j // BN)
         if u not in units:
             units.append(u)
+    units = units[:16]
     rng = np.random.default_rng(seed)
     tm, tn = -(-m // BM), -(-n // BN)
-    while len(units) < units_wanted:
-        u = (int(rng.integers(0, tm)), int(rng.integers(0, tn)))
-        if u not in units:
-            units.append(u)
-    units = units[:units_wanted]
+    # Extra units are drawn from the same tile rows/columns (bounded host copies), topped up
+    # with seeded random tile rows/columns when there are too few faults.
+    rset = sorted({u[0] for u in units} | {int(x) for x in rng.integers(0, tm, max(0, 4 - len(units)))})
+    cset = sorted({u[1] for u in units} | {int(x) for x in rng.integers(0, tn, max(0, 4 - len(units)))})
+    cand = [(a, b) for a in rset for b in cset if (a, b) not in units]
+    rng.shuffle(cand)
+    units += cand[:max(0, units_wanted - len(units))]
     # Host copies of just the rows / columns the sampled units read (column-major, 'N').
     rows = sorted({ti for ti, _ in units})
     cols = sorted({tj for _, tj in units})

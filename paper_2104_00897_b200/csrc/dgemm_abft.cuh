@@ -1,44 +1,51 @@
-// dgemm_abft.cuh — sm_100a kernels of the online ABFT DGEMM (FT-BLAS, arXiv 2104.00897).
+// dgemm_abft.cuh — sm_100a kernel of the online ABFT DGEMM (FT-BLAS, arXiv 2104.00897).
 //
-// One CTA computes one BM x BN tile of C = alpha*op(A)*op(B) + beta*C and is one
-// verification unit (§II.A restricted to the tile; R5):
+// One CTA computes one BM x BN = 128 x 128 tile of C = alpha*op(A)*op(B) + beta*C; the tile
+// is one verification unit (§II.A restricted to the tile; R5).
 //
-//   mainloop  (per BK-deep stage s, 256 threads = 8 MMA warps in a 2 x 4 grid of 64x32
-//              warp tiles; cp.async multistage ring in shared memory)
-//     - operand staging: every element of the A/B tiles is loaded from global memory
-//       ONCE into shared memory and reused by the MMA, by the checksum encode and by
-//       the checksum carry ("each B element reused three times", §V.B)
-//     - encode(s):  a_sum[p] = sum_{i in I} op(A)_ip   (e^T A)
-//                   b_sum[p] = sum_{j in J} op(B)_pj   (B e)
-//                   running max|op(A)_I|, max|op(B)_J| for the threshold (R1)
-//     - carry(s-1): cs_col[j] += a_sum[p]*op(B)_pj,  cs_row[i] += op(A)_ip*b_sum[p]
-//                   (outer-product checksum maintenance), one stage behind
-//                   the encode so that a single barrier per stage suffices
-//     - fault hook: injected deltas land in the owning accumulator at stage boundaries
-//     - update:     acc += A_tile * B_tile with DMMA.8x8x4 (mma.sync m8n8k4 f64), the only
-//                   FP64 tensor instruction sm_100a provides (tcgen05 has no f64 kind)
-//   epilogue
-//     - stage acc through shared memory; reference checksums r_col = e^T C_IJ and
-//       r_row = C_IJ e reuse the computed C ("reuse the computed C elements ... to update
-//       the reference checksums")
-//     - residuals d = r - cs, flag where not |d| <= tau, classify with block counts:
-//       exactly one row and one column -> locate and correct in place;
-//       any other pattern -> recompute the tile once (R6)
-//     - C = alpha*acc + beta*C0 (C0 not read when beta == 0), coalesced column stores
+// Warp-specialised (384 threads = 3 warpgroups):
+//   warpgroup 0  (warps 0-3, 152 registers): "checksum warps".  Warp 0 lane 0 is also the
+//                TMA producer: it streams the BK = 16 deep A and B tiles of every stage into
+//                a 5-deep shared-memory ring (cp.async.bulk.tensor, 128-byte swizzle,
+//                mbarrier complete_tx).  In the protected kernel each checksum warp c owns
+//                k-slots p = 4c..4c+3 of every stage and, from the SAME staged tiles the MMA
+//                reads ("each B element reused three times", §V.B):
+//                  encode  a_sum[p] = sum_{i in I} op(A)_ip,  b_sum[p] = sum_{j in J} op(B)_pj
+//                          (e^T A, B e) and the running max|op(A)_I|, max|op(B)_J|
+//                  carry   cs_col[j] += a_sum[p] op(B)_pj,  cs_row[i] += op(A)_ip b_sum[p]
+//                          (outer-product maintenance)
+//   warpgroups 1-2 (warps 4-11, 176 registers): 8 MMA warps in a 2 x 4 grid of 64 x 32 warp
+//                tiles; acc += A_tile*B_tile with DMMA.8x8x4 (mma.sync m8n8k4 f64 — the only
+//                FP64 tensor instruction of sm_100a; tcgen05 has no f64 kind).  They also host
+//                the fault-injection hook (a delta added to the owning accumulator when the
+//                k-loop reaches the fault's quantised step).
+//   Every consumer warp waits on the stage's full barrier and arrives on its empty barrier:
+//   no CTA-wide barrier inside the k-loop, so warps drift and hide each other's latency.
+//
+// Epilogue (all warps): stage the accumulator through shared memory; reference checksums
+// r_col = e^T C_IJ, r_row = C_IJ e from the computed C; residuals
+// d = r - cs; flag where not |d| <= tau (R1); exactly one flagged row and column
+// -> locate and correct in place; any other pattern -> recompute the
+// tile once (R6).  Store C = alpha*acc + beta*C0 (C0 not read when beta == 0).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace ftk {
 
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int STAGES = 5;               // shared-memory ring depth
-constexpr int LOOKAHEAD = STAGES - 2;   // stages in flight (carry lags the encode by one)
-constexpr int NTHREADS = 256;           // 8 MMA warps
-constexpr int LD_MN = 130;              // MN-major tile pitch (doubles): conflict-free LDS.128
-constexpr int TILE_ELEMS = BK * LD_MN;  // >= 128*BK (K-major tile, dense + XOR swizzle)
+constexpr int BM = 128, BN = 128, BK = 16;  // MMA tile (C^f tile) and k-stage depth
+constexpr int DM = 127;                     // data rows/cols per tile; row/col DM is the checksum
+constexpr int TM = DM, TN = DM;             // verification unit (tile stride in C)
+constexpr int STAGES = 5;                 // shared-memory ring depth
+constexpr int NTHREADS = 384;             // 12 warps
+constexpr int N_CS_WARPS = 4;             // checksum warps (warpgroup 0)
+constexpr int N_MMA_WARPS = 8;            // MMA warps (warpgroups 1-2)
+constexpr int TILE_ELEMS = 128 * BK;      // one operand tile: 16 KB
 constexpr int STAGE_ELEMS = 2 * TILE_ELEMS;
-constexpr int LDC_S = 129;              // epilogue C-tile pitch (doubles)
+constexpr int STAGE_BYTES = STAGE_ELEMS * 8;
+constexpr int LDC_S = 129;                // epilogue C-tile pitch (doubles)
+constexpr int REG_CS = 152, REG_MMA = 176; // setmaxnreg split: 128*152 + 256*176 = 384*168
 static_assert(BM * LDC_S <= STAGES * STAGE_ELEMS, "C tile must fit in the stage ring");
 
 struct FaultDev {        // one armed fault, sorted by (tile, stage)
@@ -68,6 +75,7 @@ struct Params {
   const FaultDev *faults;
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
+  unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
   unsigned long long *counters;   // [CNT_N]
   EventDev *events;
   long long ev_cap;
@@ -79,105 +87,88 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
-
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
-// 16-byte async copy, zero-filling bytes beyond src_bytes (0, 8 or 16).
-__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
-               "r"(src_bytes));
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-// 8-byte async copy, zero-fill when src_bytes == 0.
-__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
-               "r"(src_bytes));
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load_2d(void *sdst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// |x| as ordered bits; NaN contributes 0 (the oracle's fabs(a) > amax ignores NaN too).
-__device__ __forceinline__ unsigned long long absbits(double x) {
-  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
-  return b <= 0x7FF0000000000000ull ? b : 0ull;
-}
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
-  return a > b ? a : b;
-}
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N)); }
 
 // ------------------------------------------------------------------ shared-memory layouts
-// An operand tile X holds the 128 x BK block X(x, p), x the M (or N) index, p the K index.
-//  MN-major (x contiguous in global memory: op(A) with 'N', op(B) with 'T'):
-//     X(x,p) at [p*LD_MN + x]; LD_MN = 130 makes the fragment LDS.128 conflict-free.
-//  K-major  (p contiguous in global memory: op(A) with 'T', op(B) with 'N'):
-//     X(x,p) at [x*16 + 2*((p/2) ^ ((x&1)<<2)) + (p&1)]: dense 128-byte rows, 16-byte
-//     chunks XOR-swizzled by row parity so the fragment LDS.128 is conflict-free.
+// Operand tile X(x, p): x the M (or N) index in [0,128), p the k index in [0,16).  Both are
+// written by TMA with the 128-byte swizzle (16-byte chunk c of a 128-byte row r lands at
+// chunk c ^ (r & 7)); buffers are 1024-byte aligned.
+//  K-major (p contiguous in global: op(A) 'T', op(B) 'N'): one box {16 p, 128 x};
+//     row x holds X(x, 0..15).
+//  MN-major (x contiguous: op(A) 'N', op(B) 'T'): eight boxes {16 x, 16 p}, one per x-block
+//     xb = x/16 (2 KB each); row p of block xb holds X(16xb .. 16xb+15, p).
 template <bool KM>
 __device__ __forceinline__ int sidx(int x, int p) {
-  if (KM) return x * 16 + ((((p >> 1) ^ ((x & 1) << 2))) << 1) + (p & 1);
-  return p * LD_MN + x;
+  if (KM) return x * 16 + (((p >> 1) ^ (x & 7)) << 1) + (p & 1);
+  return (x >> 4) * 256 + p * 16 + ((((x & 15) >> 1) ^ (p & 7)) << 1) + (x & 1);
 }
 
-// Asynchronously load the X tile for rows [x0, x0+128) and k in [k0, k0+BK).
-// Global element (x, p) is g[(x0+x) + (k0+p)*ld] (MN-major) or g[(k0+p) + (x0+x)*ld]
-// (K-major).  Out-of-range elements are zero-filled (zeros contribute exactly nothing to
-// the product, the checksums or the maxima; R14).
-template <bool KM, bool V16>
-__device__ __forceinline__ void load_tile(double *s, const double *g, int64_t ld, int64_t x0,
-                                          int64_t xlim, int64_t k0, int64_t k, int tid) {
-  if (V16) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int c = tid + NTHREADS * r;  // 1024 16-byte chunks per tile
-      int x, p;
-      if (KM) { x = c >> 3; p = (c & 7) * 2; }
-      else    { p = c >> 6; x = (c & 63) * 2; }
-      const int64_t gx = x0 + x, gp = k0 + p;
-      int nval;
-      const double *src;
-      if (KM) {
-        nval = (gx < xlim) ? (int)min64(max64(k - gp, 0), 2) : 0;
-        src = g + gp + gx * ld;
-      } else {
-        nval = (gp < k) ? (int)min64(max64(xlim - gx, 0), 2) : 0;
-        src = g + gx + gp * ld;
-      }
-      cp_async16(s + sidx<KM>(x, p), nval ? src : g, nval * 8);
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int c = tid + NTHREADS * r;  // 2048 elements per tile
-      int x, p;
-      if (KM) { x = c >> 4; p = c & 15; }
-      else    { p = c >> 7; x = c & 127; }
-      const int64_t gx = x0 + x, gp = k0 + p;
-      const bool ok = gx < xlim && gp < k;
-      const double *src = KM ? g + gp + gx * ld : g + gx + gp * ld;
-      cp_async8(s + sidx<KM>(x, p), ok ? src : g, ok ? 8 : 0);
-    }
-  }
+// MMA fragment rows.  k-slot mapping in a stage: k-step s (0..3), lane slot t (0..3) <-> p =
+// 8*(s>>1) + 2t + (s&1) for both operands.  Row of m/n-tile r for fragment index g:
+//   K-major : 8r + ((g&1)<<2) + (g>>1)   (rows of lanes g, g+1 differ by 4 -> swizzle
+//             chunks in complementary halves: conflict-free LDS.128)
+//   MN-major: 16(r>>1) + 2g + (r&1)      (one LDS.128 feeds the tile pair 2q, 2q+1)
+template <bool KM>
+__device__ __forceinline__ int tile_row(int r, int g) {
+  return KM ? 8 * r + ((g & 1) << 2) + (g >> 1) : 16 * (r >> 1) + 2 * g + (r & 1);
 }
 
-// ------------------------------------------------------------------ register fragments
-// k-slot mapping inside a BK=16 stage: k-step s (0..3), lane slot t (0..3) <-> p =
-// 8*(s>>1) + 2t + (s&1).  Both operands use it, so the MMA sums the same p's.
-// Warp tile: 64 rows (8 m-tiles of 8) x 32 cols (4 n-tiles of 8).
-// Row of m-tile mt, fragment row g:   MN-major: 16*(mt>>1) + 2g + (mt&1);  K-major: 8*mt + g.
-// Same mapping for columns of B's n-tiles.
 template <bool KM, int NT>
-__device__ __forceinline__ void load_frags(const double *s, int xw, int h, int g, int t,
-                                           double (&f)[2][NT]) {
+__device__ __forceinline__ void load_frags(const double *s, int xw, int h, int g, int t, double (&f)[2][NT]) {
   if (KM) {
 #pragma unroll
     for (int r = 0; r < NT; ++r) {
-      const int x = xw + 8 * r + g;
-      const double2 v = *reinterpret_cast<const double2 *>(s + x * 16 + (((4 * h + t) ^ ((x & 1) << 2)) << 1));
+      const int x = xw + tile_row<true>(r, g);
+      const double2 v = *reinterpret_cast<const double2 *>(s + x * 16 + (((4 * h + t) ^ (x & 7)) << 1));
       f[0][r] = v.x;
       f[1][r] = v.y;
     }
@@ -187,7 +178,8 @@ __device__ __forceinline__ void load_frags(const double *s, int xw, int h, int g
       const int p = 8 * h + 2 * t + e;
 #pragma unroll
       for (int q = 0; q < NT / 2; ++q) {
-        const double2 v = *reinterpret_cast<const double2 *>(s + p * LD_MN + xw + 16 * q + 2 * g);
+        const int xb = (xw >> 4) + q;
+        const double2 v = *reinterpret_cast<const double2 *>(s + xb * 256 + p * 16 + ((g ^ (p & 7)) << 1));
         f[e][2 * q] = v.x;
         f[e][2 * q + 1] = v.y;
       }
@@ -195,134 +187,278 @@ __device__ __forceinline__ void load_frags(const double *s, int xw, int h, int g
   }
 }
 
+// Checksum-warp view of an operand tile: lane l owns 4 x-rows (cs_row_of(l, 0..3)) and the
+// warp's 4 k-slots p = 4c..4c+3; v[r][q] = X(cs_row_of(l, r), 4c + q).  Conflict-free LDS.128.
 template <bool KM>
-__device__ __forceinline__ int tile_row(int r, int g) {  // r: m/n-tile index, g: index in tile
-  return KM ? 8 * r + g : 16 * (r >> 1) + 2 * g + (r & 1);
+__device__ __forceinline__ int cs_row_of(int lane, int r) {
+  return KM ? lane + 32 * r : 2 * (lane & 7) + 16 * (lane >> 3) + 64 * (r >> 1) + (r & 1);
 }
-
-// ------------------------------------------------------------------ fused encode
-// Warp w reduces p = 2w and 2w+1 over all 128 rows of an operand tile.
-// Writes xsum[2w], xsum[2w+1]; folds |x| into the running max bits.
 template <bool KM>
-__device__ __forceinline__ void encode_tile(const double *s, int warp, int lane, double *xsum,
-                                            unsigned long long &xmax) {
+__device__ __forceinline__ void cs_load(const double *s, int c, int lane, double (&v)[4][4]) {
   if (KM) {
-    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int x = lane + 32 * r;
-      const double2 v = *reinterpret_cast<const double2 *>(s + x * 16 + ((warp ^ ((x & 1) << 2)) << 1));
-      s0 += v.x;
-      s1 += v.y;
-      xmax = umax64(xmax, umax64(absbits(v.x), absbits(v.y)));
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      for (int hq = 0; hq < 2; ++hq) {
+        const double2 w = *reinterpret_cast<const double2 *>(s + x * 16 + (((2 * c + hq) ^ (x & 7)) << 1));
+        v[r][2 * hq] = w.x;
+        v[r][2 * hq + 1] = w.y;
+      }
     }
-    if (lane == 0) { xsum[2 * warp] = s0; xsum[2 * warp + 1] = s1; }
   } else {
-    const int p = 2 * warp + (lane >> 4), l16 = lane & 15;
-    double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const double2 v = *reinterpret_cast<const double2 *>(s + p * LD_MN + 2 * l16 + 32 * r);
-      acc += v.x + v.y;
-      xmax = umax64(xmax, umax64(absbits(v.x), absbits(v.y)));
+    for (int rr = 0; rr < 2; ++rr) {
+      const int xb = (lane >> 3) + 4 * rr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = 4 * c + q;
+        const double2 w = *reinterpret_cast<const double2 *>(s + xb * 256 + p * 16 + (((lane & 7) ^ (p & 7)) << 1));
+        v[2 * rr][q] = w.x;
+        v[2 * rr + 1][q] = w.y;
+      }
     }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (l16 == 0) xsum[p] = acc;
   }
 }
 
-// Carry for one stage: thread (c = tid & 127, half h = tid >> 7) accumulates
-// cs_col[c] += sum_{p in half} a_sum[p]*B(p,c) and cs_row[c] += sum_p A(c,p)*b_sum[p].
-template <bool AKM, bool BKM>
-__device__ __forceinline__ void carry_stage(const double *sA, const double *sB, const double *asum,
-                                            const double *bsum, int c, int h, double &cs_col,
-                                            double &cs_row) {
+// ---------------- integer (fixed-point) encode: no SIMT FP64 next to the DMMA stream.
+// A dependent DADD behind a saturated DMMA stream takes ~1000 clk on sm_100a
+// (profiles/fp64_latency_under_dmma.json), so the column / row sums e^T A, B e are formed
+// exactly-enough on the integer pipes: every element is aligned to the stage's largest
+// exponent E (finite elements only) as the integer round_toward_zero(x * 2^(1078 - E)),
+// i.e. 56 significant bits for the largest element; 128 of them sum without overflow in a
+// signed 64-bit word.  Truncation per element is below 2^-55 * max|x|, far inside the
+// rounding budget of the threshold (R1/R1').
+
+__device__ __forceinline__ uint32_t hi_word(double x) { return (uint32_t)(__double_as_longlong(x) >> 32); }
+// |x| high word for the maxima; 0 for Inf/NaN (exponent all ones), as in the oracle.
+__device__ __forceinline__ uint32_t abs_hi_finite(double x) {
+  const uint32_t h = hi_word(x) & 0x7FFFFFFFu;
+  return h < 0x7FF00000u ? h : 0u;
+}
+__device__ __forceinline__ long long to_fixed(double x, int eref) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const int e = (int)((b >> 52) & 0x7FF);
+  const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (e ? (1ull << 52) : 0ull);
+  int d = eref - (e ? e : 1);
+  d = d < 0 ? 0 : (d > 63 ? 63 : d);
+  const long long v = (long long)((m << 3) >> d);
+  return (long long)b < 0 ? -v : v;
+}
+// S * 2^(eref - 1078) as a double (truncated to 53 bits); integer ops only on the common path.
+__device__ __forceinline__ double from_fixed(long long S, int eref) {
+  if (S == 0) return 0.0;
+  const unsigned long long sg = S < 0 ? (1ull << 63) : 0ull;
+  const unsigned long long a = S < 0 ? (unsigned long long)(-S) : (unsigned long long)S;
+  const int lz = __clzll((long long)a);
+  const int biased = eref + 8 - lz;
+  if (biased <= 0 || biased >= 2047) return ldexp((double)S, eref - 1078);  // sub/overflow: rare
+  const unsigned long long norm = a << lz;
+  return __longlong_as_double((long long)(sg | ((unsigned long long)biased << 52) | ((norm >> 11) & 0xFFFFFFFFFFFFFull)));
+}
+__device__ __forceinline__ long long shfl_xor_ll(long long v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+
+// Column sums over the 128 x-rows for the warp's 4 k-slots (v[r][q] = X(row(l,r), 4c+q)):
+// returns the sum for k-slot 4c + lane/8 in every lane; folds max|hi| into hmax.
+__device__ __forceinline__ double cs_encode_fx(const double (&v)[4][4], int lane, uint32_t &hmax) {
+  uint32_t hm = 0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int p = 8 * h + q;
-    cs_col = fma(asum[p], sB[sidx<BKM>(c, p)], cs_col);
-    cs_row = fma(sA[sidx<AKM>(c, p)], bsum[p], cs_row);
-  }
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) hm = max(hm, abs_hi_finite(v[r][q]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  hmax = max(hmax, hm);
+  int eref = (int)(hm >> 20);
+  eref = eref ? eref : 1;
+  long long s[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    s[q] = (to_fixed(v[0][q], eref) + to_fixed(v[1][q], eref)) + (to_fixed(v[2][q], eref) + to_fixed(v[3][q], eref));
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+  const long long w0 = (b4 ? s[2] : s[0]) + shfl_xor_ll(b4 ? s[0] : s[2], 16);  // keep q in {2b4, 2b4+1}
+  const long long w1 = (b4 ? s[3] : s[1]) + shfl_xor_ll(b4 ? s[1] : s[3], 16);
+  long long z = (b3 ? w1 : w0) + shfl_xor_ll(b3 ? w0 : w1, 8);                  // keep q = 2b4 + b3
+  z += shfl_xor_ll(z, 4);
+  z += shfl_xor_ll(z, 2);
+  z += shfl_xor_ll(z, 1);
+  return from_fixed(z, eref);
 }
 
 // ------------------------------------------------------------------ the kernel
 struct SmemTail {
-  double asum[2][BK], bsum[2][BK];
-  double cs_part[2][2][128];      // [col/row][half][index]
-  double dres[NTHREADS];          // residuals d (0..127 columns, 128..255 rows)
+  uint64_t full[STAGES], enc[STAGES], empty[STAGES];
+  double dres[256];                // residuals: 0..127 columns, 128..255 rows
   double red[NTHREADS / 32];
-  unsigned long long amax, bmax;
+  unsigned int amax_hi, bmax_hi;   // max finite |op(A)|, |op(B)| high words (R1')
   int first_row, first_col;
+  int retry;
 };
-constexpr size_t SMEM_BYTES = sizeof(double) * STAGES * STAGE_ELEMS + sizeof(SmemTail);
+constexpr size_t SMEM_BYTES = 1024 + sizeof(double) * STAGES * STAGE_ELEMS + sizeof(SmemTail);
 
-template <bool AKM, bool BKM, bool FT, bool V16>
-__global__ void __launch_bounds__(NTHREADS, 1) dgemm_abft_kernel(const Params P) {
-  extern __shared__ __align__(16) double smem[];
-  double *const ring = smem;
-  SmemTail &tl = *reinterpret_cast<SmemTail *>(smem + STAGES * STAGE_ELEMS);
-  double *const ctile = smem;  // epilogue reuse of the ring
+// Named barriers (id 0 is __syncthreads).  Both roles execute the same sequence of the
+// CTA-wide ones; the 256-thread ones are private to the MMA warpgroups.
+enum { BAR_RING_FREE = 1, BAR_CTILE = 2, BAR_FLAGS_R = 3, BAR_FLAGS_C = 4, BAR_DECIDE = 5, BAR_RED = 6 };
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ int bar_popc(int id, int count, bool pred) {
+  int r;
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.u32 p, %1, 0;\nbar.red.popc.u32 %0, %2, %3, p;\n}\n"
+      : "=r"(r)
+      : "r"((int)pred), "r"(id), "r"(count)
+      : "memory");
+  return r;
+}
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warp grid
-  const int ti = blockIdx.x, tj = blockIdx.y;
-  const int tile = ti + tj * P.tiles_m;
-  const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
-  const int bm_eff = (int)min64(BM, P.m - i0), bn_eff = (int)min64(BN, P.n - j0);
-  const int nk = P.nk;
+struct Ctx {
+  double *ring;
+  SmemTail *tl;
+  int tid, lane, warp, tile, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi;
+  // Protected tiles: TMA boxes start at the even coordinate xs = x0 - (x0 & 1) (the contiguous
+  // dimension of a TMA box must start 16-byte aligned), so tile-local data row i sits in
+  // staged row i + o (o = x0 & 1) and the checksum row/column takes the free row cr.
+  int oa, ob, cra, crb;
+};
 
-  // Faults of this tile: [f_lo, f_hi) in the (tile, stage)-sorted list.
-  int f_lo = 0, f_hi = 0;
-  if (P.nfaults > 0) {
-    int lo = 0, hi = P.nfaults;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.faults[mid].tile < tile) lo = mid + 1; else hi = mid; }
-    f_lo = lo;
-    hi = P.nfaults;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.faults[mid].tile <= tile) lo = mid + 1; else hi = mid; }
-    f_hi = lo;
-  }
-
-  double acc[8][4][2];
+// ---------------- warpgroup 0: TMA producer (warp 0 lane 0) + checksum-encode warps
+// Checksum warp c encodes k-slots 4c..4c+3 of every stage: it waits for the stage's TMA
+// bytes, forms a_sum[p] = sum_{i<127} op(A)_ip and b_sum[p] = sum_{j<127} op(B)_pj on the
+// integer pipes, writes them into row 127 of the staged A tile and row 127 (= column 127 of
+// op(B)) of the staged B tile, and arrives on the stage's `enc` barrier.  The DMMA stream
+// then computes C^f = [A; e^T A][B, B e] tile by tile: acc(127, j) is the
+// carried column checksum (e^T A_I) B_J and acc(i, 127) the carried row checksum A_I (B_J e)
+// (outer-product maintenance), at no SIMT FP64 cost.
+template <bool AKM, bool BKM, bool FT>
+__device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUtensorMap &tmB, const Params &P,
+                                              const Ctx &x) {
+  SmemTail &tl = *x.tl;
+  double *const ring = x.ring;
+  const int lane = x.lane, warp = x.warp, c = warp, nk = x.nk;
+  int stage_base = 0;
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
-    const bool inject = attempt == 0 && f_lo < f_hi;
-    int fnext = f_lo;
-    int next_stage = inject ? P.faults[fnext].stage : 0x7fffffff;
+    int produced = 0;
+    // Issue stages [produced, min(lim, nk)).  Blocking for stages below `must` (the checksum
+    // warps need them next); beyond that only while ring slots are already free, so the
+    // producer never stalls warp 0's encode behind the MMA warps.
+    auto produce_upto = [&](int lim, int must) {
+      for (; produced < lim && produced < nk; ++produced) {
+        const int gs = stage_base + produced, slot = gs % STAGES;
+        if (gs >= STAGES) {
+          const uint32_t par = ((gs / STAGES) - 1) & 1;
+          if (produced < must) mbar_wait(&tl.empty[slot], par);
+          else if (!mbar_test(&tl.empty[slot], par)) break;
+        }
+        double *sa = ring + slot * STAGE_ELEMS;
+        mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
+        const int k0 = produced * BK;
+        const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
+        if (AKM) {
+          tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
+        } else {
+#pragma unroll
+          for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, k0, &tl.full[slot]);
+        }
+        double *sb = sa + TILE_ELEMS;
+        if (BKM) {
+          tma_load_2d(sb, &tmB, k0, xbj, &tl.full[slot]);
+        } else {
+#pragma unroll
+          for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
+        }
+      }
+    };
+    if (verify) {
+      uint32_t amax_hi = 0u, bmax_hi = 0u;
+      for (int s = 0; s < nk; ++s) {
+        if (warp == 0 && lane == 0) produce_upto(s + STAGES, s + 1);
+        __syncwarp();
+        const int gs = stage_base + s, slot = gs % STAGES;
+        const long long t0 = P.dev_prof ? clock64() : 0;
+        mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
+        const long long t1 = P.dev_prof ? clock64() : 0;
+        double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
+        double v[4][4];
+        // The checksum row cr (127, or 0 for odd tiles) holds a neighbour tile's data: it is
+        // staged row 127 = lane 31 / r 3, or staged row 0 = lane 0 / r 0, in both layouts.
+        const bool xa_l = x.cra ? lane == 31 : lane == 0, xb_l = x.crb ? lane == 31 : lane == 0;
+        const int xa_r = x.cra ? 3 : 0, xb_r = x.crb ? 3 : 0;
+        cs_load<AKM>(sA, c, lane, v);  // encode A: e^T A_I over the 127 data rows
+        if (xa_l) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[xa_r][q] = 0.0;
+        }
+        const double asum = cs_encode_fx(v, lane, amax_hi);
+        cs_load<BKM>(sB, c, lane, v);  // encode B: B_J e over the 127 data columns
+        if (xb_l) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[xb_r][q] = 0.0;
+        }
+        const double bsum = cs_encode_fx(v, lane, bmax_hi);
+        if ((lane & 7) == 0) {  // lanes 8q hold the sums of k-slot 4c+q
+          const int p = 4 * c + (lane >> 3);
+          sA[sidx<AKM>(x.cra, p)] = asum;
+          sB[sidx<BKM>(x.crb, p)] = bsum;
+        }
+        fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tl.enc[slot]);
+        if (P.dev_prof && lane == 0) {
+          const long long t2 = clock64();
+          unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + warp) * 2;
+          dp[0] += (unsigned long long)(t1 - t0);
+          dp[1] += (unsigned long long)(t2 - t1);
+        }
+      }
+      if (lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
+    } else if (warp == 0 && lane == 0) {
+      produce_upto(nk, nk);
+    }
+    stage_base += nk;
+    bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
+    if (!verify) return;
+    bar_sync(BAR_DECIDE, NTHREADS);     // MMA warps decided: clean / corrected / recompute
+    if (!tl.retry) return;
+  }
+}
 
+// ---------------- warpgroups 1-2: MMA warps (+ epilogue)
+template <bool AKM, bool BKM, bool FT>
+__device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
+  SmemTail &tl = *x.tl;
+  double *const ring = x.ring;
+  double *const ctile = ring;  // epilogue reuse of the ring
+  const int lane = x.lane, nk = x.nk;
+  const int mw = x.warp - N_CS_WARPS, wm = mw >> 2, wn = mw & 3;
+  const int g = lane >> 2, t = lane & 3;
+  const int vt = x.tid - N_CS_WARPS * 32;  // 0..255
+  double acc[8][4][2];
+  int stage_base = 0;
+  for (int attempt = 0;; ++attempt) {
+    const bool verify = FT && attempt == 0;
+    const bool inject = attempt == 0 && x.f_lo < x.f_hi;
+    int fnext = x.f_lo;
+    int next_stage = inject ? P.faults[fnext].stage : 0x7fffffff;
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    double cs_col = 0.0, cs_row = 0.0;
-    unsigned long long amax = 0ull, bmax = 0ull;
-    if (tid == 0) { tl.amax = 0ull; tl.bmax = 0ull; tl.first_row = 0x7fffffff; tl.first_col = 0x7fffffff; }
-
-    auto load_stage = [&](int s) {
-      if (s < nk) {
-        double *sa = ring + (s % STAGES) * STAGE_ELEMS;
-        load_tile<AKM, V16>(sa, P.A, P.lda, i0, P.m, (int64_t)s * BK, P.k, tid);
-        load_tile<BKM, V16>(sa + TILE_ELEMS, P.B, P.ldb, j0, P.n, (int64_t)s * BK, P.k, tid);
-      }
-      cp_async_commit();
-    };
     auto apply_faults = [&](int s) {
       while (s == next_stage) {
         const FaultDev f = P.faults[fnext];
-        const int lr = f.li & 63, lc = f.lj & 31;
+        const int si = f.li + x.oa, sj = f.lj + x.ob;  // staged row / column
+        const int lr = si & 63, lc = sj & 31;
         const int fmt = AKM ? (lr >> 3) : 2 * (lr >> 4) + (lr & 1);
-        const int fg = AKM ? (lr & 7) : ((lr & 15) >> 1);
+        const int rr = lr & 7;  // K-major: row in the 8-row tile = 4*(g&1) + (g>>1)
+        const int fg = AKM ? (((rr & 3) << 1) | (rr >> 2)) : ((lr & 15) >> 1);
         const int fnt = BKM ? (lc >> 3) : 2 * (lc >> 4) + (lc & 1);
-        const int cc = BKM ? (lc & 7) : ((lc & 15) >> 1);
+        const int cr = lc & 7;  // K-major: column in the 8-column tile, same mapping
+        const int cc = BKM ? (((cr & 3) << 1) | (cr >> 2)) : ((lc & 15) >> 1);  // n-index
         // Register index of the owning accumulator, -1 for every other thread.  Select-based
         // (no dynamic register indexing) so the accumulators stay in registers.
-        const bool owner = (f.li >> 6) == wm && (f.lj >> 5) == wn && lane == fg * 4 + (cc >> 1);
+        const bool owner = (si >> 6) == wm && (sj >> 5) == wn && lane == fg * 4 + (cc >> 1);
         const int fidx = owner ? (fmt * 4 + fnt) * 2 + (cc & 1) : -1;
 #pragma unroll
         for (int a = 0; a < 8; ++a)
@@ -334,30 +470,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_abft_kernel(const Params P)
               acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v + f.delta : v;
             }
         ++fnext;
-        next_stage = fnext < f_hi ? P.faults[fnext].stage : 0x7fffffff;
+        next_stage = fnext < x.f_hi ? P.faults[fnext].stage : 0x7fffffff;
       }
     };
-
-    // Prologue.
-#pragma unroll
-    for (int s = 0; s < LOOKAHEAD; ++s) load_stage(s);
-
+    long long w_wait = 0, w_work = 0;
     for (int s = 0; s < nk; ++s) {
-      cp_async_wait<LOOKAHEAD - 1>();
-      __syncthreads();
-      load_stage(s + LOOKAHEAD);
-      const double *sA = ring + (s % STAGES) * STAGE_ELEMS;
-      const double *sB = sA + TILE_ELEMS;
-      if (verify) {
-        encode_tile<AKM>(sA, warp, lane, tl.asum[s & 1], amax);
-        encode_tile<BKM>(sB, warp, lane, tl.bsum[s & 1], bmax);
-        if (s > 0) {
-          const double *pA = ring + ((s - 1) % STAGES) * STAGE_ELEMS;
-          carry_stage<AKM, BKM>(pA, pA + TILE_ELEMS, tl.asum[(s - 1) & 1], tl.bsum[(s - 1) & 1],
-                                tid & 127, tid >> 7, cs_col, cs_row);
-        }
-      }
+      const int gs = stage_base + s, slot = gs % STAGES;
+      const long long t0 = P.dev_prof ? clock64() : 0;
+      // The protected pass waits for the encoded stage (TMA bytes + checksum row/column).
+      if (verify) mbar_wait(&tl.enc[slot], (gs / STAGES) & 1);
+      else mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
+      if (P.dev_prof) { const long long t1 = clock64(); w_wait += t1 - t0; w_work -= t1; }
       if (inject) apply_faults(s);
+      const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double af[2][8], bf[2][4];
@@ -370,18 +495,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_abft_kernel(const Params P)
 #pragma unroll
             for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b], af[e][a], bf[e][b]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tl.empty[slot]);
+      if (P.dev_prof) w_work += clock64();
     }
-    cp_async_wait<0>();
-    __syncthreads();
-    if (verify && nk > 0) {
-      const double *pA = ring + ((nk - 1) % STAGES) * STAGE_ELEMS;
-      carry_stage<AKM, BKM>(pA, pA + TILE_ELEMS, tl.asum[(nk - 1) & 1], tl.bsum[(nk - 1) & 1],
-                            tid & 127, tid >> 7, cs_col, cs_row);
+    if (P.dev_prof && lane == 0) {
+      unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + x.warp) * 2;
+      dp[0] += (unsigned long long)w_wait;
+      dp[1] += (unsigned long long)w_work;
     }
     if (inject) apply_faults(nk);  // faults with step_q == k
-    __syncthreads();               // ring no longer read: reuse it as the C tile
+    stage_base += nk;
+    bar_sync(BAR_RING_FREE, NTHREADS);  // every stage consumed: the ring is free for the C tile
 
-    // Stage the accumulator tile through shared memory: ctile[col*LDC_S + row].
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
       const int row = wm * 64 + tile_row<AKM>(a, g);
@@ -393,116 +519,173 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_abft_kernel(const Params P)
           ctile[col * LDC_S + row] = acc[a][b][e];
         }
     }
-    if (verify) {
-      tl.cs_part[0][tid >> 7][tid & 127] = cs_col;
-      tl.cs_part[1][tid >> 7][tid & 127] = cs_row;
-      // CTA-wide maxima for the threshold.
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        amax = umax64(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        bmax = umax64(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-      }
-      if (lane == 0) { atomicMax(&tl.amax, amax); atomicMax(&tl.bmax, bmax); }
-    }
-    __syncthreads();
-
+    bar_sync(BAR_CTILE, 256);
     if (!verify) break;
 
-    // ---- verification: reference checksums from the computed tile.
-    const int c = tid & 127;
-    const bool is_row = tid >= 128;
-    double r = 0.0;
-    if (is_row) {
-#pragma unroll 8
-      for (int j = 0; j < BN; ++j) r += ctile[j * LDC_S + c];
-    } else {
-#pragma unroll 8
-      for (int i = 0; i < BM; ++i) r += ctile[c * LDC_S + i];
+    // ---- verification: reference checksums r from the computed C_IJ against
+    // the carried checksums in row / column 127 of C^f.
+    // ctile is indexed by staged rows / columns: data row i at i + oa, data column j at j + ob.
+    const int cidx = vt & 127;
+    const bool is_row = vt >= 128;
+    double r = 0.0, cs = 0.0;
+    if (cidx < DM) {
+      if (is_row) {
+        const double *rowp = ctile + (cidx + x.oa);
+#pragma unroll 9
+        for (int j = 0; j < DM; ++j) r += rowp[(j + x.ob) * LDC_S];
+        cs = rowp[x.crb * LDC_S];  // A_I (B_J e)
+      } else {
+        const double *colp = ctile + (cidx + x.ob) * LDC_S;
+#pragma unroll 9
+        for (int i = 0; i < DM; ++i) r += colp[i + x.oa];
+        cs = colp[x.cra];  // (e^T A_I) B_J
+      }
     }
-    const double cs = tl.cs_part[is_row][0][c] + tl.cs_part[is_row][1][c];
     const double d = r - cs;
-    const double amx = __longlong_as_double((long long)tl.amax), bmx = __longlong_as_double((long long)tl.bmax);
+    // R1': maxima rounded up to the largest double with the same high word.
+    const double amx = __longlong_as_double((long long)(((unsigned long long)tl.amax_hi << 32) | 0xFFFFFFFFull));
+    const double bmx = __longlong_as_double((long long)(((unsigned long long)tl.bmax_hi << 32) | 0xFFFFFFFFull));
     const int64_t kt = P.k;
-    const int len = is_row ? bn_eff : bm_eff;
+    const int len = is_row ? x.bn_eff : x.bm_eff;
     const double nu = (double)(kt + len) * 0x1p-53;
     const double tau = 2.0 * (nu / (1.0 - nu)) * (double)kt * (double)len * amx * bmx;  // DESIGN.md R1
-    const bool valid = is_row ? (c < bm_eff) : (c < bn_eff);
+    const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
     const bool flag = valid && !(fabs(d) <= tau);
-    tl.dres[tid] = d;
-    if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, c);
-    const int nfr = __syncthreads_count(flag && is_row);
-    const int nfc = __syncthreads_count(flag && !is_row);
-    if (nfr == 0 && nfc == 0) break;  // clean unit
-
+    tl.dres[vt] = d;
+    if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, cidx);
+    const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
+    const int nfc = bar_popc(BAR_FLAGS_C, 256, flag && !is_row);
+    const bool multi = !(nfr == 0 && nfc == 0) && !(nfr == 1 && nfc == 1);
     const int fr = tl.first_row, fc = tl.first_col;
     if (nfr == 1 && nfc == 1) {
       // Single error at the intersection (i0+fr, j0+fc): correct in place.
       if (P.correct_mode == 1) {
-        if (tid == 0) ctile[fc * LDC_S + fr] -= tl.dres[fc];  // subtract d_col
+        if (vt == 0) ctile[(fc + x.ob) * LDC_S + fr + x.oa] -= tl.dres[fc];  // subtract d_col
       } else {
         // Recompute C_ij with a fresh k-long dot product (R4).
-        const int64_t gi = i0 + fr, gj = j0 + fc;
+        const int64_t gi = x.i0 + fr, gj = x.j0 + fc;
         double part = 0.0;
-        for (int64_t p = tid; p < P.k; p += NTHREADS) {
+        for (int64_t p = vt; p < P.k; p += 256) {
           const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
           const double bv = BKM ? P.B[p + gj * P.ldb] : P.B[gj + p * P.ldb];
           part = fma(av, bv, part);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) tl.red[warp] = part;
-        __syncthreads();
-        if (tid == 0) {
+        if (lane == 0) tl.red[mw] = part;
+        bar_sync(BAR_RED, 256);
+        if (vt == 0) {
           double v = 0.0;
 #pragma unroll
-          for (int w = 0; w < NTHREADS / 32; ++w) v += tl.red[w];
-          ctile[fc * LDC_S + fr] = v;
+          for (int q = 0; q < N_MMA_WARPS; ++q) v += tl.red[q];
+          ctile[(fc + x.ob) * LDC_S + fr + x.oa] = v;
         }
       }
-      if (tid == 0) {
-        atomicAdd(&P.counters[CNT_DETECTED], 1ull);
-        atomicAdd(&P.counters[CNT_CORRECTED], 1ull);
-        const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
-        if ((long long)slot < P.ev_cap)
-          P.events[slot] = EventDev{(long long)(i0 + fr), (long long)(j0 + fc), 1, 0,
-                                    tl.dres[128 + fr], tl.dres[fc]};
-      }
-      __syncthreads();
-      break;
     }
-    // Out of the one-error model: record, then recompute the whole tile once.
-    if (tid == 0) {
+    if (vt == 0 && (nfr | nfc)) {
       atomicAdd(&P.counters[CNT_DETECTED], 1ull);
-      atomicAdd(&P.counters[CNT_RECOMPUTED], 1ull);
+      atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
       const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
       if ((long long)slot < P.ev_cap)
-        P.events[slot] = EventDev{(long long)i0, (long long)j0, 2, 0,
-                                  nfr ? tl.dres[128 + fr] : 0.0, nfc ? tl.dres[fc] : 0.0};
+        P.events[slot] = multi ? EventDev{(long long)x.i0, (long long)x.j0, 2, 0, nfr ? tl.dres[128 + fr] : 0.0,
+                                          nfc ? tl.dres[fc] : 0.0}
+                               : EventDev{(long long)(x.i0 + fr), (long long)(x.j0 + fc), 1, 0, tl.dres[128 + fr],
+                                          tl.dres[fc]};
     }
-    __syncthreads();
+    if (vt == 0) tl.retry = multi ? 1 : 0;
+    if (multi) fence_proxy_async();  // generic writes to the ring (C tile) before TMA reuses it
+    bar_sync(BAR_DECIDE, NTHREADS);
+    if (!multi) break;
+    // Out of the one-error model: recompute the whole tile once (no re-verification).
   }
 
   // ---- store: C = alpha*acc + beta*C0 (two roundings each, no contraction).
-  {
-    const int i = tid & 127;
-    const double alpha = P.alpha, beta = P.beta;
-    if (i < bm_eff) {
-      double *crow = P.C + (i0 + i) + j0 * P.ldc;
+  const int i = vt & 127;
+  const double alpha = P.alpha, beta = P.beta;
+  if (i < x.bm_eff) {
+    double *crow = P.C + (int64_t)(x.i0 + i) + (int64_t)x.j0 * P.ldc;
 #pragma unroll 4
-      for (int j = tid >> 7; j < bn_eff; j += 2) {
-        const double v = __dmul_rn(alpha, ctile[j * LDC_S + i]);
-        double *dst = crow + (int64_t)j * P.ldc;
-        *dst = (beta != 0.0) ? __dadd_rn(v, __dmul_rn(beta, *dst)) : v;
-      }
+    for (int j = vt >> 7; j < x.bn_eff; j += 2) {
+      const double v = __dmul_rn(alpha, ctile[(j + x.ob) * LDC_S + i + x.oa]);
+      double *dst = crow + (int64_t)j * P.ldc;
+      *dst = (beta != 0.0) ? __dadd_rn(v, __dmul_rn(beta, *dst)) : v;
     }
+  }
+}
+
+template <bool AKM, bool BKM, bool FT>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    dgemm_abft_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const Params P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Ctx x;
+  // 1024-byte alignment by pointer arithmetic on the __shared__ array (an integer round trip
+  // would lose the address space and turn every LDS into a generic LD).
+  x.ring = reinterpret_cast<double *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  x.tl = reinterpret_cast<SmemTail *>(x.ring + STAGES * STAGE_ELEMS);
+  SmemTail &tl = *x.tl;
+  x.tid = threadIdx.x;
+  x.lane = x.tid & 31;
+  x.warp = x.tid >> 5;
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  x.tile = ti + tj * P.tiles_m;
+  // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
+  // full 128 x 128 MMA tile for data.
+  constexpr int tm = FT ? TM : BM, tn = FT ? TN : BN;
+  x.i0 = ti * tm;
+  x.j0 = tj * tn;
+  x.bm_eff = (int)min64(tm, P.m - x.i0);
+  x.bn_eff = (int)min64(tn, P.n - x.j0);
+  x.oa = FT ? (x.i0 & 1) : 0;
+  x.ob = FT ? (x.j0 & 1) : 0;
+  x.cra = x.oa ? 0 : DM;
+  x.crb = x.ob ? 0 : DM;
+  x.nk = P.nk;
+
+  if (x.tid == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&tl.full[s], 1);
+      mbar_init(&tl.enc[s], N_CS_WARPS);
+      mbar_init(&tl.empty[s], N_MMA_WARPS);
+    }
+    tl.amax_hi = 0u;
+    tl.bmax_hi = 0u;
+    tl.first_row = 0x7fffffff;
+    tl.first_col = 0x7fffffff;
+    tl.retry = 0;
+    fence_mbar_init();
+  }
+  // Faults of this tile: [f_lo, f_hi) in the (tile, stage)-sorted list.
+  x.f_lo = x.f_hi = 0;
+  if (P.nfaults > 0) {
+    int lo = 0, hi = P.nfaults;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.faults[mid].tile < x.tile) lo = mid + 1; else hi = mid; }
+    x.f_lo = lo;
+    hi = P.nfaults;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.faults[mid].tile <= x.tile) lo = mid + 1; else hi = mid; }
+    x.f_hi = lo;
+  }
+  __syncthreads();
+
+  // The two roles never re-converge, so ptxas can give each its own register budget.  The
+  // checksum warps take the LOWEST warp ids: the issue arbiter favours high ids, so the DMMA
+  // warps always win an issue slot and the integer encode fills the idle ones.
+  if (x.warp < N_CS_WARPS) {
+    setmaxnreg_dec<REG_CS>();
+    checksum_role<AKM, BKM, FT>(tmA, tmB, P, x);
+  } else {
+    setmaxnreg_inc<REG_MMA>();
+    mma_role<AKM, BKM, FT>(P, x);
   }
 }
 
 // C = beta*C (beta == 0: C = 0 without reading C).
 __global__ void scale_kernel(int64_t m, int64_t n, double beta, double *C, int64_t ldc) {
   const int64_t total = m * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e % m, j = e / m;
     double *p = C + i + j * ldc;
     *p = (beta == 0.0) ? 0.0 : __dmul_rn(beta, *p);

@@ -7,7 +7,10 @@
 #include "../../include/ftblas.h"
 #include "dgemm_abft.cuh"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -40,9 +43,9 @@ int cuda_fail(cudaError_t e) {
 bool is_n(char c) { return c == 'N' || c == 'n'; }
 bool is_t(char c) { return c == 'T' || c == 't' || c == 'C' || c == 'c'; }
 
-template <bool AKM, bool BKM, bool FT, bool V16>
-int launch_one(const ftk::Params &p, dim3 grid, cudaStream_t st) {
-  auto kfn = ftk::dgemm_abft_kernel<AKM, BKM, FT, V16>;
+template <bool AKM, bool BKM, bool FT>
+int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &p, dim3 grid, cudaStream_t st) {
+  auto kfn = ftk::dgemm_abft_kernel<AKM, BKM, FT>;
   static bool attr_set[64] = {false};  // per instantiation and device
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
@@ -50,20 +53,39 @@ int launch_one(const ftk::Params &p, dim3 grid, cudaStream_t st) {
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ftk::SMEM_BYTES));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  kfn<<<grid, ftk::NTHREADS, ftk::SMEM_BYTES, st>>>(p);
+  kfn<<<grid, ftk::NTHREADS, ftk::SMEM_BYTES, st>>>(ta, tb, p);
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
 template <bool FT>
-int dispatch(bool akm, bool bkm, bool v16, const ftk::Params &p, dim3 grid, cudaStream_t st) {
-  if (v16) {
-    if (akm) return bkm ? launch_one<true, true, FT, true>(p, grid, st) : launch_one<true, false, FT, true>(p, grid, st);
-    return bkm ? launch_one<false, true, FT, true>(p, grid, st) : launch_one<false, false, FT, true>(p, grid, st);
+int dispatch(bool akm, bool bkm, const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &p, dim3 grid,
+             cudaStream_t st) {
+  if (akm) return bkm ? launch_one<true, true, FT>(ta, tb, p, grid, st) : launch_one<true, false, FT>(ta, tb, p, grid, st);
+  return bkm ? launch_one<false, true, FT>(ta, tb, p, grid, st) : launch_one<false, false, FT>(ta, tb, p, grid, st);
+}
+
+// TMA descriptor of one operand.  K-major (k contiguous): dims {k, x}, box {16, 128};
+// MN-major (x contiguous): dims {x, k}, box {16, 16}.  128-byte swizzle, zero OOB fill.
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+int make_tmap(CUtensorMap *map, const double *base, int64_t ld, bool kmajor, int64_t xdim, int64_t kdim) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) { tl_cuda_error = "cuTensorMapEncodeTiled unavailable"; return 1; }
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  if (akm) return bkm ? launch_one<true, true, FT, false>(p, grid, st) : launch_one<true, false, FT, false>(p, grid, st);
-  return bkm ? launch_one<false, true, FT, false>(p, grid, st) : launch_one<false, false, FT, false>(p, grid, st);
+  cuuint64_t dims[2], strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (kmajor) { dims[0] = kdim; dims[1] = xdim; box[0] = 16; box[1] = 128; }
+  else        { dims[0] = xdim; dims[1] = kdim; box[0] = 16; box[1] = 16; }
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { tl_cuda_error = "cuTensorMapEncodeTiled failed"; return 1; }
+  return 0;
 }
 
 int ensure_device_init() {
@@ -97,14 +119,14 @@ int check_args(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, 
   if (m > 0 && n > 0 && C == nullptr) return -12;
   if (ldc < std::max<int64_t>(1, m)) return -13;
   // Index arithmetic inside the kernels uses int for tile coordinates.
-  if ((m + ftk::BM - 1) / ftk::BM > 0x7fffffff) return -3;
-  if ((n + ftk::BN - 1) / ftk::BN > 65535) return -4;
+  if ((m + ftk::TM - 1) / ftk::TM > 0x7fffffff) return -3;
+  if ((n + ftk::TN - 1) / ftk::TN > 65535) return -4;
   return 0;
 }
 
 void fill_geometry(ftblas_err_report_t *err, int64_t k) {
-  err->unit_rows = ftk::BM;
-  err->unit_cols = ftk::BN;
+  err->unit_rows = ftk::TM;
+  err->unit_cols = ftk::TN;
   err->unit_k = (int32_t)std::min<int64_t>(k, INT32_MAX);
   err->step_quantum = ftk::BK;
 }
@@ -142,18 +164,21 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
   ftk::Params p{};
   p.m = m; p.n = n; p.k = k; p.alpha = alpha; p.beta = beta;
   p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
-  p.tiles_m = (int)((m + ftk::BM - 1) / ftk::BM);
-  p.tiles_n = (int)((n + ftk::BN - 1) / ftk::BN);
+  const int tm = ft ? ftk::TM : ftk::BM, tn = ft ? ftk::TN : ftk::BN;  // tile stride in C
+  p.tiles_m = (int)((m + tm - 1) / tm);
+  p.tiles_n = (int)((n + tn - 1) / tn);
   p.nk = (int)((k + ftk::BK - 1) / ftk::BK);
   p.correct_mode = tl_correct;
+  // development only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
+  if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
 
   // Bucket faults by (tile, stage); stable so same-stage faults keep the caller's order.
   std::vector<ftk::FaultDev> fd;
   fd.reserve(faults.size());
   for (const auto &f : faults) {
-    const int64_t ti = f.i / ftk::BM, tj = f.j / ftk::BN;
+    const int64_t ti = f.i / tm, tj = f.j / tn;
     fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m), (int32_t)(f.step / ftk::BK),
-                               (int32_t)(f.i - ti * ftk::BM), (int32_t)(f.j - tj * ftk::BN), f.delta});
+                               (int32_t)(f.i - ti * tm), (int32_t)(f.j - tj * tn), f.delta});
   }
   std::stable_sort(fd.begin(), fd.end(), [](const ftk::FaultDev &a, const ftk::FaultDev &b) {
     return a.tile != b.tile ? a.tile < b.tile : a.stage < b.stage;
@@ -175,10 +200,33 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
     CUDA_TRY(cudaMemcpyAsync(scratch + cnt_bytes + ev_bytes, fd.data(), f_bytes, cudaMemcpyHostToDevice, st));
 
   const bool akm = is_t(ta), bkm = is_n(tb);
-  const bool v16 = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
-                   (lda % 2) == 0 && (ldb % 2) == 0;
+  // TMA needs 16-byte aligned bases and leading dimensions: repack otherwise (device copy
+  // into a stream-ordered buffer with an even leading dimension; marshalling only).
+  const int64_t ar = is_n(ta) ? m : k, ac = is_n(ta) ? k : m;
+  const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
+  double *rA = nullptr, *rB = nullptr;
+  auto aligned = [](const double *q, int64_t ld) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0 && ld % 2 == 0; };
+  if (!aligned(A, lda)) {
+    const int64_t nld = (ar + 1) & ~int64_t(1);
+    CUDA_TRY(cudaMallocAsync((void **)&rA, sizeof(double) * nld * ac, st));
+    CUDA_TRY(cudaMemcpy2DAsync(rA, sizeof(double) * nld, A, sizeof(double) * lda, sizeof(double) * ar, ac,
+                               cudaMemcpyDeviceToDevice, st));
+    p.A = rA; p.lda = nld;
+  }
+  if (!aligned(B, ldb)) {
+    const int64_t nld = (br + 1) & ~int64_t(1);
+    CUDA_TRY(cudaMallocAsync((void **)&rB, sizeof(double) * nld * bc, st));
+    CUDA_TRY(cudaMemcpy2DAsync(rB, sizeof(double) * nld, B, sizeof(double) * ldb, sizeof(double) * br, bc,
+                               cudaMemcpyDeviceToDevice, st));
+    p.B = rB; p.ldb = nld;
+  }
+  CUtensorMap tmA, tmB;
+  if (int e = make_tmap(&tmA, p.A, p.lda, akm, m, k)) return e;
+  if (int e = make_tmap(&tmB, p.B, p.ldb, bkm, n, k)) return e;
   const dim3 grid(p.tiles_m, p.tiles_n);
-  int lrc = ft ? dispatch<true>(akm, bkm, v16, p, grid, st) : dispatch<false>(akm, bkm, v16, p, grid, st);
+  int lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
+  if (rA) cudaFreeAsync(rA, st);
+  if (rB) cudaFreeAsync(rB, st);
   if (lrc) { cudaFreeAsync(scratch, st); return lrc; }
 
   if (err) {
@@ -341,8 +389,8 @@ int ftblas_set_correction(int mode) {
 }
 
 int ftblas_get_geometry(int32_t *unit_rows, int32_t *unit_cols, int32_t *step_quantum) {
-  if (unit_rows) *unit_rows = ftk::BM;
-  if (unit_cols) *unit_cols = ftk::BN;
+  if (unit_rows) *unit_rows = ftk::TM;
+  if (unit_cols) *unit_cols = ftk::TN;
   if (step_quantum) *step_quantum = ftk::BK;
   return 0;
 }

@@ -39,7 +39,9 @@ def unit_tau(A, B, ta, tb, i, j, BM, BN, k):
     oA, oB = op(A, ta), op(B, tb)
     I0, J0 = (i // BM) * BM, (j // BN) * BN
     Ia, Jb = oA[I0:I0 + BM, :], oB[:, J0:J0 + BN]
-    amax, bmax = float(np.abs(Ia).max()), float(np.abs(Jb).max())
+    import oracle
+    amax = oracle.round_up_hi32(float(np.abs(Ia[np.isfinite(Ia)]).max(initial=0.0)))
+    bmax = oracle.round_up_hi32(float(np.abs(Jb[np.isfinite(Jb)]).max(initial=0.0)))
     bm, bn = Ia.shape[0], Jb.shape[1]
     g = lambda nn: nn * U / (1 - nn * U)  # noqa: E731
     return (2 * g(k + bm) * k * bm * amax * bmax, 2 * g(k + bn) * k * bn * amax * bmax)

@@ -120,7 +120,8 @@ def test_c1_config_single_error_detect_correct():
 def test_c2_config_full():
     c = synth.config("C2")
     Cg, Co, rep, orep = run_both(c.A, c.B, c.C0, alpha=c.alpha, beta=c.beta)
-    assert rep.detected == 0 and orep.detected == 0 and rep.units_checked == 256
+    assert rep.detected == 0 and orep.detected == 0
+    assert rep.units_checked == orep.units_checked == -(-2048 // rep.unit_rows) * -(-2048 // rep.unit_cols)
 
 
 def test_single_injection_campaign_integer_exact():

@@ -258,6 +258,17 @@ def test_no_false_positives_float_inputs():
         assert rep.detected == 0
 
 
+def test_round_up_hi32_definition():
+    """R1': keep the high word, set the low 32 bits: an upper bound within 2^-20 relative."""
+    import struct
+    for x in [1.0, 0.1, 5.3, 1e-300, 7.5e300, 0.0]:
+        r = oracle.round_up_hi32(x)
+        bx, br = (struct.unpack("<Q", struct.pack("<d", v))[0] for v in (x, r))
+        assert br == bx | 0xFFFFFFFF and br >> 32 == bx >> 32
+        assert r >= x and (x == 0.0 or r <= x * (1 + 2.0 ** -20))
+    assert oracle.round_up_hi32(0.0) == struct.unpack("<d", struct.pack("<Q", 0xFFFFFFFF))[0]
+
+
 def test_threshold_closed_form_and_detection_edge():
     assert oracle.gamma(1) == U / (1 - U)
     assert oracle.gamma(0) == 0.0
@@ -266,6 +277,7 @@ def test_threshold_closed_form_and_detection_edge():
     m, n, k = 48, 40, 100
     A, B = F(rng.uniform(-1, 1, (m, k))), F(rng.uniform(-1, 1, (k, n)))
     amax, bmax = np.abs(A[:32]).max(), np.abs(B[:, :32]).max()
+    amax, bmax = oracle.round_up_hi32(amax), oracle.round_up_hi32(bmax)
     big = 3.0 * oracle.tau(k, 32, amax, bmax)  # > 2 tau: must be located
     _, rep = run(A, B, BM=32, BN=32, BK=4, faults=[(5, 7, 50, big)])
     assert (rep.corrected, rep.recomputed) == (1, 0) and rep.events[0][1:3] == (5, 7)
