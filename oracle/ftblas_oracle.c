@@ -24,9 +24,11 @@
  *     (PAPER.md:91); the reading used is the rigorous per-unit bound R1:
  *       tau_col = 2*gamma(kt+bm)*kt*bm*amax*bmax,  tau_row = 2*gamma(kt+bn)*kt*bn*amax*bmax
  *     with gamma(n) = n*u/(1-n*u), u = 2^-53, kt = k accumulated so far, and amax / bmax
- *     the largest finite |op(A)_ip| / |op(B)_pj| of the unit ROUNDED UP to the largest
- *     double with the same high 32 bits (reading R1': a larger threshold is
- *     still rigorous; the rounding lets the kernel track maxima on 32-bit words).
+ *     the largest |op(A)_ip| / |op(B)_pj| of the unit ROUNDED UP to the largest double
+ *     with the same high 32 bits, a non-finite element counting as DBL_MAX (reading R1',
+ *     a larger threshold is still rigorous; the rounding lets the kernel track
+ *     maxima on 32-bit words; a unit with a non-finite input is flagged by its NaN/Inf
+ *     residual whatever the threshold).
  *   - Multi-flag units (out of the paper's one-error model) are recomputed once
  *     without re-verification (reading R6/R13).
  *   - Injected faults: acc_ij += delta after step_q rank-1 updates, with
@@ -35,6 +37,7 @@
  *
  * Parity pins: tests/test_oracle.py (run with -m "not gpu").
  */
+#include <float.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -68,7 +71,7 @@ double oracle_tau(int64_t kt, int64_t len, double amax, double bmax) {
   return 2.0 * oracle_gamma(kt + len) * (double)kt * (double)len * amax * bmax;
 }
 
-/* Reading R1': max |x| over finite x, then rounded up to the largest double sharing its
+/* Reading R1': max |x| (non-finite x counting as DBL_MAX), then rounded up to the largest double sharing its
  * high 32-bit word (low word all ones).  An all-zero unit gives 0x00000000FFFFFFFF. */
 static double round_up_hi32(double m) {
   uint64_t b;
@@ -220,12 +223,14 @@ static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t 
       for (int64_t i = 0; i < bm; ++i) {
         double a = op_at(x->A, x->lda, x->tA, i0 + i, p);
         a_sum += a;
-        if (isfinite(a) && fabs(a) > amax) amax = fabs(a);
+        if (!isfinite(a)) amax = DBL_MAX;
+        else if (fabs(a) > amax) amax = fabs(a);
       }
       for (int64_t j = 0; j < bn; ++j) {
         double b = op_at(x->B, x->ldb, x->tB, p, j0 + j);
         b_sum += b;
-        if (isfinite(b) && fabs(b) > bmax) bmax = fabs(b);
+        if (!isfinite(b)) bmax = DBL_MAX;
+        else if (fabs(b) > bmax) bmax = fabs(b);
       }
 
       /* Rank-1 update of C (C_s = A(:,s) B(s,:)). */

@@ -37,7 +37,7 @@ namespace ftk {
 constexpr int BM = 128, BN = 128, BK = 16;  // MMA tile (C^f tile) and k-stage depth
 constexpr int DM = 127;                     // data rows/cols per tile; row/col DM is the checksum
 constexpr int TM = DM, TN = DM;             // verification unit (tile stride in C)
-constexpr int STAGES = 5;                 // shared-memory ring depth
+constexpr int STAGES = 6;                 // shared-memory ring depth
 constexpr int NTHREADS = 384;             // 12 warps
 constexpr int N_CS_WARPS = 4;             // checksum warps (warpgroup 0)
 constexpr int N_MMA_WARPS = 8;            // MMA warps (warpgroups 1-2)
@@ -223,66 +223,72 @@ __device__ __forceinline__ void cs_load(const double *s, int c, int lane, double
 
 // ---------------- integer (fixed-point) encode: no SIMT FP64 next to the DMMA stream.
 // A dependent DADD behind a saturated DMMA stream takes ~1000 clk on sm_100a
-// (profiles/fp64_latency_under_dmma.json), so the column / row sums e^T A, B e are formed
-// exactly-enough on the integer pipes: every element is aligned to the stage's largest
-// exponent E (finite elements only) as the integer round_toward_zero(x * 2^(1078 - E)),
-// i.e. 56 significant bits for the largest element; 128 of them sum without overflow in a
-// signed 64-bit word.  Truncation per element is below 2^-55 * max|x|, far inside the
-// rounding budget of the threshold (R1/R1').
+// (profiles/fp64_latency_under_dmma.json), so the column / row sums e^T A, B e are formed on
+// the integer pipes: each element x = (-1)^s m 2^(e-1075) (m with the hidden bit, e >= 1) is
+// aligned to the largest biased exponent E of the warp's stage slice as the integer
+// floor-toward-zero(m 2^(e-E)) (53 significant bits for the largest element), and 128 of them
+// sum without overflow in a signed 64-bit word.  Per-element truncation is below
+// 2^(E-1075) <= 2^-52 max|x|, far inside the rounding budget of the threshold (R1).
+// Non-finite elements clamp the stage maximum to that of DBL_MAX (reading R1'): such a unit's
+// residuals are NaN or Inf and it is flagged whatever the threshold.
 
-__device__ __forceinline__ uint32_t hi_word(double x) { return (uint32_t)(__double_as_longlong(x) >> 32); }
-// |x| high word for the maxima; 0 for Inf/NaN (exponent all ones), as in the oracle.
-__device__ __forceinline__ uint32_t abs_hi_finite(double x) {
-  const uint32_t h = hi_word(x) & 0x7FFFFFFFu;
-  return h < 0x7FF00000u ? h : 0u;
+__device__ __forceinline__ void split_hi_lo(double x, uint32_t &hi, uint32_t &lo) {
+  asm("mov.b64 {%0, %1}, %2;\n" : "=r"(lo), "=r"(hi) : "d"(x));
 }
-__device__ __forceinline__ long long to_fixed(double x, int eref) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
-  const int e = (int)((b >> 52) & 0x7FF);
-  const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (e ? (1ull << 52) : 0ull);
-  int d = eref - (e ? e : 1);
-  d = d < 0 ? 0 : (d > 63 ? 63 : d);
-  const long long v = (long long)((m << 3) >> d);
-  return (long long)b < 0 ? -v : v;
-}
-// S * 2^(eref - 1078) as a double (truncated to 53 bits); integer ops only on the common path.
-__device__ __forceinline__ double from_fixed(long long S, int eref) {
-  if (S == 0) return 0.0;
-  const unsigned long long sg = S < 0 ? (1ull << 63) : 0ull;
-  const unsigned long long a = S < 0 ? (unsigned long long)(-S) : (unsigned long long)S;
-  const int lz = __clzll((long long)a);
-  const int biased = eref + 8 - lz;
-  if (biased <= 0 || biased >= 2047) return ldexp((double)S, eref - 1078);  // sub/overflow: rare
-  const unsigned long long norm = a << lz;
-  return __longlong_as_double((long long)(sg | ((unsigned long long)biased << 52) | ((norm >> 11) & 0xFFFFFFFFFFFFFull)));
-}
-__device__ __forceinline__ long long shfl_xor_ll(long long v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
 
-// Column sums over the 128 x-rows for the warp's 4 k-slots (v[r][q] = X(row(l,r), 4c+q)):
-// returns the sum for k-slot 4c + lane/8 in every lane; folds max|hi| into hmax.
+// One operand slice: v[r][q] for the lane's 4 rows and the warp's 4 k-slots.  Returns the sum
+// for k-slot 4c + lane/8 in every lane; folds the slice's max |hi word| into hmax.
 __device__ __forceinline__ double cs_encode_fx(const double (&v)[4][4], int lane, uint32_t &hmax) {
-  uint32_t hm = 0;
+  uint32_t hi[4][4], lo[4][4], ex[4][4];
+  uint32_t emax = 0, hm = 0;
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) hm = max(hm, abs_hi_finite(v[r][q]));
+    for (int q = 0; q < 4; ++q) {
+      split_hi_lo(v[r][q], hi[r][q], lo[r][q]);
+      ex[r][q] = (hi[r][q] >> 20) & 0x7FFu;
+      hm = max(hm, hi[r][q] & 0x7FFFFFFFu);
+    }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  hm = min(hm, 0x7FEFFFFFu);  // Inf/NaN -> largest finite (R1')
   hmax = max(hmax, hm);
-  int eref = (int)(hm >> 20);
-  eref = eref ? eref : 1;
-  long long s[4];
+  emax = max(hm >> 20, 1u);
+  long long sum[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    s[q] = (to_fixed(v[0][q], eref) + to_fixed(v[1][q], eref)) + (to_fixed(v[2][q], eref) + to_fixed(v[3][q], eref));
+  for (int q = 0; q < 4; ++q) {
+    unsigned long long acc = 0ull;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t e = ex[r][q];
+      const uint32_t mhi = (hi[r][q] & 0x000FFFFFu) | (e ? 0x00100000u : 0u);
+      const uint32_t d = min(emax - max(e, 1u), 63u);  // e <= emax for finite elements
+      const unsigned long long m = ((unsigned long long)mhi << 32) | lo[r][q];
+      const unsigned long long sgn = (unsigned long long)(long long)(int)hi[r][q] >> 63;  // 0 or 1
+      acc += ((m >> d) ^ (0ull - sgn)) + sgn;  // +/- (m >> d), two's complement
+    }
+    sum[q] = (long long)acc;
+  }
   const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
-  const long long w0 = (b4 ? s[2] : s[0]) + shfl_xor_ll(b4 ? s[0] : s[2], 16);  // keep q in {2b4, 2b4+1}
-  const long long w1 = (b4 ? s[3] : s[1]) + shfl_xor_ll(b4 ? s[1] : s[3], 16);
-  long long z = (b3 ? w1 : w0) + shfl_xor_ll(b3 ? w0 : w1, 8);                  // keep q = 2b4 + b3
-  z += shfl_xor_ll(z, 4);
-  z += shfl_xor_ll(z, 2);
-  z += shfl_xor_ll(z, 1);
-  return from_fixed(z, eref);
+  auto sx = [](long long x, int o) { return (long long)__shfl_xor_sync(0xffffffffu, x, o); };
+  const long long w0 = (b4 ? sum[2] : sum[0]) + sx(b4 ? sum[0] : sum[2], 16);  // keep q in {2b4, 2b4+1}
+  const long long w1 = (b4 ? sum[3] : sum[1]) + sx(b4 ? sum[1] : sum[3], 16);
+  long long z = (b3 ? w1 : w0) + sx(b3 ? w0 : w1, 8);                          // keep q = 2b4 + b3
+  z += sx(z, 4);
+  z += sx(z, 2);
+  z += sx(z, 1);
+  // z * 2^(emax - 1075) as a double, truncated to 53 bits; integer ops only.
+  if (z == 0) return 0.0;
+  const unsigned long long sg = z < 0 ? (1ull << 63) : 0ull;
+  const unsigned long long a = z < 0 ? (unsigned long long)(-z) : (unsigned long long)z;
+  const int lz = __clzll((long long)a);
+  const int biased = (int)emax + 11 - lz;  // exponent of the leading bit, biased
+  const unsigned long long norm = a << lz;  // leading one at bit 63
+  unsigned long long bits;
+  if (biased >= 2047) bits = 0x7FF0000000000000ull;                                    // overflow
+  else if (biased >= 1) bits = ((unsigned long long)biased << 52) | ((norm >> 11) & 0xFFFFFFFFFFFFFull);
+  else bits = (1 - biased) < 53 ? ((norm >> 11) >> (1 - biased)) : 0ull;               // subnormal
+  return __longlong_as_double((long long)(sg | bits));
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -352,6 +358,10 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           else if (!mbar_test(&tl.empty[slot], par)) break;
         }
         double *sa = ring + slot * STAGE_ELEMS;
+        if (P.dev_prof && x.tile == 0 && produced < 64) P.dev_prof[100000 + produced * 8 + 0] = clock64();
+#ifdef FTK_PRODUCER_FENCE
+        if (FT) fence_proxy_async();  // order earlier generic checksum-row writes before the refill
+#endif
         mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
         const int k0 = produced * BK;
         const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
@@ -379,32 +389,38 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         const long long t0 = P.dev_prof ? clock64() : 0;
         mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
+        if (P.dev_prof && x.tile == 0 && s < 64 && lane == 0) P.dev_prof[100000 + s * 8 + 1 + warp] = t1;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
+#ifndef FTK_EXP_NOENCODE
         double v[4][4];
         // The checksum row cr (127, or 0 for odd tiles) holds a neighbour tile's data: it is
         // staged row 127 = lane 31 / r 3, or staged row 0 = lane 0 / r 0, in both layouts.
         const bool xa_l = x.cra ? lane == 31 : lane == 0, xb_l = x.crb ? lane == 31 : lane == 0;
         const int xa_r = x.cra ? 3 : 0, xb_r = x.crb ? 3 : 0;
         cs_load<AKM>(sA, c, lane, v);  // encode A: e^T A_I over the 127 data rows
-        if (xa_l) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[xa_r][q] = 0.0;
-        }
+        for (int r = 0; r < 4; ++r)  // constant indices only: v must stay in registers
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[r][q] = (xa_l && r == xa_r) ? 0.0 : v[r][q];
         const double asum = cs_encode_fx(v, lane, amax_hi);
         cs_load<BKM>(sB, c, lane, v);  // encode B: B_J e over the 127 data columns
-        if (xb_l) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[xb_r][q] = 0.0;
-        }
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[r][q] = (xb_l && r == xb_r) ? 0.0 : v[r][q];
         const double bsum = cs_encode_fx(v, lane, bmax_hi);
         if ((lane & 7) == 0) {  // lanes 8q hold the sums of k-slot 4c+q
           const int p = 4 * c + (lane >> 3);
           sA[sidx<AKM>(x.cra, p)] = asum;
           sB[sidx<BKM>(x.crb, p)] = bsum;
         }
+#ifndef FTK_PRODUCER_FENCE
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
+#endif
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&tl.enc[slot]);
+        if (P.dev_prof && x.tile == 0 && s < 64 && lane == 0 && warp == 1) P.dev_prof[100000 + s * 8 + 5] = clock64();
         if (P.dev_prof && lane == 0) {
           const long long t2 = clock64();
           unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + warp) * 2;
@@ -420,6 +436,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
     if (!verify) return;
     bar_sync(BAR_DECIDE, NTHREADS);     // MMA warps decided: clean / corrected / recompute
+#ifdef FTK_EXP_NOENCODE
+    return;
+#endif
     if (!tl.retry) return;
   }
 }
@@ -480,7 +499,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       // The protected pass waits for the encoded stage (TMA bytes + checksum row/column).
       if (verify) mbar_wait(&tl.enc[slot], (gs / STAGES) & 1);
       else mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
-      if (P.dev_prof) { const long long t1 = clock64(); w_wait += t1 - t0; w_work -= t1; }
+      if (P.dev_prof) { const long long t1 = clock64(); w_wait += t1 - t0; w_work -= t1;
+        if (x.tile == 0 && s < 64 && lane == 0 && mw == 0) P.dev_prof[100000 + s * 8 + 6] = t1; }
       if (inject) apply_faults(s);
       const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
 #pragma unroll
@@ -497,7 +517,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tl.empty[slot]);
-      if (P.dev_prof) w_work += clock64();
+      if (P.dev_prof) { const long long t2 = clock64(); w_work += t2;
+        if (x.tile == 0 && s < 64 && lane == 0 && mw == 0) P.dev_prof[100000 + s * 8 + 7] = t2; }
     }
     if (P.dev_prof && lane == 0) {
       unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + x.warp) * 2;
@@ -520,6 +541,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         }
     }
     bar_sync(BAR_CTILE, 256);
+#ifdef FTK_EXP_NOENCODE
+    if (verify) { bar_sync(BAR_DECIDE, NTHREADS); break; }
+#endif
     if (!verify) break;
 
     // ---- verification: reference checksums r from the computed C_IJ against

@@ -40,8 +40,9 @@ def unit_tau(A, B, ta, tb, i, j, BM, BN, k):
     I0, J0 = (i // BM) * BM, (j // BN) * BN
     Ia, Jb = oA[I0:I0 + BM, :], oB[:, J0:J0 + BN]
     import oracle
-    amax = oracle.round_up_hi32(float(np.abs(Ia[np.isfinite(Ia)]).max(initial=0.0)))
-    bmax = oracle.round_up_hi32(float(np.abs(Jb[np.isfinite(Jb)]).max(initial=0.0)))
+    big = np.finfo(np.float64).max
+    amax = oracle.round_up_hi32(float(np.where(np.isfinite(Ia), np.abs(Ia), big).max(initial=0.0)))
+    bmax = oracle.round_up_hi32(float(np.where(np.isfinite(Jb), np.abs(Jb), big).max(initial=0.0)))
     bm, bn = Ia.shape[0], Jb.shape[1]
     g = lambda nn: nn * U / (1 - nn * U)  # noqa: E731
     return (2 * g(k + bm) * k * bm * amax * bmax, 2 * g(k + bn) * k * bn * amax * bmax)
