@@ -37,7 +37,7 @@ namespace ftk {
 constexpr int BM = 128, BN = 128, BK = 16;  // MMA tile (C^f tile) and k-stage depth
 constexpr int DM = 127;                     // data rows/cols per tile; row/col DM is the checksum
 constexpr int TM = DM, TN = DM;             // verification unit (tile stride in C)
-constexpr int STAGES = 6;                 // shared-memory ring depth
+constexpr int STAGES = 6;                 // shared-memory ring depth (6 x 32 KB)
 constexpr int NTHREADS = 384;             // 12 warps
 constexpr int N_CS_WARPS = 4;             // checksum warps (warpgroup 0)
 constexpr int N_MMA_WARPS = 8;            // MMA warps (warpgroups 1-2)
@@ -358,10 +358,6 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           else if (!mbar_test(&tl.empty[slot], par)) break;
         }
         double *sa = ring + slot * STAGE_ELEMS;
-        if (P.dev_prof && x.tile == 0 && produced < 64) P.dev_prof[100000 + produced * 8 + 0] = clock64();
-#ifdef FTK_PRODUCER_FENCE
-        if (FT) fence_proxy_async();  // order earlier generic checksum-row writes before the refill
-#endif
         mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
         const int k0 = produced * BK;
         const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
@@ -389,9 +385,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         const long long t0 = P.dev_prof ? clock64() : 0;
         mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
-        if (P.dev_prof && x.tile == 0 && s < 64 && lane == 0) P.dev_prof[100000 + s * 8 + 1 + warp] = t1;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
-#ifndef FTK_EXP_NOENCODE
         double v[4][4];
         // The checksum row cr (127, or 0 for odd tiles) holds a neighbour tile's data: it is
         // staged row 127 = lane 31 / r 3, or staged row 0 = lane 0 / r 0, in both layouts.
@@ -414,13 +408,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           sA[sidx<AKM>(x.cra, p)] = asum;
           sB[sidx<BKM>(x.crb, p)] = bsum;
         }
-#ifndef FTK_PRODUCER_FENCE
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
-#endif
-#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&tl.enc[slot]);
-        if (P.dev_prof && x.tile == 0 && s < 64 && lane == 0 && warp == 1) P.dev_prof[100000 + s * 8 + 5] = clock64();
         if (P.dev_prof && lane == 0) {
           const long long t2 = clock64();
           unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + warp) * 2;
@@ -436,9 +426,6 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
     if (!verify) return;
     bar_sync(BAR_DECIDE, NTHREADS);     // MMA warps decided: clean / corrected / recompute
-#ifdef FTK_EXP_NOENCODE
-    return;
-#endif
     if (!tl.retry) return;
   }
 }
@@ -499,8 +486,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       // The protected pass waits for the encoded stage (TMA bytes + checksum row/column).
       if (verify) mbar_wait(&tl.enc[slot], (gs / STAGES) & 1);
       else mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
-      if (P.dev_prof) { const long long t1 = clock64(); w_wait += t1 - t0; w_work -= t1;
-        if (x.tile == 0 && s < 64 && lane == 0 && mw == 0) P.dev_prof[100000 + s * 8 + 6] = t1; }
+      if (P.dev_prof) { const long long t1 = clock64(); w_wait += t1 - t0; w_work -= t1; }
       if (inject) apply_faults(s);
       const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
 #pragma unroll
@@ -517,8 +503,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tl.empty[slot]);
-      if (P.dev_prof) { const long long t2 = clock64(); w_work += t2;
-        if (x.tile == 0 && s < 64 && lane == 0 && mw == 0) P.dev_prof[100000 + s * 8 + 7] = t2; }
+      if (P.dev_prof) w_work += clock64();
     }
     if (P.dev_prof && lane == 0) {
       unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + x.warp) * 2;
@@ -541,9 +526,6 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         }
     }
     bar_sync(BAR_CTILE, 256);
-#ifdef FTK_EXP_NOENCODE
-    if (verify) { bar_sync(BAR_DECIDE, NTHREADS); break; }
-#endif
     if (!verify) break;
 
     // ---- verification: reference checksums r from the computed C_IJ against
