@@ -132,14 +132,13 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU oracle arm
-def oracle_sample(W, rank_rows, seed, units_wanted, torch, A_dev, B_dev, lda, ldb):
+def oracle_sample(W, rank_rows, seed, units_wanted, torch, A_dev, B_dev, lda, ldb, BM, BN, BK):
     """Run the oracle (as it stands) on a bounded sample of units of this workload:
     the units containing faults first, then seeded random units.  Returns
     (tflops, seconds, units, threads)."""
     import numpy as np
     import oracle
     m, n, k = rank_rows, W["n"], W["k"]
-    BM = BN = 128
     faults = W["local_faults"]
     units = []
     for (i, j, s, d) in faults:
@@ -174,10 +173,19 @@ def oracle_sample(W, rank_rows, seed, units_wanted, torch, A_dev, B_dev, lda, ld
     C0 = np.zeros(ms * ns)
     t0 = time.perf_counter()
     _, rep = oracle.dgemm_abft("N", "N", ms, ns, k, W["alpha"], A_f, ms, B_f, k, 0.0, C0, ms,
-                               BM=BM, BN=BN, BK=16, faults=sub_faults, units=sub_units)
+                               BM=BM, BN=BN, BK=BK, faults=sub_faults, units=sub_units)
     dt = time.perf_counter() - t0
     flops = 2.0 * BM * BN * k * len(units)
     return flops / dt / 1e12, dt, len(units), oracle.num_threads(), rep
+
+
+def unit_geometry():
+    """(BM, BN, BK) of the library's verification units (header constants; no GPU needed)."""
+    try:
+        from paper_2104_00897_b200 import ftblas as F
+        return F.ftblas_get_geometry()
+    except Exception:  # library not built: the documented constants
+        return 127, 127, 16
 
 
 def reference_arm(args):
@@ -190,7 +198,7 @@ def reference_arm(args):
     import synth
     W = workload(args.config, args.size, args.seed)
     k = W["k"]
-    BM = BN = 128
+    BM, BN, BK = unit_geometry()
     threads = oracle.num_threads()
     units_per_step = max(2, min(threads, 64))
     rng = np.random.default_rng(args.seed)
@@ -207,7 +215,7 @@ def reference_arm(args):
         t0 = time.perf_counter()
         oracle.dgemm_abft("N", "N", BM * units_per_step, BN, k, W["alpha"], Arows,
                           BM * units_per_step, B, k, 0.0, np.zeros((BM * units_per_step, BN)),
-                          BM * units_per_step, BM=BM, BN=BN, BK=16, faults=fl, units=units)
+                          BM * units_per_step, BM=BM, BN=BN, BK=BK, faults=fl, units=units)
         if step >= args.warmup:
             times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
@@ -217,7 +225,7 @@ def reference_arm(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": W["name"], "m": W["m"], "n": W["n"], "k": k},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{units_per_step} verification units (128x128 tiles, k={k}) "
+                             "sample": f"{units_per_step} verification units ({BM}x{BN}, k={k}) "
                                        "of the workload per step, one injected error"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -368,12 +376,13 @@ def main():
         import oracle
         nthreads = oracle.num_threads()
         # ~10-30 s of host work: every unit holding a fault plus seeded random units.
-        per_unit = 2.0 * 128 * 128 * k
-        want = args.cpu_sample_units or int(max(len({(i // 128, j // 128) for i, j, _, _ in W["local_faults"]}),
+        BM, BN, BK = F.ftblas_get_geometry()
+        per_unit = 2.0 * BM * BN * k
+        want = args.cpu_sample_units or int(max(len({(i // BM, j // BN) for i, j, _, _ in W["local_faults"]}),
                                                 min(4096, 1.5e10 * nthreads / per_unit)))
-        v, dt, nu, thr, orep = oracle_sample(W, mloc, args.seed, want, torch, A, B, lda, ldb)
+        v, dt, nu, thr, orep = oracle_sample(W, mloc, args.seed, want, torch, A, B, lda, ldb, BM, BN, BK)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
-               "sample": f"{nu} verification units (128x128, k={k}) of the workload incl. every "
+               "sample": f"{nu} verification units ({BM}x{BN}, k={k}) of the workload incl. every "
                          f"unit holding a fault; {dt:.1f} s; oracle found {orep.detected} flagged units"}
 
     achieved = flops_total / world / (kern_ms * 1e-3) / 1e12
