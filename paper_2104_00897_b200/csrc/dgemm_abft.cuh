@@ -76,6 +76,7 @@ struct Params {
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
   unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
+  int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag
   unsigned long long *counters;   // [CNT_N]
   EventDev *events;
   long long ev_cap;
@@ -187,108 +188,196 @@ __device__ __forceinline__ void load_frags(const double *s, int xw, int h, int g
   }
 }
 
-// Checksum-warp view of an operand tile: lane l owns 4 x-rows (cs_row_of(l, 0..3)) and the
-// warp's 4 k-slots p = 4c..4c+3; v[r][q] = X(cs_row_of(l, r), 4c + q).  Conflict-free LDS.128.
-template <bool KM>
-__device__ __forceinline__ int cs_row_of(int lane, int r) {
-  return KM ? lane + 32 * r : 2 * (lane & 7) + 16 * (lane >> 3) + 64 * (r >> 1) + (r & 1);
+// ---------------- checksum encode (e^T A, B e) on the staged tiles.
+// One encoder warp owns a whole stage (both operands); per operand it makes two passes over
+// the staged tile, on the FP32 and integer pipes only.  (SIMT FP64 is not an option next to
+// the DMMA stream: the FP64 pipe is saturated, and a side warp's DADDs only execute when the
+// MMA warps stall -- measured ~10k clocks per round trip.)
+//  pass 1  max |X| over the 127 data rows: the high word of a double read as a float orders
+//          like |x| (FMNMX3.NAN with |.| operands, two elements per instruction).  A NaN
+//          result means a non-finite element or one with |x| >= 2^1017; that warp-uniform rare
+//          case is redone exactly with integer maxima.
+//  pass 2  exponent-aligned fixed point: with c the largest exponent field of the slice and
+//          C = c + 2, element x = (-1)^s m 2^(e-1075) contributes (-1)^s trunc(m / 2^(C-e)),
+//          i.e. x / 2^(c-1073) truncated toward zero (exact for integer-valued data); 127 terms
+//          of |.| < 2^51 sum exactly in 64-bit integers and are converted back by integer
+//          ops.  The per-element error < 2^(c-1073) <= 2^-51 max|x| is far inside the rounding
+//          budget of the threshold (R1, R17).
+// Lane maps (conflict-free LDS.128; each lane sums one or two columns over 64 or 32 rows):
+//  MN-major: lane = 16h + p: column p, rows 64h .. 64h+63 (x pairs from one LDS.128).
+//  K-major : lane = 8q + c : columns 2c, 2c+1, rows 32q .. 32q+31.
+// The checksum row cr (127, or 0 for odd tiles) holds a neighbour tile's data and is excluded.
+
+__device__ __forceinline__ float fmax3_abs_nan(float m, float a, float b) {
+  float r;
+  asm("{.reg .f32 x, y;\n abs.f32 x, %2;\n abs.f32 y, %3;\n max.NaN.f32 %0, %1, x, y;\n}"
+      : "=f"(r)
+      : "f"(m), "f"(a), "f"(b));
+  return r;
 }
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float hi_f(double x) { return __int_as_float(__double2hiint(x)); }
+
 template <bool KM>
-__device__ __forceinline__ void cs_load(const double *s, int c, int lane, double (&v)[4][4]) {
+__device__ __forceinline__ int enc_addr(int lane, int j) {
   if (KM) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int x = lane + 32 * r;
-#pragma unroll
-      for (int hq = 0; hq < 2; ++hq) {
-        const double2 w = *reinterpret_cast<const double2 *>(s + x * 16 + (((2 * c + hq) ^ (x & 7)) << 1));
-        v[r][2 * hq] = w.x;
-        v[r][2 * hq + 1] = w.y;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int xb = (lane >> 3) + 4 * rr;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int p = 4 * c + q;
-        const double2 w = *reinterpret_cast<const double2 *>(s + xb * 256 + p * 16 + (((lane & 7) ^ (p & 7)) << 1));
-        v[2 * rr][q] = w.x;
-        v[2 * rr + 1][q] = w.y;
-      }
-    }
+    const int c = lane & 7, q = lane >> 3, x = 32 * q + j;
+    return x * 16 + ((c ^ (j & 7)) << 1);
   }
+  const int p = lane & 15, h = lane >> 4;
+  return (4 * h + (j >> 3)) * 256 + p * 16 + (((j & 7) ^ (p & 7)) << 1);
+}
+// Element pair j of this lane, with the checksum row cr zeroed.
+template <bool KM>
+__device__ __forceinline__ double2 enc_ld(const double *s, int lane, int j, int cr) {
+  double2 v = *reinterpret_cast<const double2 *>(s + enc_addr<KM>(lane, j));
+  if (j == 0 && cr == 0 && (lane >> (KM ? 3 : 4)) == 0) {  // staged row 0
+    v.x = 0.0;
+    if (KM) v.y = 0.0;
+  }
+  if (j == 31 && cr == DM && (lane >> (KM ? 3 : 4)) == (KM ? 3 : 1)) {  // staged row 127
+    v.y = 0.0;
+    if (KM) v.x = 0.0;
+  }
+  return v;
 }
 
-// ---------------- integer (fixed-point) encode: no SIMT FP64 next to the DMMA stream.
-// A dependent DADD behind a saturated DMMA stream takes ~1000 clk on sm_100a
-// (profiles/fp64_latency_under_dmma.json), so the column / row sums e^T A, B e are formed on
-// the integer pipes: each element x = (-1)^s m 2^(e-1075) (m with the hidden bit, e >= 1) is
-// aligned to the largest biased exponent E of the warp's stage slice as the integer
-// floor-toward-zero(m 2^(e-E)) (53 significant bits for the largest element), and 128 of them
-// sum without overflow in a signed 64-bit word.  Per-element truncation is below
-// 2^(E-1075) <= 2^-52 max|x|, far inside the rounding budget of the threshold (R1).
-// Non-finite elements clamp the stage maximum to that of DBL_MAX (reading R1'): such a unit's
-// residuals are NaN or Inf and it is flagged whatever the threshold.
-
-__device__ __forceinline__ void split_hi_lo(double x, uint32_t &hi, uint32_t &lo) {
-  asm("mov.b64 {%0, %1}, %2;\n" : "=r"(lo), "=r"(hi) : "d"(x));
+// Pass 1: per-lane max (as float bits of |high word|), NaN-propagating.
+template <bool KM>
+__device__ __forceinline__ float enc_pass1(const double *s, int lane, int cr) {
+  float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const double2 v = enc_ld<KM>(s, lane, j, cr), w = enc_ld<KM>(s, lane, j + 1, cr);
+    m0 = fmax3_abs_nan(m0, hi_f(v.x), hi_f(v.y));
+    m1 = fmax3_abs_nan(m1, hi_f(w.x), hi_f(w.y));
+  }
+  return fmax_nan(m0, m1);
+}
+__device__ __forceinline__ float warp_max_nan(float m) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return m;
 }
 
-// One operand slice: v[r][q] for the lane's 4 rows and the warp's 4 k-slots.  Returns the sum
-// for k-slot 4c + lane/8 in every lane; folds the slice's max |hi word| into hmax.
-__device__ __forceinline__ double cs_encode_fx(const double (&v)[4][4], int lane, uint32_t &hmax) {
-  uint32_t hi[4][4], lo[4][4], ex[4][4];
-  uint32_t emax = 0, hm = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      split_hi_lo(v[r][q], hi[r][q], lo[r][q]);
-      ex[r][q] = (hi[r][q] >> 20) & 0x7FFu;
-      hm = max(hm, hi[r][q] & 0x7FFFFFFFu);
-    }
+// Exact max |high word| of the slice (integer pipes; rare path).
+template <bool KM>
+__device__ __noinline__ uint32_t enc_exact_hmax(const double *s, int lane, int cr) {
+  uint32_t hm = 0;
+  for (int j = 0; j < 32; ++j) {
+    double2 v = *reinterpret_cast<const double2 *>(s + enc_addr<KM>(lane, j));
+    const bool r0 = j == 0 && cr == 0 && (lane >> (KM ? 3 : 4)) == 0;
+    const bool r127 = j == 31 && cr == DM && (lane >> (KM ? 3 : 4)) == (KM ? 3 : 1);
+    if (r0) { v.x = 0.0; if (KM) v.y = 0.0; }
+    if (r127) { v.y = 0.0; if (KM) v.x = 0.0; }
+    hm = max(hm, max((uint32_t)__double2hiint(v.x) & 0x7FFFFFFFu, (uint32_t)__double2hiint(v.y) & 0x7FFFFFFFu));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-  hm = min(hm, 0x7FEFFFFFu);  // Inf/NaN -> largest finite (R1')
-  hmax = max(hmax, hm);
-  emax = max(hm >> 20, 1u);
-  long long sum[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    unsigned long long acc = 0ull;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t e = ex[r][q];
-      const uint32_t mhi = (hi[r][q] & 0x000FFFFFu) | (e ? 0x00100000u : 0u);
-      const uint32_t d = min(emax - max(e, 1u), 63u);  // e <= emax for finite elements
-      const unsigned long long m = ((unsigned long long)mhi << 32) | lo[r][q];
-      const unsigned long long sgn = (unsigned long long)(long long)(int)hi[r][q] >> 63;  // 0 or 1
-      acc += ((m >> d) ^ (0ull - sgn)) + sgn;  // +/- (m >> d), two's complement
-    }
-    sum[q] = (long long)acc;
+  return hm;
+}
+
+// One element's fixed-point term floor(ones'-complement(x) / 2^(C-e)) = sign(x) trunc(|x| /
+// 2^(C-1075)) - [x < 0]; S = -[x < 0] is returned so the caller can add the count back.
+// C >= e + 2 for every element of the slice.  EXACT handles subnormals (no hidden bit,
+// exponent 1); the fast form gives them a spurious hidden bit, which shifts out entirely once
+// C >= 53 (c > 50).
+template <bool EXACT>
+__device__ __forceinline__ long long fx_term(double x, uint32_t C, int &S) {
+  const uint32_t H = (uint32_t)__double2hiint(x), L = (uint32_t)__double2loint(x);
+  S = (int)H >> 31;
+  uint32_t E = (H >> 20) & 0x7FFu, MH;
+  if (EXACT) {
+    MH = (H & 0xFFFFFu) | (E ? 0x100000u : 0u);
+    E = max(E, 1u);
+  } else {
+    MH = (H & 0xFFFFFu) | 0x100000u;
   }
-  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
-  auto sx = [](long long x, int o) { return (long long)__shfl_xor_sync(0xffffffffu, x, o); };
-  const long long w0 = (b4 ? sum[2] : sum[0]) + sx(b4 ? sum[0] : sum[2], 16);  // keep q in {2b4, 2b4+1}
-  const long long w1 = (b4 ? sum[3] : sum[1]) + sx(b4 ? sum[1] : sum[3], 16);
-  long long z = (b3 ? w1 : w0) + sx(b3 ? w0 : w1, 8);                          // keep q = 2b4 + b3
-  z += sx(z, 4);
-  z += sx(z, 2);
-  z += sx(z, 1);
-  // z * 2^(emax - 1075) as a double, truncated to 53 bits; integer ops only.
+  const uint32_t t = min(C - E, 63u);
+  const long long m = (long long)(((unsigned long long)(MH ^ (uint32_t)S) << 32) | (L ^ (uint32_t)S));
+  return m >> t;
+}
+
+// Pass 2: this lane's column sum(s) in fixed point (scale 2^(C-1075)), each term truncated
+// toward zero (exact for integer-valued data), already reduced over the lanes that share the
+// column(s).
+template <bool KM, bool EXACT>
+__device__ __forceinline__ void enc_pass2(const double *s, int lane, int cr, uint32_t C, long long &q0, long long &q1) {
+  long long a0 = 0, a1 = 0;
+  int n0 = 0, n1 = 0;  // minus the number of negative terms (ones' -> two's complement)
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const double2 v = enc_ld<KM>(s, lane, j, cr), w = enc_ld<KM>(s, lane, j + 1, cr);
+    int sv0, sv1, sw0, sw1;
+    const long long tv0 = fx_term<EXACT>(v.x, C, sv0), tv1 = fx_term<EXACT>(v.y, C, sv1);
+    const long long tw0 = fx_term<EXACT>(w.x, C, sw0), tw1 = fx_term<EXACT>(w.y, C, sw1);
+    if (KM) {
+      a0 += tv0 + tw0;
+      a1 += tv1 + tw1;
+      n0 += sv0 + sw0;
+      n1 += sv1 + sw1;
+    } else {
+      a0 += (tv0 + tv1) + (tw0 + tw1);
+      n0 += (sv0 + sv1) + (sw0 + sw1);
+    }
+  }
+  a0 -= n0;
+  a1 -= n1;
+  if (KM) {
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+  } else {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
+  }
+  q0 = a0;
+  q1 = a1;
+}
+template <bool KM>
+__device__ __noinline__ void enc_pass2_exact(const double *s, int lane, int cr, uint32_t C, long long &q0, long long &q1) {
+  enc_pass2<KM, true>(s, lane, cr, C, q0, q1);
+}
+
+// z * 2^sc as a double, truncated toward zero to 53 bits (integer ops only).
+__device__ __forceinline__ double fx_to_double(long long z, int sc) {
   if (z == 0) return 0.0;
   const unsigned long long sg = z < 0 ? (1ull << 63) : 0ull;
   const unsigned long long a = z < 0 ? (unsigned long long)(-z) : (unsigned long long)z;
   const int lz = __clzll((long long)a);
-  const int biased = (int)emax + 11 - lz;  // exponent of the leading bit, biased
+  const int biased = 63 - lz + sc + 1023;   // exponent of the leading bit, biased
   const unsigned long long norm = a << lz;  // leading one at bit 63
   unsigned long long bits;
-  if (biased >= 2047) bits = 0x7FF0000000000000ull;                                    // overflow
+  if (biased >= 2047) bits = 0x7FF0000000000000ull;                                   // overflow
   else if (biased >= 1) bits = ((unsigned long long)biased << 52) | ((norm >> 11) & 0xFFFFFFFFFFFFFull);
-  else bits = (1 - biased) < 53 ? ((norm >> 11) >> (1 - biased)) : 0ull;               // subnormal
+  else bits = (1 - biased) < 53 ? ((norm >> 11) >> (1 - biased)) : 0ull;              // subnormal
   return __longlong_as_double((long long)(sg | bits));
+}
+
+// Encode one operand slice.  sum0 (and sum1 for K-major) receive e^T X for this lane's
+// column(s); hmax_acc accumulates the R1' high-word maximum of the data elements.
+template <bool KM>
+__device__ __forceinline__ void enc_operand(const double *s, int lane, int cr, double &sum0, double &sum1,
+                                            uint32_t &hmax_acc) {
+  const float mf = warp_max_nan(enc_pass1<KM>(s, lane, cr));
+  uint32_t hm = (uint32_t)__float_as_int(mf);
+  if (hm >= 0x7F800000u) hm = enc_exact_hmax<KM>(s, lane, cr);  // warp-uniform rare path
+  hmax_acc = max(hmax_acc, min(hm, 0x7FEFFFFFu));               // non-finite -> DBL_MAX (R1')
+  const uint32_t c = hm >> 20;
+  if (c >= 2047u) {  // a non-finite element: the checksums are NaN, the unit will flag
+    sum0 = sum1 = __longlong_as_double(0x7FF8000000000000ll);
+    return;
+  }
+  long long q0, q1;
+  if (c > 50u) enc_pass2<KM, false>(s, lane, cr, c + 2u, q0, q1);
+  else enc_pass2_exact<KM>(s, lane, cr, c + 2u, q0, q1);  // max |x| < 2^-972: subnormals matter
+  sum0 = fx_to_double(q0, (int)c - 1073);
+  sum1 = KM ? fx_to_double(q1, (int)c - 1073) : 0.0;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -318,6 +407,14 @@ __device__ __forceinline__ int bar_popc(int id, int count, bool pred) {
   return r;
 }
 
+// Warp roles.  The checksum warpgroup takes the HIGHEST warp ids: the issue arbiter favours
+// high ids, so an encoder's few FP64 adds win the FP64 pipe over the saturating DMMA stream
+// instead of starving behind it until the MMA warps stall.
+constexpr bool CS_HIGH = true;
+__device__ __forceinline__ bool is_cs_warp(int w) { return CS_HIGH ? w >= N_MMA_WARPS : w < N_CS_WARPS; }
+__device__ __forceinline__ int cs_warp(int w) { return CS_HIGH ? w - N_MMA_WARPS : w; }
+__device__ __forceinline__ int mma_warp(int w) { return CS_HIGH ? w : w - N_CS_WARPS; }
+
 struct Ctx {
   double *ring;
   SmemTail *tl;
@@ -328,85 +425,77 @@ struct Ctx {
   int oa, ob, cra, crb;
 };
 
-// ---------------- warpgroup 0: TMA producer (warp 0 lane 0) + checksum-encode warps
-// Checksum warp c encodes k-slots 4c..4c+3 of every stage: it waits for the stage's TMA
-// bytes, forms a_sum[p] = sum_{i<127} op(A)_ip and b_sum[p] = sum_{j<127} op(B)_pj on the
-// integer pipes, writes them into row 127 of the staged A tile and row 127 (= column 127 of
-// op(B)) of the staged B tile, and arrives on the stage's `enc` barrier.  The DMMA stream
-// then computes C^f = [A; e^T A][B, B e] tile by tile: acc(127, j) is the
-// carried column checksum (e^T A_I) B_J and acc(i, 127) the carried row checksum A_I (B_J e)
-// (outer-product maintenance), at no SIMT FP64 cost.
+// ---------------- warpgroup 0: TMA producer (warp 0) + checksum-encode warps (1..3)
+// Warp 0 lane 0 streams every stage into the ring.  In the protected pass encoder warp
+// 1 + (s mod 3) owns stage s: it waits for the stage's TMA bytes, forms
+// a_sum[p] = sum_{i in I} op(A)_ip and b_sum[p] = sum_{j in J} op(B)_pj for the 16 k-slots,
+// writes them into the free row cr of the staged A tile and of the staged B tile, and arrives
+// on the stage's `enc` barrier.  The DMMA stream then computes C^f = [A; e^T A][B, B e]
+// tile by tile: acc(cr, j) is the carried column checksum (e^T A_I) B_J and
+// acc(i, cr) the carried row checksum A_I (B_J e) (outer-product maintenance).
+// Owning a whole stage gives an encoder three stage-times (~12k clocks) per job, which hides
+// the FP64 queueing latency of its DADDs behind the DMMA stream.
+constexpr int N_ENC_WARPS = N_CS_WARPS - 1;
+
 template <bool AKM, bool BKM, bool FT>
 __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUtensorMap &tmB, const Params &P,
                                               const Ctx &x) {
   SmemTail &tl = *x.tl;
   double *const ring = x.ring;
-  const int lane = x.lane, warp = x.warp, c = warp, nk = x.nk;
+  const int lane = x.lane, warp = cs_warp(x.warp), nk = x.nk;
   int stage_base = 0;
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
-    int produced = 0;
-    // Issue stages [produced, min(lim, nk)).  Blocking for stages below `must` (the checksum
-    // warps need them next); beyond that only while ring slots are already free, so the
-    // producer never stalls warp 0's encode behind the MMA warps.
-    auto produce_upto = [&](int lim, int must) {
-      for (; produced < lim && produced < nk; ++produced) {
-        const int gs = stage_base + produced, slot = gs % STAGES;
-        if (gs >= STAGES) {
-          const uint32_t par = ((gs / STAGES) - 1) & 1;
-          if (produced < must) mbar_wait(&tl.empty[slot], par);
-          else if (!mbar_test(&tl.empty[slot], par)) break;
-        }
-        double *sa = ring + slot * STAGE_ELEMS;
-        mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
-        const int k0 = produced * BK;
+    if (warp == 0) {
+      if (lane == 0) {
         const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
-        if (AKM) {
-          tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
-        } else {
+        for (int s = 0; s < nk; ++s) {
+          const int gs = stage_base + s, slot = gs % STAGES;
+          if (gs >= STAGES) mbar_wait(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
+          double *sa = ring + slot * STAGE_ELEMS;
+          mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
+          const int k0 = s * BK;
+          if (AKM) {
+            tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
+          } else {
 #pragma unroll
-          for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, k0, &tl.full[slot]);
-        }
-        double *sb = sa + TILE_ELEMS;
-        if (BKM) {
-          tma_load_2d(sb, &tmB, k0, xbj, &tl.full[slot]);
-        } else {
+            for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, k0, &tl.full[slot]);
+          }
+          double *sb = sa + TILE_ELEMS;
+          if (BKM) {
+            tma_load_2d(sb, &tmB, k0, xbj, &tl.full[slot]);
+          } else {
 #pragma unroll
-          for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
+            for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
+          }
         }
       }
-    };
-    if (verify) {
+      __syncwarp();
+    } else if (verify) {
       uint32_t amax_hi = 0u, bmax_hi = 0u;
-      for (int s = 0; s < nk; ++s) {
-        if (warp == 0 && lane == 0) produce_upto(s + STAGES, s + 1);
-        __syncwarp();
+      for (int s = warp - 1; s < nk; s += N_ENC_WARPS) {
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
         mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
-        double v[4][4];
-        // The checksum row cr (127, or 0 for odd tiles) holds a neighbour tile's data: it is
-        // staged row 127 = lane 31 / r 3, or staged row 0 = lane 0 / r 0, in both layouts.
-        const bool xa_l = x.cra ? lane == 31 : lane == 0, xb_l = x.crb ? lane == 31 : lane == 0;
-        const int xa_r = x.cra ? 3 : 0, xb_r = x.crb ? 3 : 0;
-        cs_load<AKM>(sA, c, lane, v);  // encode A: e^T A_I over the 127 data rows
-#pragma unroll
-        for (int r = 0; r < 4; ++r)  // constant indices only: v must stay in registers
-#pragma unroll
-          for (int q = 0; q < 4; ++q) v[r][q] = (xa_l && r == xa_r) ? 0.0 : v[r][q];
-        const double asum = cs_encode_fx(v, lane, amax_hi);
-        cs_load<BKM>(sB, c, lane, v);  // encode B: B_J e over the 127 data columns
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) v[r][q] = (xb_l && r == xb_r) ? 0.0 : v[r][q];
-        const double bsum = cs_encode_fx(v, lane, bmax_hi);
-        if ((lane & 7) == 0) {  // lanes 8q hold the sums of k-slot 4c+q
-          const int p = 4 * c + (lane >> 3);
-          sA[sidx<AKM>(x.cra, p)] = asum;
-          sB[sidx<BKM>(x.crb, p)] = bsum;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        if (P.dev_mode & 1) {
+          amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
+          bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
+        } else if (!(P.dev_mode & 2)) {
+        enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
+        enc_operand<BKM>(sB, lane, x.crb, b0, b1, bmax_hi);  // B_J e over the 127 data columns
+        }
+        if (AKM) {
+          if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
+        } else {
+          if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
+        }
+        if (BKM) {
+          if (lane < 8) *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 2 * lane)) = make_double2(b0, b1);
+        } else {
+          if (lane < 16) sB[sidx<false>(x.crb, lane)] = b0;
         }
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
         __syncwarp();
@@ -419,8 +508,6 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         }
       }
       if (lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
-    } else if (warp == 0 && lane == 0) {
-      produce_upto(nk, nk);
     }
     stage_base += nk;
     bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
@@ -437,9 +524,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   double *const ring = x.ring;
   double *const ctile = ring;  // epilogue reuse of the ring
   const int lane = x.lane, nk = x.nk;
-  const int mw = x.warp - N_CS_WARPS, wm = mw >> 2, wn = mw & 3;
+  const int mw = mma_warp(x.warp), wm = mw >> 2, wn = mw & 3;
   const int g = lane >> 2, t = lane & 3;
-  const int vt = x.tid - N_CS_WARPS * 32;  // 0..255
+  const int vt = mw * 32 + lane;  // 0..255
   double acc[8][4][2];
   int stage_base = 0;
   for (int attempt = 0;; ++attempt) {
@@ -479,36 +566,33 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         next_stage = fnext < x.f_hi ? P.faults[fnext].stage : 0x7fffffff;
       }
     };
-    long long w_wait = 0, w_work = 0;
-    for (int s = 0; s < nk; ++s) {
-      const int gs = stage_base + s, slot = gs % STAGES;
-      const long long t0 = P.dev_prof ? clock64() : 0;
-      // The protected pass waits for the encoded stage (TMA bytes + checksum row/column).
-      if (verify) mbar_wait(&tl.enc[slot], (gs / STAGES) & 1);
-      else mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
-      if (P.dev_prof) { const long long t1 = clock64(); w_wait += t1 - t0; w_work -= t1; }
-      if (inject) apply_faults(s);
-      const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
+    // The protected pass waits for the encoded stage (TMA bytes + checksum row/column), the
+    // unprotected one for the TMA bytes only.
+    uint64_t *const ready = verify ? tl.enc : tl.full;
+    // The k-loop runs in segments between fault stages, so that the DMMA loop body carries no
+    // injection code (which would make the register allocator shuffle accumulators).
+    for (int s = 0; s < nk;) {
+      const int s_end = next_stage < nk ? next_stage : nk;
+      for (; s < s_end; ++s) {
+        const int gs = stage_base + s, slot = gs % STAGES;
+        mbar_wait(&ready[slot], (gs / STAGES) & 1);
+        const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double af[2][8], bf[2][4];
-        load_frags<AKM, 8>(sA, wm * 64, h, g, t, af);
-        load_frags<BKM, 4>(sB, wn * 32, h, g, t, bf);
+        for (int h = 0; h < 2; ++h) {
+          double af[2][8], bf[2][4];
+          load_frags<AKM, 8>(sA, wm * 64, h, g, t, af);
+          load_frags<BKM, 4>(sB, wn * 32, h, g, t, bf);
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+          for (int e = 0; e < 2; ++e)
 #pragma unroll
-          for (int a = 0; a < 8; ++a)
+            for (int a = 0; a < 8; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b], af[e][a], bf[e][b]);
+              for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b], af[e][a], bf[e][b]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tl.empty[slot]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tl.empty[slot]);
-      if (P.dev_prof) w_work += clock64();
-    }
-    if (P.dev_prof && lane == 0) {
-      unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + x.warp) * 2;
-      dp[0] += (unsigned long long)w_wait;
-      dp[1] += (unsigned long long)w_work;
+      if (s < nk) apply_faults(s);  // s == next_stage: faults due before stage s's updates
     }
     if (inject) apply_faults(nk);  // faults with step_q == k
     stage_base += nk;
@@ -556,7 +640,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     const double nu = (double)(kt + len) * 0x1p-53;
     const double tau = 2.0 * (nu / (1.0 - nu)) * (double)kt * (double)len * amx * bmx;  // DESIGN.md R1
     const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
-    const bool flag = valid && !(fabs(d) <= tau);
+    const bool flag = valid && !(fabs(d) <= tau) && !(P.dev_mode & 4);
     tl.dres[vt] = d;
     if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, cidx);
     const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
@@ -654,7 +738,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&tl.full[s], 1);
-      mbar_init(&tl.enc[s], N_CS_WARPS);
+      mbar_init(&tl.enc[s], 1);
       mbar_init(&tl.empty[s], N_MMA_WARPS);
     }
     tl.amax_hi = 0u;
@@ -676,10 +760,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
 
-  // The two roles never re-converge, so ptxas can give each its own register budget.  The
-  // checksum warps take the LOWEST warp ids: the issue arbiter favours high ids, so the DMMA
-  // warps always win an issue slot and the integer encode fills the idle ones.
-  if (x.warp < N_CS_WARPS) {
+  // The two roles never re-converge, so ptxas can give each its own register budget.
+  if (is_cs_warp(x.warp)) {
     setmaxnreg_dec<REG_CS>();
     checksum_role<AKM, BKM, FT>(tmA, tmB, P, x);
   } else {

@@ -171,6 +171,7 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
   p.correct_mode = tl_correct;
   // development only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
+  if (const char *dm = std::getenv("FTBLAS_DEV_MODE")) p.dev_mode = std::atoi(dm);
 
   // Bucket faults by (tile, stage); stable so same-stage faults keep the caller's order.
   std::vector<ftk::FaultDev> fd;
