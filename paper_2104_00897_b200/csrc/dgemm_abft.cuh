@@ -38,6 +38,7 @@ constexpr int BM = 128, BN = 128, BK = 16;  // MMA tile (C^f tile) and k-stage d
 constexpr int DM = 127;                     // data rows/cols per tile; row/col DM is the checksum
 constexpr int TM = DM, TN = DM;             // verification unit (tile stride in C)
 constexpr int STAGES = 6;                 // shared-memory ring depth (6 x 32 KB)
+constexpr int RASTER_G = 12;              // tile rows per raster band (grouped CTA order)
 constexpr int NTHREADS = 384;             // 12 warps
 constexpr int N_CS_WARPS = 4;             // checksum warps (warpgroup 0)
 constexpr int N_MMA_WARPS = 8;            // MMA warps (warpgroups 1-2)
@@ -76,7 +77,8 @@ struct Params {
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
   unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
-  int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag
+  int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
+                                  // 8 MMA waits for the TMA bytes only
   unsigned long long *counters;   // [CNT_N]
   EventDev *events;
   long long ev_cap;
@@ -425,17 +427,18 @@ struct Ctx {
   int oa, ob, cra, crb;
 };
 
-// ---------------- warpgroup 0: TMA producer (warp 0) + checksum-encode warps (1..3)
-// Warp 0 lane 0 streams every stage into the ring.  In the protected pass encoder warp
-// 1 + (s mod 3) owns stage s: it waits for the stage's TMA bytes, forms
+// ---------------- checksum warpgroup: four encoder warps, each also its stages' TMA producer
+// Encoder warp w owns stages s = w (mod 4).  It issues the TMA loads of its own stages (lane
+// 0: the first ring's worth up front, then stage s + 4 once the MMA warps have released that
+// ring slot) and, in the protected pass, waits for stage s's bytes, forms
 // a_sum[p] = sum_{i in I} op(A)_ip and b_sum[p] = sum_{j in J} op(B)_pj for the 16 k-slots,
 // writes them into the free row cr of the staged A tile and of the staged B tile, and arrives
 // on the stage's `enc` barrier.  The DMMA stream then computes C^f = [A; e^T A][B, B e]
 // tile by tile: acc(cr, j) is the carried column checksum (e^T A_I) B_J and
 // acc(i, cr) the carried row checksum A_I (B_J e) (outer-product maintenance).
-// Owning a whole stage gives an encoder three stage-times (~12k clocks) per job, which hides
-// the FP64 queueing latency of its DADDs behind the DMMA stream.
-constexpr int N_ENC_WARPS = N_CS_WARPS - 1;
+// One encoder per SM sub-partition spreads the encode's issue slots evenly over the four DMMA
+// streams, and owning every fourth stage leaves ~4 stage-times per encode job.
+constexpr int N_ENC_WARPS = N_CS_WARPS;
 
 template <bool AKM, bool BKM, bool FT>
 __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUtensorMap &tmB, const Params &P,
@@ -443,49 +446,48 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   SmemTail &tl = *x.tl;
   double *const ring = x.ring;
   const int lane = x.lane, warp = cs_warp(x.warp), nk = x.nk;
+  const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
   int stage_base = 0;
+  // Lane 0: load stage s into its ring slot once the slot's previous stage is consumed.
+  auto issue = [&](int s) {
+    const int gs = stage_base + s, slot = gs % STAGES;
+    if (gs >= STAGES) mbar_wait(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
+    double *sa = ring + slot * STAGE_ELEMS;
+    mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
+    const int k0 = s * BK;
+    if (AKM) {
+      tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
+    } else {
+#pragma unroll
+      for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, k0, &tl.full[slot]);
+    }
+    double *sb = sa + TILE_ELEMS;
+    if (BKM) {
+      tma_load_2d(sb, &tmB, k0, xbj, &tl.full[slot]);
+    } else {
+#pragma unroll
+      for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
+    }
+  };
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
-    if (warp == 0) {
-      if (lane == 0) {
-        const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
-        for (int s = 0; s < nk; ++s) {
-          const int gs = stage_base + s, slot = gs % STAGES;
-          if (gs >= STAGES) mbar_wait(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
-          double *sa = ring + slot * STAGE_ELEMS;
-          mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
-          const int k0 = s * BK;
-          if (AKM) {
-            tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
-          } else {
-#pragma unroll
-            for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, k0, &tl.full[slot]);
-          }
-          double *sb = sa + TILE_ELEMS;
-          if (BKM) {
-            tma_load_2d(sb, &tmB, k0, xbj, &tl.full[slot]);
-          } else {
-#pragma unroll
-            for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
-          }
-        }
-      }
-      __syncwarp();
-    } else if (verify) {
-      uint32_t amax_hi = 0u, bmax_hi = 0u;
-      for (int s = warp - 1; s < nk; s += N_ENC_WARPS) {
+    if (lane == 0)
+      for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
+    uint32_t amax_hi = 0u, bmax_hi = 0u;
+    for (int s = warp; s < nk; s += N_ENC_WARPS) {
+      if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
         mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-        if (P.dev_mode & 1) {
+        if (P.dev_mode & 1) {  // development: pass 1 only
           amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
           bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
         } else if (!(P.dev_mode & 2)) {
-        enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
-        enc_operand<BKM>(sB, lane, x.crb, b0, b1, bmax_hi);  // B_J e over the 127 data columns
+          enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
+          enc_operand<BKM>(sB, lane, x.crb, b0, b1, bmax_hi);  // B_J e over the 127 data columns
         }
         if (AKM) {
           if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
@@ -502,13 +504,16 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         if (lane == 0) mbar_arrive(&tl.enc[slot]);
         if (P.dev_prof && lane == 0) {
           const long long t2 = clock64();
-          unsigned long long *dp = P.dev_prof + ((size_t)(blockIdx.x + blockIdx.y * gridDim.x) * 12 + warp) * 2;
+          unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + warp) * 2;
           dp[0] += (unsigned long long)(t1 - t0);
           dp[1] += (unsigned long long)(t2 - t1);
         }
       }
-      if (lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
+      const int s2 = s + N_ENC_WARPS;  // this warp's next stage beyond the first ring
+      if (lane == 0 && s2 >= STAGES && s2 < nk) issue(s2);
+      __syncwarp();
     }
+    if (verify && lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
     stage_base += nk;
     bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
     if (!verify) return;
@@ -568,7 +573,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     };
     // The protected pass waits for the encoded stage (TMA bytes + checksum row/column), the
     // unprotected one for the TMA bytes only.
-    uint64_t *const ready = verify ? tl.enc : tl.full;
+    uint64_t *const ready = (verify && !(P.dev_mode & 8)) ? tl.enc : tl.full;
     // The k-loop runs in segments between fault stages, so that the DMMA loop body carries no
     // injection code (which would make the register allocator shuffle accumulators).
     for (int s = 0; s < nk;) {
@@ -717,7 +722,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   x.tid = threadIdx.x;
   x.lane = x.tid & 31;
   x.warp = x.tid >> 5;
-  const int ti = blockIdx.x, tj = blockIdx.y;
+  // Grouped raster: CTAs run in bands of RASTER_G tile rows, column by column inside a band,
+  // so that one wave of 148 CTAs touches ~12 A row panels and ~12 B column panels (L2 reuse)
+  // instead of 148 A panels and one B panel.
+  int ti, tj;
+  {
+    const int L = blockIdx.x, band_tiles = RASTER_G * P.tiles_n, band = L / band_tiles;
+    const int within = L - band * band_tiles, rows = min(RASTER_G, P.tiles_m - band * RASTER_G);
+    ti = band * RASTER_G + within % rows;
+    tj = within / rows;
+  }
   x.tile = ti + tj * P.tiles_m;
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.

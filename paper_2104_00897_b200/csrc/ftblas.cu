@@ -120,7 +120,7 @@ int check_args(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, 
   if (ldc < std::max<int64_t>(1, m)) return -13;
   // Index arithmetic inside the kernels uses int for tile coordinates.
   if ((m + ftk::TM - 1) / ftk::TM > 0x7fffffff) return -3;
-  if ((n + ftk::TN - 1) / ftk::TN > 65535) return -4;
+  if (((m + ftk::TM - 1) / ftk::TM) * ((n + ftk::TN - 1) / ftk::TN) > 0x7fffffff) return -4;
   return 0;
 }
 
@@ -224,7 +224,7 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
   CUtensorMap tmA, tmB;
   if (int e = make_tmap(&tmA, p.A, p.lda, akm, m, k)) return e;
   if (int e = make_tmap(&tmB, p.B, p.ldb, bkm, n, k)) return e;
-  const dim3 grid(p.tiles_m, p.tiles_n);
+  const dim3 grid((unsigned)((int64_t)p.tiles_m * p.tiles_n));  // 1-D: grouped raster in the kernel
   int lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
   if (rA) cudaFreeAsync(rA, st);
   if (rB) cudaFreeAsync(rB, st);

@@ -15,7 +15,7 @@ B = torch.rand(N * N, dtype=torch.float64, device="cuda", generator=g)
 C = torch.zeros(N * N, dtype=torch.float64, device="cuda")
 F.ftblas_dgemm("N", "N", N, N, N, 1.0, A, N, B, N, 0.0, C, N, report=False)
 torch.cuda.synchronize()
-jobs = (N // 16) / 3.0
+jobs = (N // 16) / 4.0
 p = prof.view(ntiles, 12, 2).double().mean(0) / jobs
 print("per-job clk [wait TMA, encode] by encoder warp:",
-      " ".join(f"w{w}:{p[w,0]:.0f}/{p[w,1]:.0f}" for w in range(1, 4)), flush=True)
+      " ".join(f"w{w}:{p[w,0]:.0f}/{p[w,1]:.0f}" for w in range(0, 4)), flush=True)
