@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--seed", type=int, default=1234)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-unfused", action="store_true", help="skip the unfused ABFT baseline timing")
     p.add_argument("--cpu-sample-units", type=int, default=0)
     return p.parse_args()
 
@@ -282,12 +283,14 @@ def main():
     counters = torch.zeros(5, dtype=torch.int64, device=dev)
 
     def step(ft=True):
+        """ft: True = the fused protected kernel, False = the unprotected twin,
+        "unfused" = the unfused ABFT baseline (NEXT-2), same faults and report."""
         if beta != 0.0:
             C.copy_(C0)
         if ft:
             F.ftblas_inject_arm(W["local_faults"])
-            rep = F.ftblas_dgemm(ta, tb, mloc, n, k, alpha, A, lda, B, ldb, beta, C, mloc,
-                                 events_capacity=1024)
+            call = F.ftblas_dgemm_unfused if ft == "unfused" else F.ftblas_dgemm
+            rep = call(ta, tb, mloc, n, k, alpha, A, lda, B, ldb, beta, C, mloc, events_capacity=1024)
             counters.copy_(torch.tensor([rep.units_checked, rep.detected, rep.corrected,
                                          rep.recomputed, rep.n_events], dtype=torch.int64))
             if world > 1:
@@ -321,7 +324,16 @@ def main():
     # bracketing only the ftblas_dgemm call (report copy excluded) on the launch stream.
     with Clocks(local) as clk:
         ms_ft, launches, reps = timed(True, args.steps, args.warmup)
+    cnt = counters.cpu().tolist()  # all-reduced counters of the last protected step
     ms_noft, _, _ = timed(False, args.steps, max(1, args.warmup // 2))
+    unf = None
+    if not args.no_unfused:
+        ms_unf, _, reps_unf = timed("unfused", args.steps, max(1, args.warmup // 2))
+        ru = reps_unf[-1]
+        unf = {"tflops": 2.0 * W["m"] * n * k * args.steps / (ms_unf * 1e-3) / 1e12,
+               "overhead_pct": 100.0 * (ms_unf - ms_noft) / ms_noft, "unit": "128x128",
+               "units_checked": ru.units_checked, "detected": ru.detected, "corrected": ru.corrected,
+               "recomputed": ru.recomputed}
     kern = []
     for _ in range(max(2, min(args.steps, 3))):
         F.ftblas_inject_arm(W["local_faults"])
@@ -337,7 +349,6 @@ def main():
     tflops = flops_total * args.steps / (ms_ft * 1e-3) / 1e12
     tflops_noft = flops_total * args.steps / (ms_noft * 1e-3) / 1e12
     rep = reps[-1]
-    cnt = counters.cpu().tolist()
 
     # End to end through the public host-buffer API (pinned host memory, H2D + D2H inside).
     e2e = None
@@ -401,7 +412,8 @@ def main():
                  "overhead_pct": 100.0 * (ms_ft - ms_noft) / ms_noft,
                  "pct_of_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_TFLOPS),
                  "units_checked": cnt[0], "detected": cnt[1], "corrected": cnt[2],
-                 "recomputed": cnt[3], "events": cnt[4]},
+                 "recomputed": cnt[3], "events": cnt[4],
+                 "unfused_baseline": unf},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": "dgemm_abft_kernel (FT)", "kernel_ms": kern_ms,

@@ -102,6 +102,19 @@ int ftblas_dgemm_noft(char transA, char transB, int64_t m, int64_t n, int64_t k,
                       const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                       double *C, int64_t ldc);
 
+/* The UNFUSED ABFT baseline (§V.A): the same
+ * protection as ftblas_dgemm built from separate kernels, as in a conventional ABFT library —
+ * encode passes e^T A_I, B_J e over A and B (memory-bound), the unprotected GEMM, the
+ * carried checksums (e^T A_I) B and A (B_J e) as two skinny GEMMs, reference-sum passes
+ * e^T C_IJ, C_IJ e over the product, then verify / locate / correct per unit.  Units are
+ * 128 x 128 (err->unit_rows/unit_cols report it).  Same arguments, report, fault injection
+ * (faults land in the product GEMM), correction modes and status codes as ftblas_dgemm.
+ * When alpha != 1 or beta != 0 the product is verified in library scratch and then combined
+ * as C = alpha*T + beta*C.  Library scratch: ~8 (2 m/128 * k + 2 m n/128 ...) bytes. */
+int ftblas_dgemm_unfused(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                         const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                         double *C, int64_t ldc, ftblas_err_report_t *err);
+
 /* Same as ftblas_dgemm / ftblas_dgemm_noft but A, B, C are HOST pointers (pinned memory
  * recommended).  Copies op inputs host->device, computes, copies C device->host and
  * synchronises the stream before returning.  Device staging is library-owned. */

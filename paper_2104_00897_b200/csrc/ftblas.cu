@@ -6,6 +6,7 @@
 // dgemm_abft.cuh; this file only marshals.
 #include "../../include/ftblas.h"
 #include "dgemm_abft.cuh"
+#include "unfused.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -137,12 +138,54 @@ void zero_report(ftblas_err_report_t *err, int64_t k) {
   fill_geometry(err, k);
 }
 
-// The core entry: device pointers, protected (FT) or not.
-int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
-               const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
-               int64_t ldc, ftblas_err_report_t *err) {
+std::vector<ftblas_fault_t> take_armed() {
   std::vector<ftblas_fault_t> faults;
   if (tl_have_armed) { faults.swap(tl_armed); tl_have_armed = false; }
+  return faults;
+}
+
+// Copy the device counters / events of one call into the caller's report (events sorted by
+// (interval, i, j)).  Synchronises the stream.
+int finish_report(ftblas_err_report_t *err, const unsigned long long *d_counters, const void *d_events,
+                  int64_t ev_cap, int64_t units_checked, cudaStream_t st) {
+  unsigned long long cnt[ftk::CNT_N];
+  CUDA_TRY(cudaMemcpyAsync(cnt, d_counters, sizeof cnt, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nev = (int64_t)cnt[ftk::CNT_EVENTS];
+  const int64_t nstore = std::min<int64_t>(nev, ev_cap);
+  std::vector<ftk::EventDev> ev((size_t)nstore);
+  if (nstore > 0) {
+    CUDA_TRY(cudaMemcpyAsync(ev.data(), d_events, sizeof(ftk::EventDev) * nstore, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  std::sort(ev.begin(), ev.end(), [](const ftk::EventDev &a, const ftk::EventDev &b) {
+    if (a.interval != b.interval) return a.interval < b.interval;
+    if (a.i != b.i) return a.i < b.i;
+    return a.j < b.j;
+  });
+  err->units_checked = units_checked;
+  err->detected = (int64_t)cnt[ftk::CNT_DETECTED];
+  err->corrected = (int64_t)cnt[ftk::CNT_CORRECTED];
+  err->recomputed = (int64_t)cnt[ftk::CNT_RECOMPUTED];
+  err->n_events = nev;
+  if (err->events && err->events_capacity > 0) {
+    const int64_t ncopy = std::min<int64_t>(nstore, err->events_capacity);
+    for (int64_t e = 0; e < ncopy; ++e) {
+      err->events[e].i = ev[e].i;
+      err->events[e].j = ev[e].j;
+      err->events[e].kind = ev[e].kind;
+      err->events[e].interval = ev[e].interval;
+      err->events[e].residual_row = ev[e].residual_row;
+      err->events[e].residual_col = ev[e].residual_col;
+    }
+  }
+  return 0;
+}
+
+// The core entry: device pointers, protected (FT) or not, explicit fault list.
+int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char tb, int64_t m, int64_t n,
+               int64_t k, double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+               double *C, int64_t ldc, ftblas_err_report_t *err) {
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
   if (rc) return rc;
   zero_report(err, k);
@@ -230,40 +273,119 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
   if (rB) cudaFreeAsync(rB, st);
   if (lrc) { cudaFreeAsync(scratch, st); return lrc; }
 
-  if (err) {
-    unsigned long long cnt[ftk::CNT_N];
-    CUDA_TRY(cudaMemcpyAsync(cnt, p.counters, cnt_bytes, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    const int64_t nev = (int64_t)cnt[ftk::CNT_EVENTS];
-    const int64_t nstore = std::min<int64_t>(nev, ev_cap);
-    std::vector<ftk::EventDev> ev((size_t)nstore);
-    if (nstore > 0) {
-      CUDA_TRY(cudaMemcpyAsync(ev.data(), p.events, sizeof(ftk::EventDev) * nstore, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-    }
-    std::sort(ev.begin(), ev.end(), [](const ftk::EventDev &a, const ftk::EventDev &b) {
-      if (a.interval != b.interval) return a.interval < b.interval;
-      if (a.i != b.i) return a.i < b.i;
-      return a.j < b.j;
-    });
-    err->units_checked = ft ? (int64_t)p.tiles_m * p.tiles_n : 0;
-    err->detected = (int64_t)cnt[ftk::CNT_DETECTED];
-    err->corrected = (int64_t)cnt[ftk::CNT_CORRECTED];
-    err->recomputed = (int64_t)cnt[ftk::CNT_RECOMPUTED];
-    err->n_events = nev;
-    if (err->events && err->events_capacity > 0) {
-      const int64_t ncopy = std::min<int64_t>(nstore, err->events_capacity);
-      for (int64_t e = 0; e < ncopy; ++e) {
-        err->events[e].i = ev[e].i;
-        err->events[e].j = ev[e].j;
-        err->events[e].kind = ev[e].kind;
-        err->events[e].interval = ev[e].interval;
-        err->events[e].residual_row = ev[e].residual_row;
-        err->events[e].residual_col = ev[e].residual_col;
-      }
-    }
-  }
+  if (err)
+    if (int e = finish_report(err, p.counters, p.events, ev_cap, ft ? (int64_t)p.tiles_m * p.tiles_n : 0, st)) return e;
   CUDA_TRY(cudaFreeAsync(scratch, st));
+  return 0;
+}
+
+int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A,
+               int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+               ftblas_err_report_t *err) {
+  const std::vector<ftblas_fault_t> faults = take_armed();
+  return dgemm_core(ft, faults, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err);
+}
+
+// The unfused ABFT baseline (kernels in unfused.cuh): encode passes,
+// the unprotected GEMM, two checksum GEMMs, reference-sum passes over the product, verify.
+int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A, int64_t lda,
+                 const double *B, int64_t ldb, double beta, double *C, int64_t ldc, ftblas_err_report_t *err) {
+  const std::vector<ftblas_fault_t> faults = take_armed();
+  const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
+  if (rc) return rc;
+  if (err) {
+    err->units_checked = err->detected = err->corrected = err->recomputed = err->n_events = 0;
+    err->unit_rows = err->unit_cols = ftu::UB;
+    err->unit_k = (int32_t)std::min<int64_t>(k, INT32_MAX);
+    err->step_quantum = ftk::BK;
+  }
+  if (m == 0 || n == 0) return 0;
+  if (alpha == 0.0 || k == 0)  // C = beta*C, no ABFT
+    return dgemm_core(false, {}, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, nullptr);
+  for (const auto &f : faults)
+    if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step > k) return 3;
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  const int64_t nbm = (m + ftu::UB - 1) / ftu::UB, nbn = (n + ftu::UB - 1) / ftu::UB;
+  const int64_t ldm = (nbm + 1) & ~int64_t(1), ldn = (nbn + 1) & ~int64_t(1), ldr = (m + 1) & ~int64_t(1);
+  const bool direct = alpha == 1.0 && beta == 0.0;  // verify C itself, else a scratch product T
+  const int64_t ev_cap = std::max<int64_t>(err ? err->events_capacity : 0, 1024);
+  // scratch: counters, events, maxima, Ac, Br, CSc, CSr, Rc, Rr (+ T)
+  const size_t cnt_b = sizeof(unsigned long long) * ftk::CNT_N, ev_b = sizeof(ftk::EventDev) * ev_cap;
+  const size_t hm_b = sizeof(unsigned) * (ldm + ldn);
+  const size_t ac_b = sizeof(double) * ldm * k, br_b = sizeof(double) * ldn * k;
+  const size_t csc_b = sizeof(double) * ldm * n, csr_b = sizeof(double) * ldr * ldn;
+  const size_t rc_b = sizeof(double) * ldm * n, rr_b = sizeof(double) * ldn * m;
+  const size_t t_b = direct ? 0 : sizeof(double) * ldr * n;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t total = al(cnt_b) + al(ev_b) + al(hm_b) + al(ac_b) + al(br_b) + al(csc_b) + al(csr_b) + al(rc_b) +
+                       al(rr_b) + al(t_b);
+  char *base = nullptr;
+  CUDA_TRY(cudaMallocAsync((void **)&base, total, st));
+  char *q = base;
+  auto take = [&](size_t b) { char *r = q; q += al(b); return r; };
+  auto *counters = reinterpret_cast<unsigned long long *>(take(cnt_b));
+  void *events = take(ev_b);
+  auto *hmax = reinterpret_cast<unsigned *>(take(hm_b));
+  auto *Ac = reinterpret_cast<double *>(take(ac_b));
+  auto *Br = reinterpret_cast<double *>(take(br_b));
+  auto *CSc = reinterpret_cast<double *>(take(csc_b));
+  auto *CSr = reinterpret_cast<double *>(take(csr_b));
+  auto *Rc = reinterpret_cast<double *>(take(rc_b));
+  auto *Rr = reinterpret_cast<double *>(take(rr_b));
+  double *T = direct ? C : reinterpret_cast<double *>(take(t_b));
+  const int64_t ldt = direct ? ldc : ldr;
+  CUDA_TRY(cudaMemsetAsync(counters, 0, cnt_b, st));
+  CUDA_TRY(cudaMemsetAsync(hmax, 0, hm_b, st));
+  // Zero the padded checksum rows once so the GEMMs on them read defined values.
+  if (ldm != nbm) CUDA_TRY(cudaMemsetAsync(Ac, 0, ac_b, st));
+  if (ldn != nbn) CUDA_TRY(cudaMemsetAsync(Br, 0, br_b, st));
+
+  auto block_sum = [&](const double *X, bool xc, int64_t ld, int64_t nx, int64_t np, double *S, int64_t lds,
+                       unsigned *hm) -> int {
+    const int64_t nb = (nx + ftu::UB - 1) / ftu::UB;
+    if (xc) {
+      const dim3 g((unsigned)nb, (unsigned)((np + 31) / 32));
+      ftu::block_sum_kernel<true><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm);
+    } else {
+      const dim3 g((unsigned)nb, (unsigned)((np + 255) / 256));
+      ftu::block_sum_kernel<false><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm);
+    }
+    ++tl_launches;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  // 1. encode: e^T A_I for every row block I (x = i), B_J e for every column block J (x = j).
+  if (int e = block_sum(A, is_n(ta), lda, m, k, Ac, ldm, hmax)) return e;
+  if (int e = block_sum(B, is_t(tb), ldb, n, k, Br, ldn, hmax + ldm)) return e;
+  // 2. the product, unprotected kernel (armed faults land here).
+  if (int e = dgemm_core(false, faults, ta, tb, m, n, k, 1.0, A, lda, B, ldb, 0.0, T, ldt, nullptr)) return e;
+  // 3. carried checksums: (e^T A_I) B (nbm x n) and A (B_J e) (m x nbn), two skinny GEMMs.
+  if (int e = dgemm_core(false, {}, 'N', tb, ldm, n, k, 1.0, Ac, ldm, B, ldb, 0.0, CSc, ldm, nullptr)) return e;
+  if (int e = dgemm_core(false, {}, ta, 'T', m, ldn, k, 1.0, A, lda, Br, ldn, 0.0, CSr, ldr, nullptr)) return e;
+  // 4. reference checksums of the product: e^T T_I (x = i) and T_J e (x = j).
+  if (int e = block_sum(T, true, ldt, m, n, Rc, ldm, nullptr)) return e;
+  if (int e = block_sum(T, false, ldt, n, m, Rr, ldn, nullptr)) return e;
+  // 5. verify / locate / correct, one CTA per 128 x 128 unit.
+  ftu::VerifyParams vp{};
+  vp.m = m; vp.n = n; vp.k = k; vp.ta = is_n(ta) ? 'N' : 'T'; vp.tb = is_n(tb) ? 'N' : 'T';
+  vp.A = A; vp.lda = lda; vp.B = B; vp.ldb = ldb; vp.T = T; vp.ldt = ldt;
+  vp.Rc = Rc; vp.CSc = CSc; vp.ldm = ldm; vp.Rr = Rr; vp.ldn = ldn; vp.CSr = CSr; vp.ldr = ldr;
+  vp.amax_hi = hmax; vp.bmax_hi = hmax + ldm; vp.nbm = (int)nbm; vp.nbn = (int)nbn;
+  vp.correct_mode = tl_correct; vp.counters = counters; vp.events = events; vp.ev_cap = ev_cap;
+  ftu::verify_kernel<<<(unsigned)(nbm * nbn), 256, 0, st>>>(vp);
+  ++tl_launches;
+  CUDA_TRY(cudaGetLastError());
+  // 6. C = alpha*T + beta*C0 when the product was verified in scratch.
+  if (!direct) {
+    const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, 148 * 16);
+    ftu::axpby_kernel<<<blocks, 256, 0, st>>>(m, n, alpha, T, ldt, beta, C, ldc);
+    ++tl_launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (err)
+    if (int e = finish_report(err, counters, events, ev_cap, nbm * nbn, st)) return e;
+  CUDA_TRY(cudaFreeAsync(base, st));
   return 0;
 }
 
@@ -335,6 +457,12 @@ int ftblas_dgemm_noft(char transA, char transB, int64_t m, int64_t n, int64_t k,
                       const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                       double *C, int64_t ldc) {
   return dgemm_impl(false, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, nullptr);
+}
+
+int ftblas_dgemm_unfused(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
+                         const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                         int64_t ldc, ftblas_err_report_t *err) {
+  return unfused_impl(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err);
 }
 
 int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,

@@ -74,6 +74,7 @@ def load():
     c, i64, d, P, i32 = ctypes.c_char, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
     gemm = [c, c, i64, i64, i64, d, P, i64, P, i64, d, P, i64]
     L.ftblas_dgemm.argtypes = gemm + [ctypes.POINTER(ErrReport)]
+    L.ftblas_dgemm_unfused.argtypes = gemm + [ctypes.POINTER(ErrReport)]
     L.ftblas_dgemm_noft.argtypes = gemm
     L.ftblas_dgemm_host.argtypes = gemm + [ctypes.POINTER(ErrReport)]
     L.ftblas_dgemm_noft_host.argtypes = gemm
@@ -89,7 +90,7 @@ def load():
     L.ftblas_status_string.restype = ctypes.c_char_p
     L.ftblas_status_string.argtypes = [i32]
     L.ftblas_finalize.argtypes = []
-    for fn in ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
+    for fn in ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
                "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
                "ftblas_set_stream", "ftblas_set_correction", "ftblas_get_geometry",
                "ftblas_finalize"):
@@ -98,7 +99,7 @@ def load():
     return L
 
 
-EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
+EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
             "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
             "ftblas_set_stream", "ftblas_set_correction", "ftblas_get_geometry",
             "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize")
@@ -133,25 +134,40 @@ def _report(r: ErrReport, evbuf) -> Report:
                   r.unit_cols, r.unit_k, r.step_quantum, ev)
 
 
-def ftblas_dgemm(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *, report=True,
-                 events_capacity=4096, raw_status=False):
-    """Protected DGEMM on device pointers.  Returns a Report (synchronises the stream) or,
-    with report=False, None (asynchronous)."""
+def _protected(fn, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, report,
+               events_capacity, raw_status):
     L = load()
+    f = getattr(L, fn)
     if report:
         evbuf = (Event * max(events_capacity, 1))()
         r = ErrReport()
         r.events = evbuf
         r.events_capacity = events_capacity
-        st = L.ftblas_dgemm(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb,
-                            beta, _ptr(C), ldc, ctypes.byref(r))
+        st = f(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb, beta, _ptr(C),
+               ldc, ctypes.byref(r))
     else:
-        st = L.ftblas_dgemm(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb,
-                            beta, _ptr(C), ldc, None)
+        st = f(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb, beta, _ptr(C),
+               ldc, None)
     if raw_status:
         return st
-    _check("ftblas_dgemm", st)
+    _check(fn, st)
     return _report(r, evbuf) if report else None
+
+
+def ftblas_dgemm(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *, report=True,
+                 events_capacity=4096, raw_status=False):
+    """Protected DGEMM on device pointers.  Returns a Report (synchronises the stream) or,
+    with report=False, None (asynchronous)."""
+    return _protected("ftblas_dgemm", transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                      report, events_capacity, raw_status)
+
+
+def ftblas_dgemm_unfused(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *,
+                         report=True, events_capacity=4096, raw_status=False):
+    """The unfused ABFT baseline (NEXT-2) on device pointers; same contract as ftblas_dgemm,
+    128 x 128 verification units."""
+    return _protected("ftblas_dgemm_unfused", transA, transB, m, n, k, alpha, A, lda, B, ldb, beta,
+                      C, ldc, report, events_capacity, raw_status)
 
 
 def ftblas_dgemm_noft(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *,
