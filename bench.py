@@ -326,6 +326,17 @@ def main():
         ms_ft, launches, reps = timed(True, args.steps, args.warmup)
     cnt = counters.cpu().tolist()  # all-reduced counters of the last protected step
     ms_noft, _, _ = timed(False, args.steps, max(1, args.warmup // 2))
+    pre = None
+    if not args.no_unfused:
+        F.ftblas_set_encode(F.ENCODE_PREPASS)
+        try:
+            ms_pre, _, reps_pre = timed(True, args.steps, max(1, args.warmup // 2))
+        finally:
+            F.ftblas_set_encode(F.ENCODE_FUSED)
+        rp = reps_pre[-1]
+        pre = {"tflops": 2.0 * W["m"] * n * k * args.steps / (ms_pre * 1e-3) / 1e12,
+               "overhead_pct": 100.0 * (ms_pre - ms_noft) / ms_noft, "units_checked": rp.units_checked,
+               "detected": rp.detected, "corrected": rp.corrected, "recomputed": rp.recomputed}
     unf = None
     if not args.no_unfused:
         ms_unf, _, reps_unf = timed("unfused", args.steps, max(1, args.warmup // 2))
@@ -413,7 +424,7 @@ def main():
                  "pct_of_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_TFLOPS),
                  "units_checked": cnt[0], "detected": cnt[1], "corrected": cnt[2],
                  "recomputed": cnt[3], "events": cnt[4],
-                 "unfused_baseline": unf},
+                 "prepass_encode": pre, "unfused_baseline": unf},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": "dgemm_abft_kernel (FT)", "kernel_ms": kern_ms,

@@ -148,6 +148,18 @@ int ftblas_set_stream(void *cuda_stream);
 #define FTBLAS_CORRECT_SUBTRACT 1
 int ftblas_set_correction(int mode);
 
+/* Where ftblas_dgemm forms the checksums e^T A_I and B_J e:
+ *   FTBLAS_ENCODE_FUSED (default): in the kernel, from the very tiles staged for the MMA
+ *     (the paper's fused encoding, §V.B);
+ *   FTBLAS_ENCODE_PREPASS: two memory-bound passes over A and B before the kernel; the
+ *     kernel copies the pre-encoded 16 k-slots into the checksum row of each staged tile.
+ * Both feed the same in-kernel carry (C^f) and fused epilogue verification; results and
+ * decisions agree within the threshold (the encode sums differ only in rounding).
+ * Thread-local; returns 4 for an unknown mode. */
+#define FTBLAS_ENCODE_FUSED 0
+#define FTBLAS_ENCODE_PREPASS 1
+int ftblas_set_encode(int mode);
+
 /* Verification-unit geometry the kernels use: BM x BN tiles, step quantum BK. */
 int ftblas_get_geometry(int32_t *unit_rows, int32_t *unit_cols, int32_t *step_quantum);
 

@@ -76,6 +76,11 @@ struct Params {
   const FaultDev *faults;
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
+  // Pre-encoded checksums (encode mode PREPASS; null = encode in the kernel): e^T A_I as
+  // Ac[ti + p*ldac], B_J e as Br[tj + p*ldbr], and the per-block maxima (R1' high words).
+  const double *Ac, *Br;
+  int64_t ldac, ldbr;
+  const unsigned int *amax_pre, *bmax_pre;
   unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
   int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
                                   // 8 MMA waits for the TMA bytes only
@@ -420,7 +425,7 @@ __device__ __forceinline__ int mma_warp(int w) { return CS_HIGH ? w : w - N_CS_W
 struct Ctx {
   double *ring;
   SmemTail *tl;
-  int tid, lane, warp, tile, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi;
+  int tid, lane, warp, tile, ti, tj, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi;
   // Protected tiles: TMA boxes start at the even coordinate xs = x0 - (x0 & 1) (the contiguous
   // dimension of a TMA box must start 16-byte aligned), so tile-local data row i sits in
   // staged row i + o (o = x0 & 1) and the checksum row/column takes the free row cr.
@@ -482,22 +487,29 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-        if (P.dev_mode & 1) {  // development: pass 1 only
+        if (P.Ac) {  // PREPASS: copy the pre-encoded 16 k-slots of e^T A_I / B_J e
+          const int p = s * BK + (lane & 15);
+          const double v = p < P.k ? (lane < 16 ? P.Ac[x.ti + (int64_t)p * P.ldac] : P.Br[x.tj + (int64_t)p * P.ldbr]) : 0.0;
+          if (lane < 16) sA[sidx<AKM>(x.cra, lane)] = v;
+          else sB[sidx<BKM>(x.crb, lane & 15)] = v;
+        } else if (P.dev_mode & 1) {  // development: pass 1 only
           amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
           bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
         } else if (!(P.dev_mode & 2)) {
           enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           enc_operand<BKM>(sB, lane, x.crb, b0, b1, bmax_hi);  // B_J e over the 127 data columns
         }
-        if (AKM) {
-          if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
-        } else {
-          if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
-        }
-        if (BKM) {
-          if (lane < 8) *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 2 * lane)) = make_double2(b0, b1);
-        } else {
-          if (lane < 16) sB[sidx<false>(x.crb, lane)] = b0;
+        if (!P.Ac) {
+          if (AKM) {
+            if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
+          } else {
+            if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
+          }
+          if (BKM) {
+            if (lane < 8) *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 2 * lane)) = make_double2(b0, b1);
+          } else {
+            if (lane < 16) sB[sidx<false>(x.crb, lane)] = b0;
+          }
         }
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
         __syncwarp();
@@ -513,7 +525,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       if (lane == 0 && s2 >= STAGES && s2 < nk) issue(s2);
       __syncwarp();
     }
-    if (verify && lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
+    if (verify && !P.Ac && lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
     stage_base += nk;
     bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
     if (!verify) return;
@@ -736,6 +748,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.
   constexpr int tm = FT ? TM : BM, tn = FT ? TN : BN;
+  x.ti = ti;
+  x.tj = tj;
   x.i0 = ti * tm;
   x.j0 = tj * tn;
   x.bm_eff = (int)min64(tm, P.m - x.i0);
@@ -755,8 +769,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&tl.enc[s], 1);
       mbar_init(&tl.empty[s], N_MMA_WARPS);
     }
-    tl.amax_hi = 0u;
-    tl.bmax_hi = 0u;
+    tl.amax_hi = P.Ac ? P.amax_pre[ti] : 0u;
+    tl.bmax_hi = P.Ac ? P.bmax_pre[tj] : 0u;
     tl.first_row = 0x7fffffff;
     tl.first_col = 0x7fffffff;
     tl.retry = 0;

@@ -25,6 +25,7 @@ thread_local cudaStream_t tl_stream = nullptr;
 thread_local std::vector<ftblas_fault_t> tl_armed;
 thread_local bool tl_have_armed = false;
 thread_local int tl_correct = FTBLAS_CORRECT_RECOMPUTE;
+thread_local int tl_encode = FTBLAS_ENCODE_FUSED;
 thread_local int64_t tl_launches = 0;
 thread_local std::string tl_cuda_error;
 
@@ -182,6 +183,23 @@ int finish_report(ftblas_err_report_t *err, const unsigned long long *d_counters
   return 0;
 }
 
+// Block sums over bs-long x-blocks (encode passes, reference sums): unfused.cuh.
+int launch_block_sum(const double *X, bool xc, int64_t ld, int64_t nx, int64_t np, double *S, int64_t lds,
+                     unsigned *hm, int bs, cudaStream_t st) {
+  const int64_t nb = (nx + bs - 1) / bs;
+  if (nb == 0 || np == 0) return 0;
+  if (xc) {
+    const dim3 g((unsigned)nb, (unsigned)((np + 31) / 32));
+    ftu::block_sum_kernel<true><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm, bs);
+  } else {
+    const dim3 g((unsigned)nb, (unsigned)((np + 255) / 256));
+    ftu::block_sum_kernel<false><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm, bs);
+  }
+  ++tl_launches;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 // The core entry: device pointers, protected (FT) or not, explicit fault list.
 int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char tb, int64_t m, int64_t n,
                int64_t k, double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
@@ -232,8 +250,25 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   const size_t cnt_bytes = sizeof(unsigned long long) * ftk::CNT_N;
   const size_t ev_bytes = sizeof(ftk::EventDev) * (size_t)ev_cap;
   const size_t f_bytes = sizeof(ftk::FaultDev) * fd.size();
+  // Encode mode PREPASS: e^T A_I, B_J e and the block maxima from two memory passes.
+  const bool prepass = ft && tl_encode == FTBLAS_ENCODE_PREPASS;
+  auto al256 = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t base_bytes = al256(cnt_bytes + ev_bytes + f_bytes + 64);
+  const size_t hm_bytes = al256(sizeof(unsigned) * (p.tiles_m + p.tiles_n));
+  const size_t pre_bytes = prepass ? hm_bytes + sizeof(double) * (size_t)(p.tiles_m + p.tiles_n) * k : 0;
   char *scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&scratch, cnt_bytes + ev_bytes + f_bytes + 64, st));
+  CUDA_TRY(cudaMallocAsync((void **)&scratch, base_bytes + pre_bytes, st));
+  if (prepass) {
+    char *pb = scratch + base_bytes;
+    auto *hm = reinterpret_cast<unsigned *>(pb);
+    double *Ac = reinterpret_cast<double *>(pb + hm_bytes);
+    double *Br = Ac + (size_t)p.tiles_m * k;
+    CUDA_TRY(cudaMemsetAsync(hm, 0, sizeof(unsigned) * (p.tiles_m + p.tiles_n), st));
+    if (int e = launch_block_sum(A, is_n(ta), lda, m, k, Ac, p.tiles_m, hm, ftk::TM, st)) return e;
+    if (int e = launch_block_sum(B, is_t(tb), ldb, n, k, Br, p.tiles_n, hm + p.tiles_m, ftk::TN, st)) return e;
+    p.Ac = Ac; p.Br = Br; p.ldac = p.tiles_m; p.ldbr = p.tiles_n;
+    p.amax_pre = hm; p.bmax_pre = hm + p.tiles_m;
+  }
   p.counters = reinterpret_cast<unsigned long long *>(scratch);
   p.events = reinterpret_cast<ftk::EventDev *>(scratch + cnt_bytes);
   p.ev_cap = ev_cap;
@@ -342,19 +377,7 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   if (ldn != nbn) CUDA_TRY(cudaMemsetAsync(Br, 0, br_b, st));
 
   auto block_sum = [&](const double *X, bool xc, int64_t ld, int64_t nx, int64_t np, double *S, int64_t lds,
-                       unsigned *hm) -> int {
-    const int64_t nb = (nx + ftu::UB - 1) / ftu::UB;
-    if (xc) {
-      const dim3 g((unsigned)nb, (unsigned)((np + 31) / 32));
-      ftu::block_sum_kernel<true><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm);
-    } else {
-      const dim3 g((unsigned)nb, (unsigned)((np + 255) / 256));
-      ftu::block_sum_kernel<false><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm);
-    }
-    ++tl_launches;
-    CUDA_TRY(cudaGetLastError());
-    return 0;
-  };
+                       unsigned *hm) -> int { return launch_block_sum(X, xc, ld, nx, np, S, lds, hm, ftu::UB, st); };
   // 1. encode: e^T A_I for every row block I (x = i), B_J e for every column block J (x = j).
   if (int e = block_sum(A, is_n(ta), lda, m, k, Ac, ldm, hmax)) return e;
   if (int e = block_sum(B, is_t(tb), ldb, n, k, Br, ldn, hmax + ldm)) return e;
@@ -514,6 +537,12 @@ int ftblas_set_stream(void *cuda_stream) {
 int ftblas_set_correction(int mode) {
   if (mode != FTBLAS_CORRECT_RECOMPUTE && mode != FTBLAS_CORRECT_SUBTRACT) return 4;
   tl_correct = mode;
+  return 0;
+}
+
+int ftblas_set_encode(int mode) {
+  if (mode != FTBLAS_ENCODE_FUSED && mode != FTBLAS_ENCODE_PREPASS) return 4;
+  tl_encode = mode;
   return 0;
 }
 

@@ -22,16 +22,16 @@ namespace ftu {
 
 constexpr int UB = 128;  // unit rows / columns of the unfused path
 
-// Sum of the 128-long x-blocks of X(x, p), element at X[x*sx + p*sp] with sx == 1 (XC) or
+// Sum of the bs-long (127 or 128) x-blocks of X(x, p), element at X[x*sx + p*sp] with sx == 1 (XC) or
 // sp == 1 (!XC).  One CTA of 256 threads per (x-block, 32 p) for XC, (x-block, 256 p) for
 // !XC; every global read is coalesced.  hmax (optional) receives max over the block of the
 // high word of |X| (reading R1': maxima tracked on 32-bit words, non-finite -> DBL_MAX's).
 template <bool XC>
 __global__ void __launch_bounds__(256) block_sum_kernel(const double *__restrict__ X, int64_t ld, int64_t nx,
                                                         int64_t np, double *__restrict__ S, int64_t lds,
-                                                        unsigned int *__restrict__ hmax) {
-  const int64_t xb = blockIdx.x, x0 = xb * UB;
-  const int xn = (int)min((int64_t)UB, nx - x0);
+                                                        unsigned int *__restrict__ hmax, int bs) {
+  const int64_t xb = blockIdx.x, x0 = xb * bs;  // block size bs <= 128
+  const int xn = (int)min((int64_t)bs, nx - x0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned int hm = 0;
   if (XC) {

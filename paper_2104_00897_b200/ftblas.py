@@ -84,6 +84,7 @@ def load():
                                        ctypes.POINTER(Fault)]
     L.ftblas_set_stream.argtypes = [P]
     L.ftblas_set_correction.argtypes = [i32]
+    L.ftblas_set_encode.argtypes = [i32]
     L.ftblas_get_geometry.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 3
     L.ftblas_take_launch_count.restype = i64
     L.ftblas_take_launch_count.argtypes = []
@@ -92,8 +93,8 @@ def load():
     L.ftblas_finalize.argtypes = []
     for fn in ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
                "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
-               "ftblas_set_stream", "ftblas_set_correction", "ftblas_get_geometry",
-               "ftblas_finalize"):
+               "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode",
+               "ftblas_get_geometry", "ftblas_finalize"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -101,7 +102,7 @@ def load():
 
 EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
             "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
-            "ftblas_set_stream", "ftblas_set_correction", "ftblas_get_geometry",
+            "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode", "ftblas_get_geometry",
             "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize")
 
 
@@ -228,6 +229,11 @@ def ftblas_set_correction(mode: int):
     _check("ftblas_set_correction", load().ftblas_set_correction(mode))
 
 
+def ftblas_set_encode(mode: int):
+    """ENCODE_FUSED (0, default) or ENCODE_PREPASS (1); thread-local."""
+    _check("ftblas_set_encode", load().ftblas_set_encode(mode))
+
+
 def ftblas_get_geometry():
     a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     _check("ftblas_get_geometry", load().ftblas_get_geometry(ctypes.byref(a), ctypes.byref(b),
@@ -247,5 +253,7 @@ def ftblas_finalize():
     _check("ftblas_finalize", load().ftblas_finalize())
 
 
+ENCODE_FUSED = 0
+ENCODE_PREPASS = 1
 CORRECT_RECOMPUTE = 0
 CORRECT_SUBTRACT = 1

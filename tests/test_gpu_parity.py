@@ -13,14 +13,18 @@ pytestmark = pytest.mark.gpu
 F = None
 
 
-@pytest.fixture(scope="module", autouse=True)
-def _lib():
+@pytest.fixture(scope="module", autouse=True, params=["fused", "prepass"])
+def _lib(request):
+    """Every parity test runs under both encode modes of ftblas_dgemm (in-kernel fused encode,
+    and the pre-encoded checksums copied into the staged tiles)."""
     global F
     from paper_2104_00897_b200 import ftblas
     ftblas.load()
     F = ftblas
+    F.ftblas_set_encode(F.ENCODE_FUSED if request.param == "fused" else F.ENCODE_PREPASS)
     yield
     F.ftblas_set_correction(F.CORRECT_RECOMPUTE)
+    F.ftblas_set_encode(F.ENCODE_FUSED)
 
 
 def geometry():
