@@ -83,7 +83,7 @@ struct Params {
   const unsigned int *amax_pre, *bmax_pre;
   unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
   int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
-                                  // 8 MMA waits for the TMA bytes only
+                                  // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait
   unsigned long long *counters;   // [CNT_N]
   EventDev *events;
   long long ev_cap;
@@ -117,6 +117,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
@@ -253,6 +264,22 @@ __device__ __forceinline__ double2 enc_ld(const double *s, int lane, int j, int 
   return v;
 }
 
+// Element pair jj (0..15, compile time) of half hh of this lane's pairs: pair j = 16 hh + jj
+// sits at a constant offset from the half's base (MN-major +512, K-major +256 elements).
+template <bool KM>
+__device__ __forceinline__ double2 enc_ld_half(const double *s, int lane, int hh, int jj, int cr) {
+  double2 v = *reinterpret_cast<const double2 *>(s + hh * (KM ? 256 : 512) + enc_addr<KM>(lane, jj));
+  if (jj == 0 && hh == 0 && cr == 0 && (lane >> (KM ? 3 : 4)) == 0) {  // staged row 0
+    v.x = 0.0;
+    if (KM) v.y = 0.0;
+  }
+  if (jj == 15 && hh == 1 && cr == DM && (lane >> (KM ? 3 : 4)) == (KM ? 3 : 1)) {  // staged row 127
+    v.y = 0.0;
+    if (KM) v.x = 0.0;
+  }
+  return v;
+}
+
 // Pass 1: per-lane max (as float bits of |high word|), NaN-propagating.
 template <bool KM>
 __device__ __forceinline__ float enc_pass1(const double *s, int lane, int cr) {
@@ -316,9 +343,13 @@ template <bool KM, bool EXACT>
 __device__ __forceinline__ void enc_pass2(const double *s, int lane, int cr, uint32_t C, long long &q0, long long &q1) {
   long long a0 = 0, a1 = 0;
   int n0 = 0, n1 = 0;  // minus the number of negative terms (ones' -> two's complement)
+  // Two halves in a rolled loop: caps the encoder's register peak (a fully unrolled pass
+  // makes ptxas spill the MMA warps' loop state in this same kernel).
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-  for (int j = 0; j < 32; j += 2) {
-    const double2 v = enc_ld<KM>(s, lane, j, cr), w = enc_ld<KM>(s, lane, j + 1, cr);
+  for (int jj = 0; jj < 16; jj += 2) {
+    const double2 v = enc_ld_half<KM>(s, lane, hh, jj, cr), w = enc_ld_half<KM>(s, lane, hh, jj + 1, cr);
     int sv0, sv1, sw0, sw1;
     const long long tv0 = fx_term<EXACT>(v.x, C, sv0), tv1 = fx_term<EXACT>(v.y, C, sv1);
     const long long tw0 = fx_term<EXACT>(w.x, C, sw0), tw1 = fx_term<EXACT>(w.y, C, sw1);
@@ -388,7 +419,18 @@ __device__ __forceinline__ void enc_operand(const double *s, int lane, int cr, d
 }
 
 // ------------------------------------------------------------------ the kernel
+// Tile geometry kept in shared memory: the MMA warps re-read it after the k-loop, so none of
+// it has to stay live in registers across the DMMA stream.
+struct TileGeom {
+  int ti, tj, i0, j0, bm_eff, bn_eff, oa, ob, cra, crb;
+};
+__device__ __forceinline__ TileGeom load_geom(const TileGeom &g) {
+  const volatile TileGeom &v = g;
+  return TileGeom{v.ti, v.tj, v.i0, v.j0, v.bm_eff, v.bn_eff, v.oa, v.ob, v.cra, v.crb};
+}
+
 struct SmemTail {
+  TileGeom geo;
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
   double dres[256];                // residuals: 0..127 columns, 128..255 rows
   double red[NTHREADS / 32];
@@ -483,7 +525,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
-        mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
+        if (!(P.dev_mode & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
@@ -534,6 +576,88 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   }
 }
 
+// ---- verification: reference checksums r from the computed C_IJ (staged in
+// ctile) against the carried checksums in row / column cr of C^f; flag, classify, correct in
+// place (R1, R4, R6), record the event.  Returns true when the
+// unit must be recomputed.  Called by the 256 MMA threads (vt = 0..255).
+template <bool AKM, bool BKM>
+__device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *ctile, int vt, int mw) {
+  const TileGeom x = load_geom(tl.geo);
+  const int lane = vt & 31;
+      // ctile is indexed by staged rows / columns: data row i at i + oa, data column j at j + ob.
+      const int cidx = vt & 127;
+      const bool is_row = vt >= 128;
+      double r = 0.0, cs = 0.0;
+      if (cidx < DM) {
+        if (is_row) {
+          const double *rowp = ctile + (cidx + x.oa);
+  #pragma unroll 9
+          for (int j = 0; j < DM; ++j) r += rowp[(j + x.ob) * LDC_S];
+          cs = rowp[x.crb * LDC_S];  // A_I (B_J e)
+        } else {
+          const double *colp = ctile + (cidx + x.ob) * LDC_S;
+  #pragma unroll 9
+          for (int i = 0; i < DM; ++i) r += colp[i + x.oa];
+          cs = colp[x.cra];  // (e^T A_I) B_J
+        }
+      }
+      const double d = r - cs;
+      // R1': maxima rounded up to the largest double with the same high word.
+      const double amx = __longlong_as_double((long long)(((unsigned long long)tl.amax_hi << 32) | 0xFFFFFFFFull));
+      const double bmx = __longlong_as_double((long long)(((unsigned long long)tl.bmax_hi << 32) | 0xFFFFFFFFull));
+      const int64_t kt = P.k;
+      const int len = is_row ? x.bn_eff : x.bm_eff;
+      const double nu = (double)(kt + len) * 0x1p-53;
+      const double tau = 2.0 * (nu / (1.0 - nu)) * (double)kt * (double)len * amx * bmx;  // DESIGN.md R1
+      const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
+      const bool flag = valid && !(fabs(d) <= tau) && !(P.dev_mode & 4);
+      tl.dres[vt] = d;
+      if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, cidx);
+      const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
+      const int nfc = bar_popc(BAR_FLAGS_C, 256, flag && !is_row);
+      const bool multi = !(nfr == 0 && nfc == 0) && !(nfr == 1 && nfc == 1);
+      const int fr = tl.first_row, fc = tl.first_col;
+      if (nfr == 1 && nfc == 1) {
+        // Single error at the intersection (i0+fr, j0+fc): correct in place.
+        if (P.correct_mode == 1) {
+          if (vt == 0) ctile[(fc + x.ob) * LDC_S + fr + x.oa] -= tl.dres[fc];  // subtract d_col
+        } else {
+          // Recompute C_ij with a fresh k-long dot product (R4).
+          const int64_t gi = x.i0 + fr, gj = x.j0 + fc;
+          double part = 0.0;
+          for (int64_t p = vt; p < P.k; p += 256) {
+            const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
+            const double bv = BKM ? P.B[p + gj * P.ldb] : P.B[gj + p * P.ldb];
+            part = fma(av, bv, part);
+          }
+  #pragma unroll
+          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          if (lane == 0) tl.red[mw] = part;
+          bar_sync(BAR_RED, 256);
+          if (vt == 0) {
+            double v = 0.0;
+  #pragma unroll
+            for (int q = 0; q < N_MMA_WARPS; ++q) v += tl.red[q];
+            ctile[(fc + x.ob) * LDC_S + fr + x.oa] = v;
+          }
+        }
+      }
+      if (vt == 0 && (nfr | nfc)) {
+        atomicAdd(&P.counters[CNT_DETECTED], 1ull);
+        atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
+        const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
+        if ((long long)slot < P.ev_cap)
+          P.events[slot] = multi ? EventDev{(long long)x.i0, (long long)x.j0, 2, 0, nfr ? tl.dres[128 + fr] : 0.0,
+                                            nfc ? tl.dres[fc] : 0.0}
+                                 : EventDev{(long long)(x.i0 + fr), (long long)(x.j0 + fc), 1, 0, tl.dres[128 + fr],
+                                            tl.dres[fc]};
+      }
+      if (vt == 0) tl.retry = multi ? 1 : 0;
+      if (multi) fence_proxy_async();  // generic writes to the ring (C tile) before TMA reuses it
+      bar_sync(BAR_DECIDE, NTHREADS);
+  return multi;
+}
+
 // ---------------- warpgroups 1-2: MMA warps (+ epilogue)
 template <bool AKM, bool BKM, bool FT>
 __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
@@ -558,7 +682,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     auto apply_faults = [&](int s) {
       while (s == next_stage) {
         const FaultDev f = P.faults[fnext];
-        const int si = f.li + x.oa, sj = f.lj + x.ob;  // staged row / column
+        const TileGeom gf = load_geom(tl.geo);
+        const int si = f.li + gf.oa, sj = f.lj + gf.ob;  // staged row / column
         const int lr = si & 63, lc = sj & 31;
         const int fmt = AKM ? (lr >> 3) : 2 * (lr >> 4) + (lr & 1);
         const int rr = lr & 7;  // K-major: row in the 8-row tile = 4*(g&1) + (g>>1)
@@ -585,14 +710,15 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     };
     // The protected pass waits for the encoded stage (TMA bytes + checksum row/column), the
     // unprotected one for the TMA bytes only.
-    uint64_t *const ready = (verify && !(P.dev_mode & 8)) ? tl.enc : tl.full;
+    // 32-bit shared address of the barrier array to wait on (enc = full + STAGES).
+    const uint32_t ready = smem_u32(tl.full) + ((verify && !(P.dev_mode & 8)) ? STAGES * 8u : 0u);
     // The k-loop runs in segments between fault stages, so that the DMMA loop body carries no
     // injection code (which would make the register allocator shuffle accumulators).
     for (int s = 0; s < nk;) {
-      const int s_end = next_stage < nk ? next_stage : nk;
+      const int s_end = __shfl_sync(0xffffffffu, next_stage < nk ? next_stage : nk, 0);
       for (; s < s_end; ++s) {
         const int gs = stage_base + s, slot = gs % STAGES;
-        mbar_wait(&ready[slot], (gs / STAGES) & 1);
+        mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
         const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -629,91 +755,22 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     bar_sync(BAR_CTILE, 256);
     if (!verify) break;
 
-    // ---- verification: reference checksums r from the computed C_IJ against
-    // the carried checksums in row / column 127 of C^f.
-    // ctile is indexed by staged rows / columns: data row i at i + oa, data column j at j + ob.
-    const int cidx = vt & 127;
-    const bool is_row = vt >= 128;
-    double r = 0.0, cs = 0.0;
-    if (cidx < DM) {
-      if (is_row) {
-        const double *rowp = ctile + (cidx + x.oa);
-#pragma unroll 9
-        for (int j = 0; j < DM; ++j) r += rowp[(j + x.ob) * LDC_S];
-        cs = rowp[x.crb * LDC_S];  // A_I (B_J e)
-      } else {
-        const double *colp = ctile + (cidx + x.ob) * LDC_S;
-#pragma unroll 9
-        for (int i = 0; i < DM; ++i) r += colp[i + x.oa];
-        cs = colp[x.cra];  // (e^T A_I) B_J
-      }
-    }
-    const double d = r - cs;
-    // R1': maxima rounded up to the largest double with the same high word.
-    const double amx = __longlong_as_double((long long)(((unsigned long long)tl.amax_hi << 32) | 0xFFFFFFFFull));
-    const double bmx = __longlong_as_double((long long)(((unsigned long long)tl.bmax_hi << 32) | 0xFFFFFFFFull));
-    const int64_t kt = P.k;
-    const int len = is_row ? x.bn_eff : x.bm_eff;
-    const double nu = (double)(kt + len) * 0x1p-53;
-    const double tau = 2.0 * (nu / (1.0 - nu)) * (double)kt * (double)len * amx * bmx;  // DESIGN.md R1
-    const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
-    const bool flag = valid && !(fabs(d) <= tau) && !(P.dev_mode & 4);
-    tl.dres[vt] = d;
-    if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, cidx);
-    const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
-    const int nfc = bar_popc(BAR_FLAGS_C, 256, flag && !is_row);
-    const bool multi = !(nfr == 0 && nfc == 0) && !(nfr == 1 && nfc == 1);
-    const int fr = tl.first_row, fc = tl.first_col;
-    if (nfr == 1 && nfc == 1) {
-      // Single error at the intersection (i0+fr, j0+fc): correct in place.
-      if (P.correct_mode == 1) {
-        if (vt == 0) ctile[(fc + x.ob) * LDC_S + fr + x.oa] -= tl.dres[fc];  // subtract d_col
-      } else {
-        // Recompute C_ij with a fresh k-long dot product (R4).
-        const int64_t gi = x.i0 + fr, gj = x.j0 + fc;
-        double part = 0.0;
-        for (int64_t p = vt; p < P.k; p += 256) {
-          const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
-          const double bv = BKM ? P.B[p + gj * P.ldb] : P.B[gj + p * P.ldb];
-          part = fma(av, bv, part);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) tl.red[mw] = part;
-        bar_sync(BAR_RED, 256);
-        if (vt == 0) {
-          double v = 0.0;
-#pragma unroll
-          for (int q = 0; q < N_MMA_WARPS; ++q) v += tl.red[q];
-          ctile[(fc + x.ob) * LDC_S + fr + x.oa] = v;
-        }
-      }
-    }
-    if (vt == 0 && (nfr | nfc)) {
-      atomicAdd(&P.counters[CNT_DETECTED], 1ull);
-      atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
-      const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
-      if ((long long)slot < P.ev_cap)
-        P.events[slot] = multi ? EventDev{(long long)x.i0, (long long)x.j0, 2, 0, nfr ? tl.dres[128 + fr] : 0.0,
-                                          nfc ? tl.dres[fc] : 0.0}
-                               : EventDev{(long long)(x.i0 + fr), (long long)(x.j0 + fc), 1, 0, tl.dres[128 + fr],
-                                          tl.dres[fc]};
-    }
-    if (vt == 0) tl.retry = multi ? 1 : 0;
-    if (multi) fence_proxy_async();  // generic writes to the ring (C tile) before TMA reuses it
-    bar_sync(BAR_DECIDE, NTHREADS);
+    // ---- verification, out of line so that its register needs do not shape
+    // the allocation of the DMMA k-loop above (the accumulators are dead here: staged in smem).
+    const bool multi = verify_tile<AKM, BKM>(P, tl, ctile, vt, mw);
     if (!multi) break;
     // Out of the one-error model: recompute the whole tile once (no re-verification).
   }
 
   // ---- store: C = alpha*acc + beta*C0 (two roundings each, no contraction).
+  const TileGeom ge = load_geom(tl.geo);
   const int i = vt & 127;
   const double alpha = P.alpha, beta = P.beta;
-  if (i < x.bm_eff) {
-    double *crow = P.C + (int64_t)(x.i0 + i) + (int64_t)x.j0 * P.ldc;
+  if (i < ge.bm_eff) {
+    double *crow = P.C + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
 #pragma unroll 4
-    for (int j = vt >> 7; j < x.bn_eff; j += 2) {
-      const double v = __dmul_rn(alpha, ctile[(j + x.ob) * LDC_S + i + x.oa]);
+    for (int j = vt >> 7; j < ge.bn_eff; j += 2) {
+      const double v = __dmul_rn(alpha, ctile[(j + ge.ob) * LDC_S + i + ge.oa]);
       double *dst = crow + (int64_t)j * P.ldc;
       *dst = (beta != 0.0) ? __dadd_rn(v, __dmul_rn(beta, *dst)) : v;
     }
@@ -747,20 +804,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   x.tile = ti + tj * P.tiles_m;
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.
-  constexpr int tm = FT ? TM : BM, tn = FT ? TN : BN;
+  const bool g127 = FT || (P.dev_mode & 32);  // dev mode 32: unprotected kernel on the 127 grid
+  const int tm = g127 ? TM : BM, tn = g127 ? TN : BN;
   x.ti = ti;
   x.tj = tj;
   x.i0 = ti * tm;
   x.j0 = tj * tn;
   x.bm_eff = (int)min64(tm, P.m - x.i0);
   x.bn_eff = (int)min64(tn, P.n - x.j0);
-  x.oa = FT ? (x.i0 & 1) : 0;
-  x.ob = FT ? (x.j0 & 1) : 0;
+  x.oa = g127 ? (x.i0 & 1) : 0;
+  x.ob = g127 ? (x.j0 & 1) : 0;
   x.cra = x.oa ? 0 : DM;
   x.crb = x.ob ? 0 : DM;
   x.nk = P.nk;
 
   if (x.tid == 0) {
+    tl.geo = TileGeom{x.ti, x.tj, x.i0, x.j0, x.bm_eff, x.bn_eff, x.oa, x.ob, x.cra, x.crb};
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
 #pragma unroll
