@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-unfused", action="store_true", help="skip the unfused ABFT baseline timing")
+    p.add_argument("--interval", type=int, default=0,
+                   help="verification interval Kc (multiple of 16; 0 = k): ftblas_set_interval")
     p.add_argument("--cpu-sample-units", type=int, default=0)
     return p.parse_args()
 
@@ -280,6 +282,7 @@ def main():
 
     stream = torch.cuda.current_stream(dev)
     F.ftblas_set_stream(stream)
+    F.ftblas_set_interval(args.interval)
     counters = torch.zeros(5, dtype=torch.int64, device=dev)
 
     def step(ft=True):
@@ -418,7 +421,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": W["name"], "m": W["m"], "n": n, "k": k, "trans": ta + tb,
                    "alpha": alpha, "beta": beta, "dist": W["dist"], "faults_per_step": len(W["faults"]),
-                   "parallelism": f"row-panels x{world}", "l2": "inputs larger than L2 (no flush)"},
+                   "parallelism": f"row-panels x{world}", "l2": "inputs larger than L2 (no flush)",
+                   "interval_Kc": args.interval or k},
         "abft": {"tflops_protected": tflops, "tflops_unprotected": tflops_noft,
                  "overhead_pct": 100.0 * (ms_ft - ms_noft) / ms_noft,
                  "pct_of_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_TFLOPS),

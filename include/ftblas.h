@@ -72,7 +72,7 @@ typedef struct {
   int64_t n_events;      /* out: events produced (may exceed events_capacity) */
   int32_t unit_rows;     /* out: BM, rows per verification unit */
   int32_t unit_cols;     /* out: BN, columns per verification unit */
-  int32_t unit_k;        /* out: Kc, k-length of a verification interval (== k today) */
+  int32_t unit_k;        /* out: Kc, k-length of a verification interval (ftblas_set_interval) */
   int32_t step_quantum;  /* out: BK; an injected fault's step is applied at floor(step/BK)*BK */
   ftblas_event_t *events;  /* in: caller-owned HOST array (may be NULL), filled with the
                               first min(n_events, events_capacity) events sorted by
@@ -159,6 +159,19 @@ int ftblas_set_correction(int mode);
 #define FTBLAS_ENCODE_FUSED 0
 #define FTBLAS_ENCODE_PREPASS 1
 int ftblas_set_encode(int mode);
+
+/* Verification interval Kc of ftblas_dgemm (§II.A,
+ * 258 §V.A: verify after every Kc rank-1 updates, one correctable error per interval).
+ * 0 (default) means Kc = k: one interval, verified in the epilogue before C is written.
+ * With 0 < Kc < k the k-loop is split into T = ceil(k/Kc) intervals; the verification unit is
+ * (tile, interval): each interval's increment A_{:,t} B_{t,:} is verified against its own
+ * carried checksums (reading R18) and corrected before it is accumulated, and an injected
+ * fault belongs to interval floor(step_q / Kc).  err->unit_k reports Kc and
+ * err->units_checked counts tiles x intervals.  The increments go through library workspace
+ * (interval groups sized to half the free device memory) and a deterministic reduction
+ * forms C = alpha * sum_t inc_t + beta * C.  Kc must be a multiple of step_quantum (16);
+ * returns 4 otherwise.  Thread-local. */
+int ftblas_set_interval(int64_t kc);
 
 /* Verification-unit geometry the kernels use: BM x BN tiles, step quantum BK. */
 int ftblas_get_geometry(int32_t *unit_rows, int32_t *unit_cols, int32_t *step_quantum);

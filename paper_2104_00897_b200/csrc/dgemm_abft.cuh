@@ -73,6 +73,12 @@ struct Params {
   double *C;
   int64_t ldc;
   int tiles_m, tiles_n, nk;
+  // Verification intervals: the k-loop is split
+  // into T intervals of Kc rank-1 updates; CTA L works on interval t = L / ntiles over
+  // k in [t*Kc, min((t+1)*Kc, k)) and, when T > 1, writes its verified raw increment to the
+  // workspace slice C + t*wstride (alpha = 1, beta = 0; a reduction kernel finishes C).
+  int64_t Kc, wstride;
+  int T, ntiles, t_base;
   const FaultDev *faults;
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
@@ -422,11 +428,12 @@ __device__ __forceinline__ void enc_operand(const double *s, int lane, int cr, d
 // Tile geometry kept in shared memory: the MMA warps re-read it after the k-loop, so none of
 // it has to stay live in registers across the DMMA stream.
 struct TileGeom {
-  int ti, tj, i0, j0, bm_eff, bn_eff, oa, ob, cra, crb;
+  int ti, tj, i0, j0, bm_eff, bn_eff, oa, ob, cra, crb, t;
+  int64_t k0, k1;  // this CTA's k range [k0, k1) (one verification interval)
 };
 __device__ __forceinline__ TileGeom load_geom(const TileGeom &g) {
   const volatile TileGeom &v = g;
-  return TileGeom{v.ti, v.tj, v.i0, v.j0, v.bm_eff, v.bn_eff, v.oa, v.ob, v.cra, v.crb};
+  return TileGeom{v.ti, v.tj, v.i0, v.j0, v.bm_eff, v.bn_eff, v.oa, v.ob, v.cra, v.crb, v.t, v.k0, v.k1};
 }
 
 struct SmemTail {
@@ -467,7 +474,8 @@ __device__ __forceinline__ int mma_warp(int w) { return CS_HIGH ? w : w - N_CS_W
 struct Ctx {
   double *ring;
   SmemTail *tl;
-  int tid, lane, warp, tile, ti, tj, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi;
+  int tid, lane, warp, tile, ti, tj, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi, t;
+  int64_t k0, k1;
   // Protected tiles: TMA boxes start at the even coordinate xs = x0 - (x0 & 1) (the contiguous
   // dimension of a TMA box must start 16-byte aligned), so tile-local data row i sits in
   // staged row i + o (o = x0 & 1) and the checksum row/column takes the free row cr.
@@ -501,7 +509,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     if (gs >= STAGES) mbar_wait(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
     double *sa = ring + slot * STAGE_ELEMS;
     mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
-    const int k0 = s * BK;
+    const int k0 = (int)x.k0 + s * BK;
     if (AKM) {
       tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
     } else {
@@ -530,8 +538,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
         if (P.Ac) {  // PREPASS: copy the pre-encoded 16 k-slots of e^T A_I / B_J e
-          const int p = s * BK + (lane & 15);
-          const double v = p < P.k ? (lane < 16 ? P.Ac[x.ti + (int64_t)p * P.ldac] : P.Br[x.tj + (int64_t)p * P.ldbr]) : 0.0;
+          const int64_t p = x.k0 + s * BK + (lane & 15);
+          const double v = p < x.k1 ? (lane < 16 ? P.Ac[x.ti + p * P.ldac] : P.Br[x.tj + p * P.ldbr]) : 0.0;
           if (lane < 16) sA[sidx<AKM>(x.cra, lane)] = v;
           else sB[sidx<BKM>(x.crb, lane & 15)] = v;
         } else if (P.dev_mode & 1) {  // development: pass 1 only
@@ -605,7 +613,7 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
       // R1': maxima rounded up to the largest double with the same high word.
       const double amx = __longlong_as_double((long long)(((unsigned long long)tl.amax_hi << 32) | 0xFFFFFFFFull));
       const double bmx = __longlong_as_double((long long)(((unsigned long long)tl.bmax_hi << 32) | 0xFFFFFFFFull));
-      const int64_t kt = P.k;
+      const int64_t kt = x.k1 - x.k0;  // rank-1 updates in this interval
       const int len = is_row ? x.bn_eff : x.bm_eff;
       const double nu = (double)(kt + len) * 0x1p-53;
       const double tau = 2.0 * (nu / (1.0 - nu)) * (double)kt * (double)len * amx * bmx;  // DESIGN.md R1
@@ -625,7 +633,7 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
           // Recompute C_ij with a fresh k-long dot product (R4).
           const int64_t gi = x.i0 + fr, gj = x.j0 + fc;
           double part = 0.0;
-          for (int64_t p = vt; p < P.k; p += 256) {
+          for (int64_t p = x.k0 + vt; p < x.k1; p += 256) {
             const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
             const double bv = BKM ? P.B[p + gj * P.ldb] : P.B[gj + p * P.ldb];
             part = fma(av, bv, part);
@@ -647,9 +655,9 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
         atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
         const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
         if ((long long)slot < P.ev_cap)
-          P.events[slot] = multi ? EventDev{(long long)x.i0, (long long)x.j0, 2, 0, nfr ? tl.dres[128 + fr] : 0.0,
+          P.events[slot] = multi ? EventDev{(long long)x.i0, (long long)x.j0, 2, x.t, nfr ? tl.dres[128 + fr] : 0.0,
                                             nfc ? tl.dres[fc] : 0.0}
-                                 : EventDev{(long long)(x.i0 + fr), (long long)(x.j0 + fc), 1, 0, tl.dres[128 + fr],
+                                 : EventDev{(long long)(x.i0 + fr), (long long)(x.j0 + fc), 1, x.t, tl.dres[128 + fr],
                                             tl.dres[fc]};
       }
       if (vt == 0) tl.retry = multi ? 1 : 0;
@@ -767,7 +775,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   const int i = vt & 127;
   const double alpha = P.alpha, beta = P.beta;
   if (i < ge.bm_eff) {
-    double *crow = P.C + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
+    double *crow = P.C + (int64_t)(ge.t - P.t_base) * P.wstride + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
 #pragma unroll 4
     for (int j = vt >> 7; j < ge.bn_eff; j += 2) {
       const double v = __dmul_rn(alpha, ctile[(j + ge.ob) * LDC_S + i + ge.oa]);
@@ -796,12 +804,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // instead of 148 A panels and one B panel.
   int ti, tj;
   {
-    const int L = blockIdx.x, band_tiles = RASTER_G * P.tiles_n, band = L / band_tiles;
+    const int L = blockIdx.x % P.ntiles, band_tiles = RASTER_G * P.tiles_n, band = L / band_tiles;
     const int within = L - band * band_tiles, rows = min(RASTER_G, P.tiles_m - band * RASTER_G);
     ti = band * RASTER_G + within % rows;
     tj = within / rows;
   }
-  x.tile = ti + tj * P.tiles_m;
+  x.t = P.t_base + (int)(blockIdx.x / P.ntiles);  // verification interval
+  x.tile = ti + tj * P.tiles_m + x.t * P.ntiles;  // fault bucket key: (tile, interval)
+  x.k0 = (int64_t)x.t * P.Kc;
+  x.k1 = min64(x.k0 + P.Kc, P.k);
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.
   const bool g127 = FT || (P.dev_mode & 32);  // dev mode 32: unprotected kernel on the 127 grid
@@ -816,10 +827,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   x.ob = g127 ? (x.j0 & 1) : 0;
   x.cra = x.oa ? 0 : DM;
   x.crb = x.ob ? 0 : DM;
-  x.nk = P.nk;
+  x.nk = (int)((x.k1 - x.k0 + BK - 1) / BK);
 
   if (x.tid == 0) {
-    tl.geo = TileGeom{x.ti, x.tj, x.i0, x.j0, x.bm_eff, x.bn_eff, x.oa, x.ob, x.cra, x.crb};
+    tl.geo = TileGeom{x.ti, x.tj, x.i0, x.j0, x.bm_eff, x.bn_eff, x.oa, x.ob, x.cra, x.crb, x.t, x.k0, x.k1};
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
 #pragma unroll
@@ -854,6 +865,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     setmaxnreg_inc<REG_MMA>();
     mma_role<AKM, BKM, FT>(P, x);
+  }
+}
+
+// Intervals (NEXT-1): C = alpha * sum_{t < G} W_t + (first ? beta * C0 : C), the increments
+// summed in interval order (deterministic), two roundings for the alpha/beta combination.
+__global__ void interval_reduce_kernel(int64_t m, int64_t n, int G, const double *__restrict__ W, int64_t ldw,
+                                       int64_t wstride, double alpha, double beta, double *__restrict__ C,
+                                       int64_t ldc, bool first) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    double acc = W[i + j * ldw];
+    for (int t = 1; t < G; ++t) acc = __dadd_rn(acc, W[t * wstride + i + j * ldw]);
+    double *c = C + i + j * ldc;
+    const double v = __dmul_rn(alpha, acc);
+    if (first) *c = beta != 0.0 ? __dadd_rn(v, __dmul_rn(beta, *c)) : v;
+    else *c = __dadd_rn(*c, v);
   }
 }
 

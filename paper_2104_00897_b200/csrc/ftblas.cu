@@ -26,6 +26,7 @@ thread_local std::vector<ftblas_fault_t> tl_armed;
 thread_local bool tl_have_armed = false;
 thread_local int tl_correct = FTBLAS_CORRECT_RECOMPUTE;
 thread_local int tl_encode = FTBLAS_ENCODE_FUSED;
+thread_local int64_t tl_interval = 0;  // Kc; 0 = k (one interval)
 thread_local int64_t tl_launches = 0;
 thread_local std::string tl_cuda_error;
 
@@ -232,6 +233,15 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.tiles_m = (int)((m + tm - 1) / tm);
   p.tiles_n = (int)((n + tn - 1) / tn);
   p.nk = (int)((k + ftk::BK - 1) / ftk::BK);
+  // Verification intervals (NEXT-1): Kc rank-1 updates each, the last one ragged.
+  const int64_t Kc = (ft && tl_interval > 0 && tl_interval < k) ? tl_interval : k;
+  const int64_t T = (k + Kc - 1) / Kc;
+  p.Kc = Kc;
+  p.T = (int)T;
+  p.ntiles = p.tiles_m * p.tiles_n;
+  p.t_base = 0;
+  p.wstride = 0;
+  if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
   p.correct_mode = tl_correct;
   // development only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
@@ -242,7 +252,11 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   fd.reserve(faults.size());
   for (const auto &f : faults) {
     const int64_t ti = f.i / tm, tj = f.j / tn;
-    fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m), (int32_t)(f.step / ftk::BK),
+    // step quantised to BK (R8); interval t = step_q / Kc (step_q == k: after the last update
+    // of the last interval), stage local to the interval.
+    const int64_t step_q = (f.step / ftk::BK) * ftk::BK;
+    const int64_t t = std::min<int64_t>(step_q / Kc, T - 1);
+    fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m + t * p.ntiles), (int32_t)((step_q - t * Kc) / ftk::BK),
                                (int32_t)(f.i - ti * tm), (int32_t)(f.j - tj * tn), f.delta});
   }
   std::stable_sort(fd.begin(), fd.end(), [](const ftk::FaultDev &a, const ftk::FaultDev &b) {
@@ -305,14 +319,41 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   CUtensorMap tmA, tmB;
   if (int e = make_tmap(&tmA, p.A, p.lda, akm, m, k)) return e;
   if (int e = make_tmap(&tmB, p.B, p.ldb, bkm, n, k)) return e;
-  const dim3 grid((unsigned)((int64_t)p.tiles_m * p.tiles_n));  // 1-D: grouped raster in the kernel
-  int lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
+  int lrc = 0;
+  if (T == 1) {
+    const dim3 grid((unsigned)p.ntiles);  // 1-D: grouped raster in the kernel
+    lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
+  } else {
+    // Every interval's verified increment goes to a workspace slice (all intervals of a group
+    // run in one launch, so the k-split also fills the machine on skinny shapes); a
+    // deterministic reduction then forms C = alpha * sum_t inc_t + beta * C0.
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const size_t slice = sizeof(double) * (size_t)m * (size_t)n;
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)(free_b / 2 / slice)));
+    double *W = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)&W, slice * (size_t)G, st));
+    ftk::Params pw = p;
+    pw.C = W; pw.ldc = m; pw.alpha = 1.0; pw.beta = 0.0; pw.wstride = m * n;
+    for (int64_t g0 = 0; g0 < T && lrc == 0; g0 += G) {
+      const int64_t gn = std::min<int64_t>(G, T - g0);
+      pw.t_base = (int)g0;
+      const dim3 grid((unsigned)(p.ntiles * gn));
+      lrc = dispatch<true>(akm, bkm, tmA, tmB, pw, grid, st);
+      if (lrc) break;
+      const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, 148 * 16);
+      ftk::interval_reduce_kernel<<<blocks, 256, 0, st>>>(m, n, (int)gn, W, m, m * n, alpha, beta, C, ldc, g0 == 0);
+      ++tl_launches;
+      if (cudaGetLastError() != cudaSuccess) lrc = 1;
+    }
+    cudaFreeAsync(W, st);
+  }
   if (rA) cudaFreeAsync(rA, st);
   if (rB) cudaFreeAsync(rB, st);
   if (lrc) { cudaFreeAsync(scratch, st); return lrc; }
 
   if (err)
-    if (int e = finish_report(err, p.counters, p.events, ev_cap, ft ? (int64_t)p.tiles_m * p.tiles_n : 0, st)) return e;
+    if (int e = finish_report(err, p.counters, p.events, ev_cap, ft ? (int64_t)p.ntiles * T : 0, st)) return e;
   CUDA_TRY(cudaFreeAsync(scratch, st));
   return 0;
 }
@@ -540,6 +581,12 @@ int ftblas_set_stream(void *cuda_stream) {
 int ftblas_set_correction(int mode) {
   if (mode != FTBLAS_CORRECT_RECOMPUTE && mode != FTBLAS_CORRECT_SUBTRACT) return 4;
   tl_correct = mode;
+  return 0;
+}
+
+int ftblas_set_interval(int64_t kc) {
+  if (kc < 0 || kc % ftk::BK != 0) return 4;
+  tl_interval = kc;
   return 0;
 }
 

@@ -85,6 +85,7 @@ def load():
     L.ftblas_set_stream.argtypes = [P]
     L.ftblas_set_correction.argtypes = [i32]
     L.ftblas_set_encode.argtypes = [i32]
+    L.ftblas_set_interval.argtypes = [i64]
     L.ftblas_get_geometry.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 3
     L.ftblas_take_launch_count.restype = i64
     L.ftblas_take_launch_count.argtypes = []
@@ -94,7 +95,7 @@ def load():
     for fn in ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
                "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
                "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode",
-               "ftblas_get_geometry", "ftblas_finalize"):
+               "ftblas_set_interval", "ftblas_get_geometry", "ftblas_finalize"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -102,8 +103,8 @@ def load():
 
 EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
             "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
-            "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode", "ftblas_get_geometry",
-            "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize")
+            "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode", "ftblas_set_interval",
+            "ftblas_get_geometry", "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize")
 
 
 def _check(fn, status):
@@ -232,6 +233,11 @@ def ftblas_set_correction(mode: int):
 def ftblas_set_encode(mode: int):
     """ENCODE_FUSED (0, default) or ENCODE_PREPASS (1); thread-local."""
     _check("ftblas_set_encode", load().ftblas_set_encode(mode))
+
+
+def ftblas_set_interval(kc: int):
+    """Verification interval Kc (multiple of 16; 0 = k); thread-local."""
+    _check("ftblas_set_interval", load().ftblas_set_interval(int(kc)))
 
 
 def ftblas_get_geometry():
