@@ -64,10 +64,10 @@ def workload(cfg: str, size: int, seed: int):
         return dict(name=f"C5 NN {n}^3 row-panels", m=n, n=n, k=n, ta="N", tb="N", alpha=1.0,
                     beta=0.0, dist="uniform", faults=synth.c5_faults(seed, size=n))
     c = {"C1": (256, 256, 256), "C2": (2048, 2048, 2048), "C3": (8192, 8192, 8192),
-         "C4a": (16384, 16384, 1024), "C4b": (16384, 512, 16384)}[cfg[:3] if cfg.startswith("C3") else cfg]
+         "C4a": (16384, 16384, 1024), "C4b": (16384, 512, 16384)}[cfg[:2] if cfg.startswith("C3") else cfg]
     m, n, k = c
     alpha, beta = (1.5, 0.5) if cfg == "C2" else (1.0, 0.0)
-    tr = cfg[2:] if cfg.startswith("C3") and len(cfg) == 4 else "NN"
+    tr = cfg[2:] if cfg.startswith("C3") and len(cfg) == 4 else "NN"  # C3 / C3NT / C3TN / C3TT
     if cfg == "C1":
         faults = [(17, 203, 128, 1e3)]
     elif cfg.startswith("C3"):
