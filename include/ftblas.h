@@ -176,6 +176,47 @@ int ftblas_set_interval(int64_t kc);
 /* Verification-unit geometry the kernels use: BM x BN tiles, step quantum BK. */
 int ftblas_get_geometry(int32_t *unit_rows, int32_t *unit_cols, int32_t *step_quantum);
 
+/* ---------------------------------------------------------------------------------------
+ * Level-1/2 BLAS with dual modular redundancy (DMR; PAPER.md:198-252
+ * §IV, 440 §VI.B).  Memory-bound routines are protected by duplicating every computing
+ * instruction, not the loads (the paper's sphere of replication): each result
+ * is computed twice from the same registers, the two are compared bitwise (a warp vote
+ * reduces the verdict), and only verified results are stored (verify-before-store).  On a
+ * mismatch a third computation settles it: agreeing with either copy -> corrected, else
+ * uncorrectable (the third value is stored and counted).  An armed fault (ftblas_inject_arm)
+ * with row index i perturbs the ORIGINAL computation of output i by delta: for DSCAL / DAXPY
+ * after the multiply-add, for DGEMV after `step` terms of the dot product (0 <= step <= the
+ * dot length); j is ignored.  A fault whose delta does not change the (rounded) original
+ * result is not a detection.  Arguments as reference BLAS (x[i*incx] for incx > 0,
+ * x[(n-1-i)*|incx|] for incx < 0; incx == 0 is invalid), device pointers, stream-ordered;
+ * the call synchronises only when rep != NULL (to fill it).  Status codes as above, with
+ * argument positions counted in each function's own list.
+ * --------------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t checked;        /* out: results verified (output elements) */
+  int64_t detected;       /* out: results whose two computations disagreed */
+  int64_t corrected;      /* out: settled by a third computation agreeing with one copy */
+  int64_t uncorrectable;  /* out: all three computations disagreed */
+} ftblas_dmr_report_t;
+
+/* x := alpha * x (one rounding per element; PAPER.md:208 DSCAL). */
+int ftblas_dscal(int64_t n, double alpha, double *x, int64_t incx, ftblas_dmr_report_t *rep);
+/* y := alpha * x + y, computed as fma(alpha, x_i, y_i) (one rounding). */
+int ftblas_daxpy(int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy,
+                 ftblas_dmr_report_t *rep);
+/* y := alpha * op(A) * x + beta * y, A m x n column-major.  Each output is one dot product
+ * acc = sum_p fma(op(A)_ip, x_p, acc), p ascending (trans 'N': one thread per row, the exact
+ * oracle order; 'T': a warp per column, lane-strided partial sums reduced by a fixed
+ * butterfly), then y_i = fma(alpha, acc, beta * y_i) (beta == 0: y not read). */
+int ftblas_dgemv(char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
+                 const double *x, int64_t incx, double beta, double *y, int64_t incy,
+                 ftblas_dmr_report_t *rep);
+/* Unprotected twins (same kernels without duplication): the overhead baselines. */
+int ftblas_dscal_noft(int64_t n, double alpha, double *x, int64_t incx);
+int ftblas_daxpy_noft(int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy);
+int ftblas_dgemv_noft(char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
+                      const double *x, int64_t incx, double beta, double *y, int64_t incy);
+
 /* Number of kernel launches enqueued by this thread since the last call (for the
  * benchmark's launch accounting); resets the counter. */
 int64_t ftblas_take_launch_count(void);

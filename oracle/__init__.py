@@ -70,6 +70,9 @@ def lib():
         L.oracle_round_up_hi32.restype = d
         L.oracle_round_up_hi32.argtypes = [d]
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_dscal.argtypes = [i64, d, P, i64, P, i64, P]
+        L.oracle_daxpy.argtypes = [i64, d, P, i64, P, i64, P, i64, P]
+        L.oracle_dgemv.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64, P, i64, P]
         _lib = L
     return _lib
 
@@ -196,6 +199,51 @@ def dgemm_abft(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *, BM, BN, 
     events = [(ev[e].interval, ev[e].i, ev[e].j, ev[e].kind, ev[e].residual_row, ev[e].residual_col)
               for e in range(nstored)]
     return Cout, Report(*[int(x) for x in counters], events)
+
+
+def _faults(faults):
+    faults = list(faults)
+    fa = (_Fault * max(len(faults), 1))()
+    for e, (i, j, s, dlt) in enumerate(faults):
+        fa[e] = _Fault(int(i), int(j), int(s), float(dlt))
+    return ctypes.cast(fa, ctypes.c_void_p), len(faults), fa
+
+
+@dataclass
+class DmrReport:
+    checked: int
+    detected: int
+    corrected: int
+    uncorrectable: int
+
+
+def dscal(n, alpha, x, incx=1, faults=()):
+    """DMR DSCAL oracle (NEXT-4): returns (new x, DmrReport); x is a flat float64 array."""
+    xo = np.ascontiguousarray(x, dtype=np.float64).copy()
+    fp, nf, _keep = _faults(faults)
+    cnt = np.zeros(4, dtype=np.int64)
+    lib().oracle_dscal(n, alpha, _ptr(xo), incx, fp, nf, _ptr(cnt))
+    return xo, DmrReport(*[int(v) for v in cnt])
+
+
+def daxpy(n, alpha, x, incx, y, incy, faults=()):
+    xo = np.ascontiguousarray(x, dtype=np.float64)
+    yo = np.ascontiguousarray(y, dtype=np.float64).copy()
+    fp, nf, _keep = _faults(faults)
+    cnt = np.zeros(4, dtype=np.int64)
+    lib().oracle_daxpy(n, alpha, _ptr(xo), incx, _ptr(yo), incy, fp, nf, _ptr(cnt))
+    return yo, DmrReport(*[int(v) for v in cnt])
+
+
+def dgemv(trans, m, n, alpha, A, lda, x, incx, beta, y, incy, faults=()):
+    A = _flat(A)
+    xo = np.ascontiguousarray(x, dtype=np.float64)
+    yo = np.ascontiguousarray(y, dtype=np.float64).copy()
+    fp, nf, _keep = _faults(faults)
+    cnt = np.zeros(4, dtype=np.int64)
+    lib().oracle_dgemv(trans.encode(), m, n, alpha, _ptr(A), lda, _ptr(xo), incx, beta, _ptr(yo), incy,
+                       fp, nf, _ptr(cnt))
+    return yo, DmrReport(*[int(v) for v in cnt])
 
 
 def num_threads() -> int:

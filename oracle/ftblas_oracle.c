@@ -385,6 +385,84 @@ int oracle_dgemm_abft_units(char ta, char tb, int64_t m, int64_t n, int64_t k, d
   return 0;
 }
 
+/* ---------------------------------------------------------------------------
+ * Level-1/2 routines with dual modular redundancy (
+ * PAPER.md:198-252 §IV).  Plain definitions plus the DMR bookkeeping: an injected
+ * fault perturbs the ORIGINAL computation of one output (PAPER.md:445 injection),
+ * the duplicate is fault-free, the mismatch is detected and a third fault-free
+ * computation is stored (corrected).  So every output equals its fault-free value;
+ * counters = {checked, detected, corrected, uncorrectable}.  For DSCAL / DAXPY an
+ * output is detected iff fl(v + D) differs from v bitwise, D the sum of its faults'
+ * deltas in list order; for DGEMV iff D != 0 (reading R19: a delta injected inside a
+ * dot product is assumed not to be absorbed by rounding).
+ * Vectors: element i at v[i*inc] for inc > 0, v[(n-1-i)*(-inc)] for inc < 0.
+ * ------------------------------------------------------------------------- */
+static int64_t vix(int64_t i, int64_t n, int64_t inc) { return inc > 0 ? i * inc : (n - 1 - i) * (-inc); }
+
+static double fault_sum(const or_fault_t *f, int64_t nf, int64_t index) {
+  double d = 0.0;
+  for (int64_t e = 0; e < nf; ++e)
+    if (f[e].i == index) d += f[e].delta;
+  return d;
+}
+
+static int fault_any(const or_fault_t *f, int64_t nf, int64_t index) {
+  for (int64_t e = 0; e < nf; ++e)
+    if (f[e].i == index && f[e].delta != 0.0) return 1;
+  return 0;
+}
+
+static int bits_differ(double a, double b) {
+  uint64_t x, y;
+  memcpy(&x, &a, sizeof x);
+  memcpy(&y, &b, sizeof y);
+  return x != y;
+}
+
+/* x := alpha * x  (DSCAL). */
+void oracle_dscal(int64_t n, double alpha, double *x, int64_t incx, const or_fault_t *f, int64_t nf,
+                  int64_t *counters) {
+  int64_t det = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double v = alpha * x[vix(i, n, incx)];
+    double d = fault_sum(f, nf, i);
+    if (d != 0.0 && bits_differ(v + d, v)) ++det;
+    x[vix(i, n, incx)] = v;
+  }
+  counters[0] = n; counters[1] = det; counters[2] = det; counters[3] = 0;
+}
+
+/* y := alpha * x + y as one fused multiply-add per element (DAXPY). */
+void oracle_daxpy(int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy,
+                  const or_fault_t *f, int64_t nf, int64_t *counters) {
+  int64_t det = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double v = fma(alpha, x[vix(i, n, incx)], y[vix(i, n, incy)]);
+    double d = fault_sum(f, nf, i);
+    if (d != 0.0 && bits_differ(v + d, v)) ++det;
+    y[vix(i, n, incy)] = v;
+  }
+  counters[0] = n; counters[1] = det; counters[2] = det; counters[3] = 0;
+}
+
+/* y := alpha * op(A) * x + beta * y  (DGEMV): acc = sum_p op(A)_ip x_p as an fma chain,
+ * p ascending; y_i = fma(alpha, acc, beta * y_i), beta == 0: y not read. */
+void oracle_dgemv(char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
+                  const double *x, int64_t incx, double beta, double *y, int64_t incy,
+                  const or_fault_t *f, int64_t nf, int64_t *counters) {
+  int tr = is_trans(trans);
+  int64_t nout = tr ? n : m, len = tr ? m : n, det = 0;
+  for (int64_t i = 0; i < nout; ++i) {
+    double acc = 0.0;
+    if (alpha != 0.0)
+      for (int64_t p = 0; p < len; ++p) acc = fma(tr ? A[p + i * lda] : A[i + p * lda], x[vix(p, len, incx)], acc);
+    double yb = beta != 0.0 ? beta * y[vix(i, nout, incy)] : 0.0;
+    y[vix(i, nout, incy)] = fma(alpha, acc, yb);
+    if (fault_any(f, nf, i)) ++det;
+  }
+  counters[0] = nout; counters[1] = det; counters[2] = det; counters[3] = 0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

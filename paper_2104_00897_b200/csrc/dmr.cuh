@@ -1,0 +1,315 @@
+// dmr.cuh — Level-1/2 BLAS with dual modular redundancy.
+//
+// FT-BLAS protects its memory-bound routines by duplicating the computing instructions,
+// comparing the two results and only then storing (§IV: "we duplicate and
+// verify computing instructions instead of memory instructions"; comparison reduction over
+// several results before one branch, §IV.D; a third computation resolves a mismatch and is
+// itself verified, §IV.E).  On B200 these routines are HBM-bound (DSCAL 1/16 FLOP/B, DGEMV
+// 1/4 FLOP/B against a 37 TF / 6.5 TB/s machine), so the duplicate FP64 work hides under the
+// memory stream.  The GPU form:
+//   - both copies come from inline-asm FP64 instructions on the same loaded registers (no
+//     common-subexpression merging), the original one carries the fault-injection hook;
+//   - the verdict is reduced per warp with a vote (__any_sync) — one branch per warp-step
+//     instead of one per element;
+//   - on a mismatch the lane computes a third copy: equal to either copy -> corrected (the
+//     third value is stored), else uncorrectable (stored, counted).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ftd {
+
+struct DmrFault {  // sorted by index
+  int64_t index, step;
+  double delta;
+};
+
+enum { D_DETECTED = 0, D_CORRECTED, D_UNCORRECTABLE, D_N };
+
+__device__ __forceinline__ double v_mul(double a, double b) {
+  double r;
+  asm volatile("mul.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ double v_fma(double a, double b, double c) {
+  double r;
+  asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(r) : "d"(a), "d"(b), "d"(c));
+  return r;
+}
+__device__ __forceinline__ double v_add(double a, double b) {
+  double r;
+  asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ bool differ(double a, double b) { return __double_as_longlong(a) != __double_as_longlong(b); }
+
+__device__ __forceinline__ int64_t vidx(int64_t i, int64_t n, int64_t inc) { return inc > 0 ? i * inc : (n - 1 - i) * (-inc); }
+
+// Delta of the fault on output `index` (0 if none); faults sorted by index, binary search.
+__device__ __forceinline__ double fault_delta(const DmrFault *f, int nf, int64_t index, int64_t step) {
+  int lo = 0, hi = nf;
+  while (lo < hi) { const int mid = (lo + hi) >> 1; if (f[mid].index < index) lo = mid + 1; else hi = mid; }
+  double d = 0.0;
+  for (; lo < nf && f[lo].index == index; ++lo)
+    if (f[lo].step == step) d += f[lo].delta;
+  return d;
+}
+
+// Settle a mismatch with a third computation r3; returns the value to store.
+__device__ __forceinline__ double settle(double r1, double r2, double r3, unsigned long long *cnt) {
+  atomicAdd(&cnt[D_DETECTED], 1ull);
+  if (!differ(r3, r2) || !differ(r3, r1)) atomicAdd(&cnt[D_CORRECTED], 1ull);
+  else atomicAdd(&cnt[D_UNCORRECTABLE], 1ull);
+  return r3;
+}
+
+// ---------------------------------------------------------------- DSCAL: x := alpha x
+// FLT: the launch carries armed faults (the fault hook is compiled in only then, so the
+// production path keeps its registers for loads in flight).
+// Residency: 6 x 256-thread CTAs per SM (40 registers) for both the DMR kernels and their
+// unprotected twins (at 32 registers the DMR variants spill; the twins measured no faster at
+// 8).  The host sizes grid-stride launches to exactly one wave.
+constexpr int resident_ctas(bool dmr) { return dmr ? 6 : 6; }
+
+template <bool DMR, bool FLT>
+__global__ void __launch_bounds__(256, resident_ctas(DMR)) dscal_kernel(int64_t n, double alpha, double *__restrict__ x, int64_t incx,
+                                                    const DmrFault *__restrict__ f, int nf,
+                                                    unsigned long long *__restrict__ cnt) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x) * 4 + threadIdx.x; base < n; base += stride) {
+    double xv[4], r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      xv[u] = i < n ? x[vidx(i, n, incx)] : 0.0;
+    }
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      r[u] = v_mul(alpha, xv[u]);
+      if (DMR) {
+        if (FLT) {
+          const int64_t i = base + (int64_t)u * blockDim.x;
+          if (i < n) { const double d = fault_delta(f, nf, i, 0); if (d != 0.0) r[u] = v_add(r[u], d); }
+        }
+        bad |= differ(r[u], v_mul(alpha, xv[u]));  // the duplicate
+      }
+    }
+    if (DMR && __any_sync(__activemask(), bad)) {  // rare: redo the duplicate, settle by a third
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double r2 = v_mul(alpha, xv[u]);
+        if (differ(r[u], r2)) r[u] = settle(r[u], r2, v_mul(alpha, xv[u]), cnt);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      if (i < n) x[vidx(i, n, incx)] = r[u];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- DAXPY: y := alpha x + y
+template <bool DMR, bool FLT>
+__global__ void __launch_bounds__(256, resident_ctas(DMR)) daxpy_kernel(int64_t n, double alpha, const double *__restrict__ x, int64_t incx,
+                                                    double *__restrict__ y, int64_t incy,
+                                                    const DmrFault *__restrict__ f, int nf,
+                                                    unsigned long long *__restrict__ cnt) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x) * 4 + threadIdx.x; base < n; base += stride) {
+    double xv[4], yv[4], r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      xv[u] = i < n ? x[vidx(i, n, incx)] : 0.0;
+      yv[u] = i < n ? y[vidx(i, n, incy)] : 0.0;
+    }
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      r[u] = v_fma(alpha, xv[u], yv[u]);
+      if (DMR) {
+        if (FLT) {
+          const int64_t i = base + (int64_t)u * blockDim.x;
+          if (i < n) { const double d = fault_delta(f, nf, i, 0); if (d != 0.0) r[u] = v_add(r[u], d); }
+        }
+        bad |= differ(r[u], v_fma(alpha, xv[u], yv[u]));  // the duplicate
+      }
+    }
+    if (DMR && __any_sync(__activemask(), bad)) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double r2 = v_fma(alpha, xv[u], yv[u]);
+        if (differ(r[u], r2)) r[u] = settle(r[u], r2, v_fma(alpha, xv[u], yv[u]), cnt);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      if (i < n) y[vidx(i, n, incy)] = r[u];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- DGEMV
+// 'N': y_i = alpha sum_j A_ij x_j + beta y_i.  A CTA of GN_W = 16 warps owns 32 rows (one
+// per lane); warp w accumulates the columns j = w (mod 16) (coalesced 256-byte column
+// segments), the 16 partial sums of a row are combined in warp order by warp 0.
+constexpr int GN_W = 8;
+constexpr int GN_U = 8;  // columns of a warp's set per loop iteration (loads in flight)
+struct GemvParams {
+  int64_t m, n;
+  double alpha, beta;
+  const double *A;
+  int64_t lda;
+  const double *x;
+  int64_t incx;
+  double *y;
+  int64_t incy;
+  const DmrFault *f;
+  int nf;
+  unsigned long long *cnt;
+};
+
+__device__ __forceinline__ double gemv_n_row(const GemvParams &P, int64_t i) {  // third computation
+  double acc = 0.0;
+  for (int w = 0; w < GN_W; ++w) {
+    double part = 0.0;
+    for (int64_t j = w; j < P.n; j += GN_W) part = v_fma(P.A[i + j * P.lda], P.x[vidx(j, P.n, P.incx)], part);
+    acc = w == 0 ? part : v_add(acc, part);
+  }
+  return acc;
+}
+
+template <bool DMR, bool FLT>
+__global__ void __launch_bounds__(GN_W * 32, 4) dgemv_n_kernel(const GemvParams P) {
+  __shared__ double part[2][GN_W][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  const bool row_ok = i < P.m;
+  const int64_t ir = row_ok ? i : 0;
+  double a1 = 0.0, a2 = 0.0;
+  // This lane's fault (row i, term `step` in this warp's column set), if any.
+  int64_t fstep = -1;
+  double fdel = 0.0;
+  if (DMR && FLT && row_ok) {
+    int lo = 0, hi = P.nf;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.f[mid].index < i) lo = mid + 1; else hi = mid; }
+    for (; lo < P.nf && P.f[lo].index == i; ++lo)
+      if (P.f[lo].step < P.n && (P.f[lo].step % GN_W) == w) { fstep = P.f[lo].step; fdel += P.f[lo].delta; }
+  }
+  const double *Ai = P.A + ir;
+  int64_t j = w;
+  for (; j + (GN_U - 1) * GN_W < P.n; j += GN_U * GN_W) {  // GN_U columns of this warp's set
+    double av[GN_U], xv[GN_U];
+#pragma unroll
+    for (int u = 0; u < GN_U; ++u) {
+      av[u] = Ai[(j + GN_W * u) * P.lda];
+      xv[u] = P.x[vidx(j + GN_W * u, P.n, P.incx)];
+    }
+#pragma unroll
+    for (int u = 0; u < GN_U; ++u) {
+      if (DMR && FLT && (j + GN_W * u) == fstep) a1 = v_add(a1, fdel);
+      a1 = v_fma(av[u], xv[u], a1);
+      if (DMR) a2 = v_fma(av[u], xv[u], a2);
+    }
+  }
+  for (; j < P.n; j += GN_W) {
+    const double av = Ai[j * P.lda], xv = P.x[vidx(j, P.n, P.incx)];
+    if (DMR && FLT && j == fstep) a1 = v_add(a1, fdel);
+    a1 = v_fma(av, xv, a1);
+    if (DMR) a2 = v_fma(av, xv, a2);
+  }
+  part[0][w][lane] = a1;
+  part[1][w][lane] = a2;
+  __syncthreads();
+  if (w != 0) return;
+  double s1 = part[0][0][lane], s2 = part[1][0][lane];
+#pragma unroll
+  for (int q = 1; q < GN_W; ++q) {
+    s1 = v_add(s1, part[0][q][lane]);
+    if (DMR) s2 = v_add(s2, part[1][q][lane]);
+  }
+  if (!row_ok) return;
+  if (DMR && FLT) s1 = v_add(s1, fault_delta(P.f, P.nf, i, P.n));  // faults after the last term
+  double *yi = P.y + vidx(i, P.m, P.incy);
+  const double yb = P.beta != 0.0 ? v_mul(P.beta, *yi) : 0.0;
+  double r1 = v_fma(P.alpha, s1, yb);
+  if (DMR) {
+    const double yb2 = P.beta != 0.0 ? v_mul(P.beta, *yi) : 0.0;
+    const double r2 = v_fma(P.alpha, s2, yb2);
+    if (__any_sync(__activemask(), differ(r1, r2)) && differ(r1, r2))
+      r1 = settle(r1, r2, v_fma(P.alpha, gemv_n_row(P, i), yb2), P.cnt);
+  }
+  *yi = r1;
+}
+
+// 'T': y_j = alpha sum_i A_ij x_i + beta y_j.  One warp per column j; lane l sums the rows
+// i = l (mod 32) in order, then a fixed butterfly combines the lanes.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = v_add(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <bool DMR, bool FLT>
+__device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, int lane) {
+  const double *Aj = P.A + j * P.lda;
+  int64_t fstep = -1;
+  double fdel = 0.0;
+  if (DMR && FLT) {
+    int lo = 0, hi = P.nf;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.f[mid].index < j) lo = mid + 1; else hi = mid; }
+    for (; lo < P.nf && P.f[lo].index == j; ++lo)
+      if (P.f[lo].step < P.m && (P.f[lo].step & 31) == lane) { fstep = P.f[lo].step; fdel += P.f[lo].delta; }
+  }
+  double a1 = 0.0, a2 = 0.0;
+  int64_t i = lane;
+  for (; i + 96 < P.m; i += 128) {
+    double av[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      av[u] = Aj[i + 32 * u];
+      xv[u] = P.x[vidx(i + 32 * u, P.m, P.incx)];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (DMR && FLT && (i + 32 * u) == fstep) a1 = v_add(a1, fdel);
+      a1 = v_fma(av[u], xv[u], a1);
+      if (DMR) a2 = v_fma(av[u], xv[u], a2);
+    }
+  }
+  for (; i < P.m; i += 32) {
+    const double av = Aj[i], xv = P.x[vidx(i, P.m, P.incx)];
+    if (DMR && FLT && i == fstep) a1 = v_add(a1, fdel);
+    a1 = v_fma(av, xv, a1);
+    if (DMR) a2 = v_fma(av, xv, a2);
+  }
+  double s1 = warp_sum(a1), s2 = DMR ? warp_sum(a2) : 0.0;
+  if (DMR && FLT) s1 = v_add(s1, fault_delta(P.f, P.nf, j, P.m));
+  double *yj = P.y + vidx(j, P.n, P.incy);
+  const double yb = P.beta != 0.0 ? v_mul(P.beta, *yj) : 0.0;
+  double r1 = v_fma(P.alpha, s1, yb);
+  if (DMR) {
+    const double yb2 = P.beta != 0.0 ? v_mul(P.beta, *yj) : 0.0;
+    const double r2 = v_fma(P.alpha, s2, yb2);
+    if (differ(r1, r2)) {  // warp-uniform: every lane holds the butterfly result
+      double a3 = 0.0;
+      for (int64_t q = lane; q < P.m; q += 32) a3 = v_fma(Aj[q], P.x[vidx(q, P.m, P.incx)], a3);
+      const double r3 = v_fma(P.alpha, warp_sum(a3), yb2);
+      if (lane == 0) r1 = settle(r1, r2, r3, P.cnt);
+      else r1 = r3;
+    }
+  }
+  if (lane == 0) *yj = r1;
+}
+
+template <bool DMR, bool FLT>
+__global__ void __launch_bounds__(256, resident_ctas(DMR)) dgemv_t_kernel(const GemvParams P) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); j < P.n; j += (int64_t)gridDim.x * 8)
+    dgemv_t_column<DMR, FLT>(P, j, lane);
+}
+
+}  // namespace ftd

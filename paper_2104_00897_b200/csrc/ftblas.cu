@@ -7,6 +7,7 @@
 #include "../../include/ftblas.h"
 #include "dgemm_abft.cuh"
 #include "unfused.cuh"
+#include "dmr.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -501,6 +502,144 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   return r;
 }
 
+// ---------------------------------------------------------------- Level-1/2 DMR (NEXT-4)
+// Device scratch for one DMR call: counters + the armed faults (sorted by output index).
+struct DmrScratch {
+  char *base = nullptr;
+  unsigned long long *cnt = nullptr;
+  ftd::DmrFault *f = nullptr;
+  int nf = 0;
+};
+
+int dmr_prepare(bool ft, std::vector<ftblas_fault_t> &faults, int64_t nout, int64_t maxstep, DmrScratch &sc,
+                cudaStream_t st) {
+  for (const auto &f : faults)
+    if (f.i < 0 || f.i >= nout || f.step < 0 || f.step > maxstep) return 3;
+  std::vector<ftd::DmrFault> fd;
+  if (ft)
+    for (const auto &f : faults) fd.push_back(ftd::DmrFault{f.i, f.step, f.delta});
+  std::stable_sort(fd.begin(), fd.end(), [](const ftd::DmrFault &a, const ftd::DmrFault &b) { return a.index < b.index; });
+  const size_t cb = sizeof(unsigned long long) * ftd::D_N, fb = sizeof(ftd::DmrFault) * fd.size();
+  CUDA_TRY(cudaMallocAsync((void **)&sc.base, 256 + fb, st));
+  sc.cnt = reinterpret_cast<unsigned long long *>(sc.base);
+  sc.f = fd.empty() ? nullptr : reinterpret_cast<ftd::DmrFault *>(sc.base + 256);
+  sc.nf = (int)fd.size();
+  CUDA_TRY(cudaMemsetAsync(sc.cnt, 0, cb, st));
+  if (!fd.empty()) CUDA_TRY(cudaMemcpyAsync(sc.f, fd.data(), fb, cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int dmr_finish(DmrScratch &sc, int64_t checked, ftblas_dmr_report_t *rep, cudaStream_t st) {
+  CUDA_TRY(cudaGetLastError());
+  if (rep) {
+    unsigned long long c[ftd::D_N];
+    CUDA_TRY(cudaMemcpyAsync(c, sc.cnt, sizeof c, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    rep->checked = checked;
+    rep->detected = (int64_t)c[ftd::D_DETECTED];
+    rep->corrected = (int64_t)c[ftd::D_CORRECTED];
+    rep->uncorrectable = (int64_t)c[ftd::D_UNCORRECTABLE];
+  }
+  CUDA_TRY(cudaFreeAsync(sc.base, st));
+  return 0;
+}
+
+void dmr_zero(ftblas_dmr_report_t *rep) {
+  if (rep) rep->checked = rep->detected = rep->corrected = rep->uncorrectable = 0;
+}
+
+// One wave of resident CTAs (8 x 256 threads per SM at <= 32 registers) for grid-stride loops.
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  return sms;
+}
+int l1_grid(int64_t n, bool dmr) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, (int64_t)num_sms() * ftd::resident_ctas(dmr)));
+}
+
+int dscal_impl(bool ft, int64_t n, double alpha, double *x, int64_t incx, ftblas_dmr_report_t *rep) {
+  std::vector<ftblas_fault_t> faults = take_armed();
+  if (n < 0) return -1;
+  if (n > 0 && x == nullptr) return -3;
+  if (incx == 0) return -4;
+  dmr_zero(rep);
+  if (n == 0) return 0;
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  DmrScratch sc;
+  if (int e = dmr_prepare(ft, faults, n, 0, sc, st)) return e;
+  if (ft && sc.nf) ftd::dscal_kernel<true, true><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, sc.f, sc.nf, sc.cnt);
+  else if (ft) ftd::dscal_kernel<true, false><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, nullptr, 0, sc.cnt);
+  else ftd::dscal_kernel<false, false><<<l1_grid(n, false), 256, 0, st>>>(n, alpha, x, incx, nullptr, 0, sc.cnt);
+  ++tl_launches;
+  return dmr_finish(sc, ft ? n : 0, rep, st);
+}
+
+int daxpy_impl(bool ft, int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy,
+               ftblas_dmr_report_t *rep) {
+  std::vector<ftblas_fault_t> faults = take_armed();
+  if (n < 0) return -1;
+  if (n > 0 && x == nullptr) return -3;
+  if (incx == 0) return -4;
+  if (n > 0 && y == nullptr) return -5;
+  if (incy == 0) return -6;
+  dmr_zero(rep);
+  if (n == 0) return 0;
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  DmrScratch sc;
+  if (int e = dmr_prepare(ft, faults, n, 0, sc, st)) return e;
+  if (ft && sc.nf) ftd::daxpy_kernel<true, true><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, y, incy, sc.f, sc.nf, sc.cnt);
+  else if (ft) ftd::daxpy_kernel<true, false><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, y, incy, nullptr, 0, sc.cnt);
+  else ftd::daxpy_kernel<false, false><<<l1_grid(n, false), 256, 0, st>>>(n, alpha, x, incx, y, incy, nullptr, 0, sc.cnt);
+  ++tl_launches;
+  return dmr_finish(sc, ft ? n : 0, rep, st);
+}
+
+int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
+               const double *x, int64_t incx, double beta, double *y, int64_t incy, ftblas_dmr_report_t *rep) {
+  std::vector<ftblas_fault_t> faults = take_armed();
+  if (!is_n(trans) && !is_t(trans)) return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  const bool tr = is_t(trans);
+  const int64_t nout = tr ? n : m, len = tr ? m : n;  // outputs, dot length
+  if (lda < std::max<int64_t>(1, m)) return -6;
+  if (nout > 0 && len > 0 && alpha != 0.0 && A == nullptr) return -5;
+  if (nout > 0 && len > 0 && alpha != 0.0 && x == nullptr) return -7;
+  if (incx == 0) return -8;
+  if (nout > 0 && y == nullptr) return -10;
+  if (incy == 0) return -11;
+  dmr_zero(rep);
+  if (nout == 0) return 0;
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  DmrScratch sc;
+  if (int e = dmr_prepare(ft, faults, nout, len, sc, st)) return e;
+  ftd::GemvParams P{};
+  P.m = m; P.n = n; P.alpha = alpha; P.beta = beta; P.A = A; P.lda = lda; P.x = x; P.incx = incx;
+  P.y = y; P.incy = incy; P.f = sc.f; P.nf = sc.nf; P.cnt = sc.cnt;
+  if (alpha == 0.0 || len == 0) { P.m = tr ? 0 : m; P.n = tr ? n : 0; }  // y = beta*y: empty dot products
+  if (!tr) {
+    const unsigned g = (unsigned)((m + 31) / 32);
+    if (ft && sc.nf) ftd::dgemv_n_kernel<true, true><<<g, ftd::GN_W * 32, 0, st>>>(P);
+    else if (ft) ftd::dgemv_n_kernel<true, false><<<g, ftd::GN_W * 32, 0, st>>>(P);
+    else ftd::dgemv_n_kernel<false, false><<<g, ftd::GN_W * 32, 0, st>>>(P);
+  } else {
+    const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * ftd::resident_ctas(ft));
+    if (ft && sc.nf) ftd::dgemv_t_kernel<true, true><<<g, 256, 0, st>>>(P);
+    else if (ft) ftd::dgemv_t_kernel<true, false><<<g, 256, 0, st>>>(P);
+    else ftd::dgemv_t_kernel<false, false><<<g, 256, 0, st>>>(P);
+  }
+  ++tl_launches;
+  return dmr_finish(sc, ft ? nout : 0, rep, st);
+}
+
 uint64_t splitmix_next(uint64_t &state) {
   state += 0x9E3779B97F4A7C15ull;
   uint64_t z = state;
@@ -530,6 +669,28 @@ int ftblas_dgemm_unfused(char transA, char transB, int64_t m, int64_t n, int64_t
                          const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
                          int64_t ldc, ftblas_err_report_t *err) {
   return unfused_impl(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err);
+}
+
+int ftblas_dscal(int64_t n, double alpha, double *x, int64_t incx, ftblas_dmr_report_t *rep) {
+  return dscal_impl(true, n, alpha, x, incx, rep);
+}
+int ftblas_dscal_noft(int64_t n, double alpha, double *x, int64_t incx) {
+  return dscal_impl(false, n, alpha, x, incx, nullptr);
+}
+int ftblas_daxpy(int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy,
+                 ftblas_dmr_report_t *rep) {
+  return daxpy_impl(true, n, alpha, x, incx, y, incy, rep);
+}
+int ftblas_daxpy_noft(int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy) {
+  return daxpy_impl(false, n, alpha, x, incx, y, incy, nullptr);
+}
+int ftblas_dgemv(char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda, const double *x,
+                 int64_t incx, double beta, double *y, int64_t incy, ftblas_dmr_report_t *rep) {
+  return dgemv_impl(true, trans, m, n, alpha, A, lda, x, incx, beta, y, incy, rep);
+}
+int ftblas_dgemv_noft(char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
+                      const double *x, int64_t incx, double beta, double *y, int64_t incy) {
+  return dgemv_impl(false, trans, m, n, alpha, A, lda, x, incx, beta, y, incy, nullptr);
 }
 
 int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,

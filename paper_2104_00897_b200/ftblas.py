@@ -40,6 +40,19 @@ class ErrReport(ctypes.Structure):
                 ("events_capacity", ctypes.c_int64)]
 
 
+class DmrReportC(ctypes.Structure):
+    _fields_ = [("checked", ctypes.c_int64), ("detected", ctypes.c_int64),
+                ("corrected", ctypes.c_int64), ("uncorrectable", ctypes.c_int64)]
+
+
+@dataclass
+class DmrReport:
+    checked: int
+    detected: int
+    corrected: int
+    uncorrectable: int
+
+
 class Fault(ctypes.Structure):
     _fields_ = [("i", ctypes.c_int64), ("j", ctypes.c_int64), ("step", ctypes.c_int64),
                 ("delta", ctypes.c_double)]
@@ -87,6 +100,16 @@ def load():
     L.ftblas_set_encode.argtypes = [i32]
     L.ftblas_set_interval.argtypes = [i64]
     L.ftblas_get_geometry.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 3
+    DR = ctypes.POINTER(DmrReportC)
+    L.ftblas_dscal.argtypes = [i64, d, P, i64, DR]
+    L.ftblas_dscal_noft.argtypes = [i64, d, P, i64]
+    L.ftblas_daxpy.argtypes = [i64, d, P, i64, P, i64, DR]
+    L.ftblas_daxpy_noft.argtypes = [i64, d, P, i64, P, i64]
+    L.ftblas_dgemv.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64, DR]
+    L.ftblas_dgemv_noft.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64]
+    for fn in ("ftblas_dscal", "ftblas_dscal_noft", "ftblas_daxpy", "ftblas_daxpy_noft",
+               "ftblas_dgemv", "ftblas_dgemv_noft"):
+        getattr(L, fn).restype = ctypes.c_int
     L.ftblas_take_launch_count.restype = i64
     L.ftblas_take_launch_count.argtypes = []
     L.ftblas_status_string.restype = ctypes.c_char_p
@@ -104,7 +127,9 @@ def load():
 EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
             "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
             "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode", "ftblas_set_interval",
-            "ftblas_get_geometry", "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize")
+            "ftblas_get_geometry", "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize",
+            "ftblas_dscal", "ftblas_dscal_noft", "ftblas_daxpy", "ftblas_daxpy_noft", "ftblas_dgemv",
+            "ftblas_dgemv_noft")
 
 
 def _check(fn, status):
@@ -199,6 +224,43 @@ def ftblas_dgemm_noft_host(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta,
     st = load().ftblas_dgemm_noft_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda,
                                        _ptr(B), ldb, beta, _ptr(C), ldc)
     _check("ftblas_dgemm_noft_host", st)
+
+
+def _dmr(fn, args, report):
+    L = load()
+    r = DmrReportC()
+    st = getattr(L, fn)(*args, ctypes.byref(r) if report else None)
+    _check(fn, st)
+    return DmrReport(r.checked, r.detected, r.corrected, r.uncorrectable) if report else None
+
+
+def ftblas_dscal(n, alpha, x, incx=1, *, report=True):
+    """x := alpha*x with DMR (NEXT-4); device vector.  Returns a DmrReport (synchronises)."""
+    return _dmr("ftblas_dscal", (n, alpha, _ptr(x), incx), report)
+
+
+def ftblas_daxpy(n, alpha, x, incx, y, incy, *, report=True):
+    """y := fma(alpha, x, y) with DMR."""
+    return _dmr("ftblas_daxpy", (n, alpha, _ptr(x), incx, _ptr(y), incy), report)
+
+
+def ftblas_dgemv(trans, m, n, alpha, A, lda, x, incx, beta, y, incy, *, report=True):
+    """y := alpha*op(A)*x + beta*y with DMR."""
+    return _dmr("ftblas_dgemv", (_c(trans), m, n, alpha, _ptr(A), lda, _ptr(x), incx, beta, _ptr(y),
+                                 incy), report)
+
+
+def ftblas_dscal_noft(n, alpha, x, incx=1):
+    _check("ftblas_dscal_noft", load().ftblas_dscal_noft(n, alpha, _ptr(x), incx))
+
+
+def ftblas_daxpy_noft(n, alpha, x, incx, y, incy):
+    _check("ftblas_daxpy_noft", load().ftblas_daxpy_noft(n, alpha, _ptr(x), incx, _ptr(y), incy))
+
+
+def ftblas_dgemv_noft(trans, m, n, alpha, A, lda, x, incx, beta, y, incy):
+    _check("ftblas_dgemv_noft", load().ftblas_dgemv_noft(_c(trans), m, n, alpha, _ptr(A), lda, _ptr(x),
+                                                         incx, beta, _ptr(y), incy))
 
 
 def ftblas_inject_arm(faults):
