@@ -202,10 +202,21 @@ int launch_block_sum(const double *X, bool xc, int64_t ld, int64_t nx, int64_t n
   return 0;
 }
 
+// Where a protected call accumulates its report when it is one piece of a larger call (the
+// row panels of the host-buffer pipeline): shared device counters / events, zeroed by the
+// caller; no synchronisation inside.
+struct ReportSink {
+  unsigned long long *counters;
+  ftk::EventDev *events;
+  int64_t ev_cap;
+  int64_t row_off;  // global row of this piece's row 0
+  int64_t units;    // out: accumulated units checked
+};
+
 // The core entry: device pointers, protected (FT) or not, explicit fault list.
 int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char tb, int64_t m, int64_t n,
                int64_t k, double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
-               double *C, int64_t ldc, ftblas_err_report_t *err) {
+               double *C, int64_t ldc, ftblas_err_report_t *err, ReportSink *sink = nullptr) {
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
   if (rc) return rc;
   zero_report(err, k);
@@ -287,12 +298,14 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
     p.Ac = Ac; p.Br = Br; p.ldac = p.tiles_m; p.ldbr = p.tiles_n;
     p.amax_pre = hm; p.bmax_pre = hm + p.tiles_m;
   }
-  p.counters = reinterpret_cast<unsigned long long *>(scratch);
-  p.events = reinterpret_cast<ftk::EventDev *>(scratch + cnt_bytes);
-  p.ev_cap = ev_cap;
+  p.counters = sink ? sink->counters : reinterpret_cast<unsigned long long *>(scratch);
+  p.events = sink ? sink->events : reinterpret_cast<ftk::EventDev *>(scratch + cnt_bytes);
+  p.ev_cap = sink ? sink->ev_cap : ev_cap;
+  p.ev_row_off = sink ? sink->row_off : 0;
+  if (sink && ft) sink->units += (int64_t)p.ntiles * T;
   p.faults = fd.empty() ? nullptr : reinterpret_cast<const ftk::FaultDev *>(scratch + cnt_bytes + ev_bytes);
   p.nfaults = (int)fd.size();
-  CUDA_TRY(cudaMemsetAsync(scratch, 0, cnt_bytes, st));
+  if (!sink) CUDA_TRY(cudaMemsetAsync(scratch, 0, cnt_bytes, st));
   if (!fd.empty())  // pageable source: the call returns once the source has been staged
     CUDA_TRY(cudaMemcpyAsync(scratch + cnt_bytes + ev_bytes, fd.data(), f_bytes, cudaMemcpyHostToDevice, st));
 
@@ -353,7 +366,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   if (rB) cudaFreeAsync(rB, st);
   if (lrc) { cudaFreeAsync(scratch, st); return lrc; }
 
-  if (err)
+  if (err && !sink)
     if (int e = finish_report(err, p.counters, p.events, ev_cap, ft ? (int64_t)p.ntiles * T : 0, st)) return e;
   CUDA_TRY(cudaFreeAsync(scratch, st));
   return 0;
@@ -457,48 +470,132 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   return 0;
 }
 
-// Host-buffer variant: stage op inputs into stream-ordered device buffers.
+// Host-buffer variant (the end-to-end API).  B goes to the device once; C is processed in row
+// panels (multiples of the 127-row unit, so the verification units are those of one call)
+// through a three-stream pipeline: the H2D copy of panel r+1's op(A) rows (and C0 rows) and
+// the D2H copy of panel r-1's result overlap the protected GEMM of panel r.  Faults are routed
+// to their panel with local rows; counters and events accumulate on the device (events carry
+// global rows) and the report is filled once at the end.
 int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
                     const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                     double *C, int64_t ldc, ftblas_err_report_t *err) {
+  std::vector<ftblas_fault_t> faults = take_armed();
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
-  if (rc) {
-    if (tl_have_armed) { tl_armed.clear(); tl_have_armed = false; }
-    return rc;
-  }
-  if (m == 0 || n == 0) {
-    if (tl_have_armed) { tl_armed.clear(); tl_have_armed = false; }
-    zero_report(err, k);
-    return 0;
-  }
+  if (rc) return rc;
+  zero_report(err, k);
+  if (m == 0 || n == 0) return 0;
   if (int e = ensure_device_init()) return e;
   cudaStream_t st = tl_stream;
   const bool reads_ab = alpha != 0.0 && k > 0;
-  const int64_t ar = is_n(ta) ? m : k, ac = is_n(ta) ? k : m;
-  const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
-  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
-  if (reads_ab) {
-    CUDA_TRY(cudaMallocAsync((void **)&dA, sizeof(double) * ar * ac, st));
-    CUDA_TRY(cudaMallocAsync((void **)&dB, sizeof(double) * br * bc, st));
-    CUDA_TRY(cudaMemcpy2DAsync(dA, sizeof(double) * ar, A, sizeof(double) * lda, sizeof(double) * ar, ac,
-                               cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpy2DAsync(dB, sizeof(double) * br, B, sizeof(double) * ldb, sizeof(double) * br, bc,
-                               cudaMemcpyHostToDevice, st));
+  if (!reads_ab) {  // C = beta*C: one device round trip, no ABFT
+    if (beta == 1.0) return 0;
+    double *dC = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)&dC, sizeof(double) * m * n, st));
+    if (beta != 0.0)
+      CUDA_TRY(cudaMemcpy2DAsync(dC, sizeof(double) * m, C, sizeof(double) * ldc, sizeof(double) * m, n,
+                                 cudaMemcpyHostToDevice, st));
+    int r = dgemm_core(false, {}, ta, tb, m, n, k, alpha, nullptr, std::max<int64_t>(1, is_n(ta) ? m : k), nullptr,
+                       std::max<int64_t>(1, is_n(tb) ? k : n), beta, dC, m, nullptr);
+    if (r == 0)
+      r = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
+                            cudaMemcpyDeviceToHost, st) == cudaSuccess ? 0 : 1;
+    cudaFreeAsync(dC, st);
+    const cudaError_t se = cudaStreamSynchronize(st);
+    return r ? r : (se == cudaSuccess ? 0 : cuda_fail(se));
   }
-  CUDA_TRY(cudaMallocAsync((void **)&dC, sizeof(double) * m * n, st));
-  if (beta != 0.0)
-    CUDA_TRY(cudaMemcpy2DAsync(dC, sizeof(double) * m, C, sizeof(double) * ldc, sizeof(double) * m, n,
-                               cudaMemcpyHostToDevice, st));
-  int r = dgemm_impl(ft, ta, tb, m, n, k, alpha, reads_ab ? dA : nullptr, reads_ab ? std::max<int64_t>(ar, 1) : lda,
-                     reads_ab ? dB : nullptr, reads_ab ? std::max<int64_t>(br, 1) : ldb, beta, dC, m, err);
-  if (r == 0 && !(reads_ab == false && beta == 1.0))
-    r = (cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
-                           cudaMemcpyDeviceToHost, st) == cudaSuccess) ? 0 : 1;
-  if (dA) cudaFreeAsync(dA, st);
-  if (dB) cudaFreeAsync(dB, st);
-  cudaFreeAsync(dC, st);
-  const cudaError_t se = cudaStreamSynchronize(st);
-  if (r == 0 && se != cudaSuccess) return cuda_fail(se);
+  for (const auto &f : faults)
+    if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step > k) return 3;
+  const int64_t Kc = (ft && tl_interval > 0 && tl_interval < k) ? tl_interval : k;
+  if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
+
+  // Panels: ~m/8 rows, a multiple of 2 x 127 (units intact, even leading dimensions); one
+  // panel when the problem is small.
+  const int64_t unit2 = 2 * ftk::TM;
+  int64_t P = m;
+  if (m >= 16 * unit2) P = ((m + 7) / 8 + unit2 - 1) / unit2 * unit2;
+  const int64_t npan = (m + P - 1) / P;
+  const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
+
+  cudaStream_t sh = nullptr, sd = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  cudaEvent_t ev_b, ev_in[2], ev_out[2], ev_free[2];
+  CUDA_TRY(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+  for (int q = 0; q < 2; ++q) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_in[q], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_out[q], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_free[q], cudaEventDisableTiming));
+  }
+  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
+  const size_t cnt_bytes = sizeof(unsigned long long) * ftk::CNT_N;
+  const size_t ev_bytes = sizeof(ftk::EventDev) * (size_t)std::max<int64_t>(ev_cap, 1);
+  const size_t pa = sizeof(double) * (size_t)P * (size_t)k, pc = sizeof(double) * (size_t)P * (size_t)n;
+  char *rep_base = nullptr;
+  double *dB = nullptr, *dA[2] = {nullptr, nullptr}, *dC[2] = {nullptr, nullptr};
+  int r = 0;
+  auto fail = [&](cudaError_t e) { if (r == 0 && e != cudaSuccess) r = cuda_fail(e); };
+  // Stream-ordered (pooled) staging on the compute stream; the copy streams wait for it.
+  fail(cudaMallocAsync((void **)&rep_base, 256 + ev_bytes, st));
+  fail(cudaMallocAsync((void **)&dB, sizeof(double) * br * bc, st));
+  for (int q = 0; q < 2 && q < npan; ++q) {
+    fail(cudaMallocAsync((void **)&dA[q], pa, st));
+    fail(cudaMallocAsync((void **)&dC[q], pc, st));
+  }
+  fail(cudaEventRecord(ev_b, st));
+  fail(cudaStreamWaitEvent(sh, ev_b, 0));
+  fail(cudaStreamWaitEvent(sd, ev_b, 0));
+  ReportSink sink{reinterpret_cast<unsigned long long *>(rep_base),
+                  reinterpret_cast<ftk::EventDev *>(rep_base + 256), ev_cap, 0, 0};
+  if (r == 0) {
+    fail(cudaMemsetAsync(rep_base, 0, cnt_bytes, st));
+    fail(cudaMemcpy2DAsync(dB, sizeof(double) * br, B, sizeof(double) * ldb, sizeof(double) * br, bc,
+                           cudaMemcpyHostToDevice, sh));
+    fail(cudaEventRecord(ev_b, sh));
+    fail(cudaStreamWaitEvent(st, ev_b, 0));
+  }
+  for (int64_t pi = 0; pi < npan && r == 0; ++pi) {
+    const int q = (int)(pi & 1);
+    const int64_t r0 = pi * P, pr = std::min<int64_t>(P, m - r0);
+    if (pi >= 2) fail(cudaStreamWaitEvent(sh, ev_free[q], 0));  // panel pi-2 left the device
+    if (is_n(ta))  // op(A) rows r0.. of an m x k matrix
+      fail(cudaMemcpy2DAsync(dA[q], sizeof(double) * pr, A + r0, sizeof(double) * lda, sizeof(double) * pr, k,
+                             cudaMemcpyHostToDevice, sh));
+    else  // columns r0.. of the k x m stored matrix
+      fail(cudaMemcpy2DAsync(dA[q], sizeof(double) * k, A + r0 * lda, sizeof(double) * lda, sizeof(double) * k, pr,
+                             cudaMemcpyHostToDevice, sh));
+    if (beta != 0.0)
+      fail(cudaMemcpy2DAsync(dC[q], sizeof(double) * pr, C + r0, sizeof(double) * ldc, sizeof(double) * pr, n,
+                             cudaMemcpyHostToDevice, sh));
+    fail(cudaEventRecord(ev_in[q], sh));
+    fail(cudaStreamWaitEvent(st, ev_in[q], 0));
+    if (r) break;
+    std::vector<ftblas_fault_t> pf;
+    for (const auto &f : faults)
+      if (f.i >= r0 && f.i < r0 + pr) pf.push_back(ftblas_fault_t{f.i - r0, f.j, f.step, f.delta});
+    sink.row_off = r0;
+    r = dgemm_core(ft, pf, ta, tb, pr, n, k, alpha, dA[q], is_n(ta) ? pr : k, dB, br, beta, dC[q], pr, nullptr,
+                   ft ? &sink : nullptr);
+    if (r) break;
+    fail(cudaEventRecord(ev_out[q], st));
+    fail(cudaStreamWaitEvent(sd, ev_out[q], 0));
+    fail(cudaMemcpy2DAsync(C + r0, sizeof(double) * ldc, dC[q], sizeof(double) * pr, sizeof(double) * pr, n,
+                           cudaMemcpyDeviceToHost, sd));
+    fail(cudaEventRecord(ev_free[q], sd));
+  }
+  fail(cudaStreamSynchronize(sd));
+  fail(cudaStreamSynchronize(sh));
+  fail(cudaStreamSynchronize(st));
+  if (r == 0 && err && ft) r = finish_report(err, sink.counters, sink.events, ev_cap, sink.units, st);
+  cudaFreeAsync(rep_base, st);
+  cudaFreeAsync(dB, st);
+  for (int q = 0; q < 2; ++q) {
+    if (dA[q]) cudaFreeAsync(dA[q], st);
+    if (dC[q]) cudaFreeAsync(dC[q], st);
+  }
+  cudaEventDestroy(ev_b);
+  for (int q = 0; q < 2; ++q) { cudaEventDestroy(ev_in[q]); cudaEventDestroy(ev_out[q]); cudaEventDestroy(ev_free[q]); }
+  cudaStreamDestroy(sh);
+  cudaStreamDestroy(sd);
   return r;
 }
 
