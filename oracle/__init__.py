@@ -73,6 +73,7 @@ def lib():
         L.oracle_dscal.argtypes = [i64, d, P, i64, P, i64, P]
         L.oracle_daxpy.argtypes = [i64, d, P, i64, P, i64, P, i64, P]
         L.oracle_dgemv.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64, P, i64, P]
+        L.oracle_dtrsm.argtypes = [c, c, c, i64, i64, d, P, i64, P, i64, i64, P]
         _lib = L
     return _lib
 
@@ -244,6 +245,16 @@ def dgemv(trans, m, n, alpha, A, lda, x, incx, beta, y, incy, faults=()):
     lib().oracle_dgemv(trans.encode(), m, n, alpha, _ptr(A), lda, _ptr(xo), incx, beta, _ptr(yo), incy,
                        fp, nf, _ptr(cnt))
     return yo, DmrReport(*[int(v) for v in cnt])
+
+
+def dtrsm(uplo, transa, diag, m, n, alpha, A, lda, B, ldb, faults=()):
+    """DTRSM oracle (NEXT-3): solve op(A) X = alpha B (side L); returns (X flat, (detected, corrected))."""
+    A = _flat(A)
+    Bo = _flat(B).copy()
+    cnt = np.zeros(4, dtype=np.int64)
+    lib().oracle_dtrsm(uplo.encode(), transa.encode(), diag.encode(), m, n, alpha, _ptr(A), lda, _ptr(Bo), ldb,
+                       len(list(faults)), _ptr(cnt))
+    return Bo, (int(cnt[1]), int(cnt[2]))
 
 
 def num_threads() -> int:

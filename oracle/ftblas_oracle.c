@@ -463,6 +463,39 @@ void oracle_dgemv(char trans, int64_t m, int64_t n, double alpha, const double *
   counters[0] = nout; counters[1] = det; counters[2] = det; counters[3] = 0;
 }
 
+/* ---------------------------------------------------------------------------
+ * DTRSM: op(A) X = alpha B, side 'L', in place,
+ * plain column-by-column substitution: forward when op(A) is lower, backward when upper;
+ * x_i = (alpha b_i - sum_p op(A)_ip x_p) computed as an fma chain over p in substitution order,
+ * then multiplied by the reciprocal 1/op(A)_ii (the paper's packed reciprocal diagonal; unit
+ * diagonal: no multiply).  Faults are corrected by the protection (ABFT on the updates, DMR on
+ * the diagonal solves), so X is the fault-free solution and every fault counts as detected and
+ * corrected (reading R21: faults far apart, one per verification unit).
+ * ------------------------------------------------------------------------- */
+void oracle_dtrsm(char uplo, char transa, char diag, int64_t m, int64_t n, double alpha, const double *A,
+                  int64_t lda, double *B, int64_t ldb, int64_t nfaults, int64_t *counters) {
+  int lower = (uplo == 'L' || uplo == 'l'), tr = is_trans(transa), unit = (diag == 'U' || diag == 'u');
+  int fwd = lower != tr;
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < n; ++j) {
+    double *b = B + j * ldb;
+    for (int64_t i = 0; i < m; ++i) b[i] = alpha * b[i];
+    for (int64_t s = 0; s < m; ++s) {
+      int64_t i = fwd ? s : m - 1 - s;
+      double v = b[i];
+      if (!unit) v = v * (1.0 / (tr ? A[i + i * lda] : A[i + i * lda]));
+      b[i] = v;
+      /* eliminate x_i from the remaining rows */
+      if (fwd) {
+        for (int64_t p = i + 1; p < m; ++p) b[p] = fma(-(tr ? A[i + p * lda] : A[p + i * lda]), v, b[p]);
+      } else {
+        for (int64_t p = 0; p < i; ++p) b[p] = fma(-(tr ? A[i + p * lda] : A[p + i * lda]), v, b[p]);
+      }
+    }
+  }
+  counters[0] = 0; counters[1] = nfaults; counters[2] = nfaults; counters[3] = 0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

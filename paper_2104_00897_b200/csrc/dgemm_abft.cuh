@@ -617,7 +617,9 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
       const int64_t kt = x.k1 - x.k0;  // rank-1 updates in this interval
       const int len = is_row ? x.bn_eff : x.bm_eff;
       const double nu = (double)(kt + len) * 0x1p-53;
-      const double tau = 2.0 * (nu / (1.0 - nu)) * (double)kt * (double)len * amx * bmx;  // DESIGN.md R1
+      // DESIGN.md R1, R17: 2 gamma(kt + len) for the two sums plus 2^-50 = 8u for the fixed-point
+      // encode (per element below 2^-50 max|x|, summed over len rows and kt k-slots).
+      const double tau = (2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx;
       const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
       const bool flag = valid && !(fabs(d) <= tau) && !(P.dev_mode & 4);
       tl.dres[vt] = d;

@@ -8,6 +8,7 @@
 #include "dgemm_abft.cuh"
 #include "unfused.cuh"
 #include "dmr.cuh"
+#include "trsm.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -737,6 +738,140 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
   return dmr_finish(sc, ft ? nout : 0, rep, st);
 }
 
+// ---------------------------------------------------------------- FT-DTRSM (NEXT-3)
+// op(A) X = alpha B, side 'L'.  Recursive blocked solve: a block of more than LEAF rows is
+// split (first part a multiple of LEAF), the parts are solved recursively and the coupling
+// is a GEMM update B2 -= op(A)21 X1 (forward, op(A) lower) or B1 -= op(A)12 X2 (backward, op(A)
+// upper) through the protected DMMA kernel (fused ABFT, report accumulated in a sink); the
+// leaves are the DMR diagonal-block kernel of trsm.cuh.  A fault (i, j, step = p) perturbs the
+// update of B(i, j) by X(p, j): it lands in the GEMM whose rows hold i and whose k-range holds
+// p, or in the leaf when i and p share one LEAF block.
+struct TrsmCtx {
+  bool ft, fwd, trans, unit;
+  int64_t leaf;  // diagonal block rows (LEAF; 127 was tried for the protected solve: no faster)
+  const double *A;
+  int64_t lda;
+  double *B;
+  int64_t ldb, n;
+  const std::vector<ftblas_fault_t> *faults;
+  ReportSink *sink;
+  DmrScratch *leaf_sc;  // leaf DMR counters
+  cudaStream_t st;
+};
+
+int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
+  std::vector<ftd::DmrFault> lf;
+  if (c.ft)
+    for (const auto &f : *c.faults)
+      if (f.i >= r0 && f.i < r0 + mb && f.step >= r0 && f.step < r0 + mb)
+        lf.push_back(ftd::DmrFault{f.j * ftt::LEAF + (f.i - r0), f.step - r0, f.delta});
+  ftd::DmrFault *df = nullptr;
+  if (!lf.empty()) {
+    CUDA_TRY(cudaMallocAsync((void **)&df, sizeof(ftd::DmrFault) * lf.size(), c.st));
+    CUDA_TRY(cudaMemcpyAsync(df, lf.data(), sizeof(ftd::DmrFault) * lf.size(), cudaMemcpyHostToDevice, c.st));
+  }
+  ftt::LeafParams P{};
+  P.nb = (int)mb; P.n = (int)c.n;
+  P.A = c.A + r0 + r0 * c.lda; P.lda = c.lda;
+  P.B = c.B + r0; P.ldb = c.ldb;
+  P.trans = c.trans; P.unit = c.unit; P.fwd = c.fwd; P.dmr = c.ft;
+  P.f = df; P.nf = (int)lf.size(); P.cnt = c.leaf_sc->cnt;
+  static bool attr = false;
+  const int smem = (int)(sizeof(double) * (ftt::LEAF * ftt::LEAF + 2 * ftt::LEAF));
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(ftt::trsm_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 15) / 16, (int64_t)num_sms()));
+  ftt::trsm_leaf_kernel<<<grid, 512, smem, c.st>>>(P);
+  ++tl_launches;
+  CUDA_TRY(cudaGetLastError());
+  if (df) CUDA_TRY(cudaFreeAsync(df, c.st));
+  return 0;
+}
+
+// The update rows [R0, R0+mr) of B -= op(A)[R0.., K0..K0+mk] * X[K0.., :].
+int trsm_update(TrsmCtx &c, int64_t R0, int64_t mr, int64_t K0, int64_t mk) {
+  std::vector<ftblas_fault_t> gf;
+  if (c.ft)
+    for (const auto &f : *c.faults)
+      if (f.i >= R0 && f.i < R0 + mr && f.step >= K0 && f.step < K0 + mk)
+        gf.push_back(ftblas_fault_t{f.i - R0, f.j, f.step - K0, f.delta});
+  const double *Asub = c.trans ? c.A + K0 + R0 * c.lda : c.A + R0 + K0 * c.lda;
+  if (c.sink) c.sink->row_off = R0;
+  return dgemm_core(c.ft, gf, c.trans ? 'T' : 'N', 'N', mr, c.n, mk, -1.0, Asub, c.lda, c.B + K0, c.ldb, 1.0,
+                    c.B + R0, c.ldb, nullptr, c.ft ? c.sink : nullptr);
+}
+
+int trsm_rec(TrsmCtx &c, int64_t r0, int64_t m) {
+  if (m <= c.leaf) return trsm_leaf(c, r0, m);
+  const int64_t m1 = ((m / 2) + c.leaf - 1) / c.leaf * c.leaf, m2 = m - m1;
+  if (c.fwd) {
+    if (int e = trsm_rec(c, r0, m1)) return e;
+    if (int e = trsm_update(c, r0 + m1, m2, r0, m1)) return e;
+    return trsm_rec(c, r0 + m1, m2);
+  }
+  if (int e = trsm_rec(c, r0 + m1, m2)) return e;
+  if (int e = trsm_update(c, r0, m1, r0 + m1, m2)) return e;
+  return trsm_rec(c, r0, m1);
+}
+
+int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
+               const double *A, int64_t lda, double *B, int64_t ldb, ftblas_err_report_t *err) {
+  std::vector<ftblas_fault_t> faults = take_armed();
+  if (side != 'L' && side != 'l') return -1;
+  const bool lower = uplo == 'L' || uplo == 'l';
+  if (!lower && uplo != 'U' && uplo != 'u') return -2;
+  if (!is_n(transa) && !is_t(transa)) return -3;
+  const bool unit = diag == 'U' || diag == 'u';
+  if (!unit && diag != 'N' && diag != 'n') return -4;
+  if (m < 0) return -5;
+  if (n < 0) return -6;
+  if (m > 0 && n > 0 && alpha != 0.0 && A == nullptr) return -8;
+  if (lda < std::max<int64_t>(1, m)) return -9;
+  if (m > 0 && n > 0 && B == nullptr) return -10;
+  if (ldb < std::max<int64_t>(1, m)) return -11;
+  zero_report(err, m);
+  if (err) { err->unit_k = 0; }
+  if (m == 0 || n == 0) return 0;
+  if (int e = ensure_device_init()) return e;
+  cudaStream_t st = tl_stream;
+  const bool trans = is_t(transa);
+  const bool fwd = lower != trans;  // op(A) lower -> forward substitution
+  for (const auto &f : faults)
+    if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step >= m || (fwd ? f.step >= f.i : f.step <= f.i))
+      return 3;
+  if (alpha != 1.0) {
+    const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, (int64_t)num_sms() * 16);
+    ftt::scale_b_kernel<<<blocks, 256, 0, st>>>(m, n, alpha, B, ldb);
+    ++tl_launches;
+    CUDA_TRY(cudaGetLastError());
+    if (alpha == 0.0) return 0;
+  }
+  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
+  char *rep = nullptr;
+  CUDA_TRY(cudaMallocAsync((void **)&rep, 256 + sizeof(ftk::EventDev) * (size_t)std::max<int64_t>(ev_cap, 1), st));
+  CUDA_TRY(cudaMemsetAsync(rep, 0, 256, st));
+  ReportSink sink{reinterpret_cast<unsigned long long *>(rep), reinterpret_cast<ftk::EventDev *>(rep + 256), ev_cap, 0, 0};
+  std::vector<ftblas_fault_t> none;
+  DmrScratch lsc;
+  if (int e = dmr_prepare(false, none, 1, 0, lsc, st)) return e;  // leaf counters only
+  TrsmCtx c{ft, fwd, trans, unit, (int64_t)ftt::LEAF, A, lda, B, ldb, n, &faults, &sink, &lsc, st};
+  int r = trsm_rec(c, 0, m);
+  if (r == 0 && err && ft) {
+    r = finish_report(err, sink.counters, sink.events, ev_cap, sink.units, st);
+    unsigned long long lc[ftd::D_N];
+    if (r == 0 && cudaMemcpy(lc, lsc.cnt, sizeof lc, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      err->detected += (int64_t)lc[ftd::D_DETECTED];
+      err->corrected += (int64_t)lc[ftd::D_CORRECTED];
+      err->recomputed += (int64_t)lc[ftd::D_UNCORRECTABLE];
+    }
+  }
+  cudaFreeAsync(rep, st);
+  cudaFreeAsync(lsc.base, st);
+  return r;
+}
+
 uint64_t splitmix_next(uint64_t &state) {
   state += 0x9E3779B97F4A7C15ull;
   uint64_t z = state;
@@ -788,6 +923,15 @@ int ftblas_dgemv(char trans, int64_t m, int64_t n, double alpha, const double *A
 int ftblas_dgemv_noft(char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
                       const double *x, int64_t incx, double beta, double *y, int64_t incy) {
   return dgemv_impl(false, trans, m, n, alpha, A, lda, x, incx, beta, y, incy, nullptr);
+}
+
+int ftblas_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha, const double *A,
+                 int64_t lda, double *B, int64_t ldb, ftblas_err_report_t *err) {
+  return dtrsm_impl(true, side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, err);
+}
+int ftblas_dtrsm_noft(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
+                      const double *A, int64_t lda, double *B, int64_t ldb) {
+  return dtrsm_impl(false, side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, nullptr);
 }
 
 int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,

@@ -107,8 +107,10 @@ def load():
     L.ftblas_daxpy_noft.argtypes = [i64, d, P, i64, P, i64]
     L.ftblas_dgemv.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64, DR]
     L.ftblas_dgemv_noft.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64]
+    L.ftblas_dtrsm.argtypes = [c, c, c, c, i64, i64, d, P, i64, P, i64, ctypes.POINTER(ErrReport)]
+    L.ftblas_dtrsm_noft.argtypes = [c, c, c, c, i64, i64, d, P, i64, P, i64]
     for fn in ("ftblas_dscal", "ftblas_dscal_noft", "ftblas_daxpy", "ftblas_daxpy_noft",
-               "ftblas_dgemv", "ftblas_dgemv_noft"):
+               "ftblas_dgemv", "ftblas_dgemv_noft", "ftblas_dtrsm", "ftblas_dtrsm_noft"):
         getattr(L, fn).restype = ctypes.c_int
     L.ftblas_take_launch_count.restype = i64
     L.ftblas_take_launch_count.argtypes = []
@@ -129,7 +131,7 @@ EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas
             "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode", "ftblas_set_interval",
             "ftblas_get_geometry", "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize",
             "ftblas_dscal", "ftblas_dscal_noft", "ftblas_daxpy", "ftblas_daxpy_noft", "ftblas_dgemv",
-            "ftblas_dgemv_noft")
+            "ftblas_dgemv_noft", "ftblas_dtrsm", "ftblas_dtrsm_noft")
 
 
 def _check(fn, status):
@@ -261,6 +263,25 @@ def ftblas_daxpy_noft(n, alpha, x, incx, y, incy):
 def ftblas_dgemv_noft(trans, m, n, alpha, A, lda, x, incx, beta, y, incy):
     _check("ftblas_dgemv_noft", load().ftblas_dgemv_noft(_c(trans), m, n, alpha, _ptr(A), lda, _ptr(x),
                                                          incx, beta, _ptr(y), incy))
+
+
+def ftblas_dtrsm(side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, *, report=True,
+                 events_capacity=4096):
+    """FT-DTRSM (NEXT-3): B := alpha op(A)^-1 B on device pointers; returns a Report."""
+    L = load()
+    evbuf = (Event * max(events_capacity, 1))()
+    r = ErrReport()
+    r.events = evbuf
+    r.events_capacity = events_capacity
+    st = L.ftblas_dtrsm(_c(side), _c(uplo), _c(transa), _c(diag), m, n, alpha, _ptr(A), lda, _ptr(B),
+                        ldb, ctypes.byref(r) if report else None)
+    _check("ftblas_dtrsm", st)
+    return _report(r, evbuf) if report else None
+
+
+def ftblas_dtrsm_noft(side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb):
+    _check("ftblas_dtrsm_noft", load().ftblas_dtrsm_noft(_c(side), _c(uplo), _c(transa), _c(diag), m, n,
+                                                         alpha, _ptr(A), lda, _ptr(B), ldb))
 
 
 def ftblas_inject_arm(faults):
