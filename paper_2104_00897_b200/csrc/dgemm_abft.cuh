@@ -79,6 +79,10 @@ struct Params {
   // workspace slice C + t*wstride (alpha = 1, beta = 0; a reduction kernel finishes C).
   int64_t Kc, wstride;
   int T, ntiles, t_base;
+  // Launched as 2-CTA clusters (fused encode): consecutive CTAs 2c, 2c+1 hold tiles of one
+  // tile column, so they stage the same B_J: each encodes half of its 16 k-slots and the pair
+  // swaps halves through distributed shared memory.  `total` = real CTAs of this launch.
+  int cluster2, total;
   const FaultDev *faults;
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
@@ -163,6 +167,41 @@ template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N)); }
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N)); }
+
+// Thread-block cluster helpers (pairs of CTAs sharing an operand's checksum encode).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 // ------------------------------------------------------------------ shared-memory layouts
 // Operand tile X(x, p): x the M (or N) index in [0,128), p the k index in [0,16).  Both are
@@ -404,6 +443,121 @@ __device__ __forceinline__ double fx_to_double(long long z, int sc) {
   return __longlong_as_double((long long)(sg | bits));
 }
 
+// ---------------- half-slice encode (thread-block clusters share an operand tile; each CTA
+// of a pair encodes the 8 k-slots hsel*8 .. hsel*8+7 of the 16 and swaps them with its partner)
+// Lane maps (conflict-free LDS.128, offsets compile-time per load j = 0..15):
+//  K-major: lane = 4q + cc: k-slot pair c = 4 hsel + cc, row x = 8j + q (the 8 rows of one load
+//           have distinct x & 7, so the 4-chunk halves of the swizzled rows tile the banks);
+//           reduce over q (xor 4, 8, 16).
+//  MN-major: lane = 8g + pp: k-slot p = 8 hsel + pp, rows x = 32g + 2j, 2j+1; reduce over g
+//           (xor 8, 16).
+template <bool KM>
+__device__ __forceinline__ double2 enc_ld_h(const double *s, int lane, int hsel, int j, int cr) {
+  int off;
+  if (KM) {
+    const int q = lane >> 2, c = 4 * hsel + (lane & 3);
+    off = (8 * j + q) * 16 + ((c ^ q) << 1);
+  } else {
+    const int g = lane >> 3, p = 8 * hsel + (lane & 7);
+    off = (2 * g + (j >> 3)) * 256 + p * 16 + (((j & 7) ^ (p & 7)) << 1);
+  }
+  double2 v = *reinterpret_cast<const double2 *>(s + off);
+  if (KM) {
+    const int q = lane >> 2;
+    if ((cr == 0 && j == 0 && q == 0) || (cr == DM && j == 15 && q == 7)) v.x = v.y = 0.0;
+  } else {
+    const int g = lane >> 3;
+    if (cr == 0 && j == 0 && g == 0) v.x = 0.0;
+    if (cr == DM && j == 15 && g == 3) v.y = 0.0;
+  }
+  return v;
+}
+
+template <bool KM>
+__device__ __forceinline__ float enc_pass1_h(const double *s, int lane, int hsel, int cr) {
+  float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const double2 v = enc_ld_h<KM>(s, lane, hsel, j, cr), w = enc_ld_h<KM>(s, lane, hsel, j + 1, cr);
+    m0 = fmax3_abs_nan(m0, hi_f(v.x), hi_f(v.y));
+    m1 = fmax3_abs_nan(m1, hi_f(w.x), hi_f(w.y));
+  }
+  return fmax_nan(m0, m1);
+}
+
+template <bool KM, bool EXACT>
+__device__ __forceinline__ void enc_pass2_h(const double *s, int lane, int hsel, int cr, uint32_t C, long long &q0,
+                                            long long &q1) {
+  long long a0 = 0, a1 = 0;
+  int n0 = 0, n1 = 0;
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+  for (int jj = 0; jj < 8; jj += 2) {
+    const int j = 8 * hh + jj;
+    const double2 v = enc_ld_h<KM>(s, lane, hsel, j, cr), w = enc_ld_h<KM>(s, lane, hsel, j + 1, cr);
+    int sv0, sv1, sw0, sw1;
+    const long long tv0 = fx_term<EXACT>(v.x, C, sv0), tv1 = fx_term<EXACT>(v.y, C, sv1);
+    const long long tw0 = fx_term<EXACT>(w.x, C, sw0), tw1 = fx_term<EXACT>(w.y, C, sw1);
+    if (KM) {
+      a0 += tv0 + tw0;
+      a1 += tv1 + tw1;
+      n0 += sv0 + sw0;
+      n1 += sv1 + sw1;
+    } else {
+      a0 += (tv0 + tv1) + (tw0 + tw1);
+      n0 += (sv0 + sv1) + (sw0 + sw1);
+    }
+  }
+  a0 -= n0;
+  a1 -= n1;
+#pragma unroll
+  for (int o = KM ? 4 : 8; o <= 16; o <<= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    if (KM) a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+  }
+  q0 = a0;
+  q1 = a1;
+}
+
+// Exact max |high word| of a half slice (rare path).
+template <bool KM>
+__device__ __noinline__ uint32_t enc_exact_hmax_h(const double *s, int lane, int hsel, int cr) {
+  uint32_t hm = 0;
+  for (int j = 0; j < 16; ++j) {
+    const double2 v = enc_ld_h<KM>(s, lane, hsel, j, cr);
+    hm = max(hm, max((uint32_t)__double2hiint(v.x) & 0x7FFFFFFFu, (uint32_t)__double2hiint(v.y) & 0x7FFFFFFFu));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  return hm;
+}
+template <bool KM>
+__device__ __noinline__ void enc_pass2_h_exact(const double *s, int lane, int hsel, int cr, uint32_t C, long long &q0,
+                                               long long &q1) {
+  enc_pass2_h<KM, true>(s, lane, hsel, cr, C, q0, q1);
+}
+
+// Encode the half slice hsel: sum0 (sum1) = e^T X for this lane's k-slot(s) (valid in the
+// lanes q == 0 / g == 0); hm_half returns the half's R1' high-word maximum.
+template <bool KM>
+__device__ __forceinline__ void enc_operand_h(const double *s, int lane, int hsel, int cr, double &sum0, double &sum1,
+                                              uint32_t &hm_half) {
+  uint32_t hm = (uint32_t)__float_as_int(warp_max_nan(enc_pass1_h<KM>(s, lane, hsel, cr)));
+  if (hm >= 0x7F800000u) hm = enc_exact_hmax_h<KM>(s, lane, hsel, cr);
+  hm_half = min(hm, 0x7FEFFFFFu);
+  const uint32_t c = hm >> 20;
+  if (c >= 2047u) {
+    sum0 = sum1 = __longlong_as_double(0x7FF8000000000000ll);
+    return;
+  }
+  long long q0, q1;
+  if (c > 50u) enc_pass2_h<KM, false>(s, lane, hsel, cr, c + 2u, q0, q1);
+  else enc_pass2_h_exact<KM>(s, lane, hsel, cr, c + 2u, q0, q1);
+  sum0 = fx_to_double(q0, (int)c - 1073);
+  sum1 = KM ? fx_to_double(q1, (int)c - 1073) : 0.0;
+}
+
 // Encode one operand slice.  sum0 (and sum1 for K-major) receive e^T X for this lane's
 // column(s); hmax_acc accumulates the R1' high-word maximum of the data elements.
 template <bool KM>
@@ -439,6 +593,13 @@ __device__ __forceinline__ TileGeom load_geom(const TileGeom &g) {
 
 struct SmemTail {
   TileGeom geo;
+  // Cluster-pair B encode: the partner's 8 k-slot sums of B_J e per stage and its half maximum;
+  // mfull[s] is arrived by the partner once mail[s] is written, mfree[s] by the partner once it
+  // has consumed what this CTA wrote into its mailbox.
+  double mail[STAGES][8];
+  uint32_t mail_hm[STAGES];
+  uint64_t mfull[STAGES], mfree[STAGES];
+  int share;  // this CTA encodes half of B and swaps it with its cluster partner
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
   double dres[256];                // residuals: 0..127 columns, 128..255 rows
   double red[NTHREADS / 32];
@@ -525,8 +686,10 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
     }
   };
+  const uint32_t rank = P.cluster2 ? cluster_rank() : 0u;
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
+    const bool share = verify && tl.share;
     if (lane == 0)
       for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
     uint32_t amax_hi = 0u, bmax_hi = 0u;
@@ -546,11 +709,48 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         } else if (P.dev_mode & 1) {  // development: pass 1 only
           amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
           bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
+        } else if (share) {
+          // Cluster pair: all of e^T A_I, the half `rank` of B_J e; swap B halves with the partner.
+          enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);
+          uint32_t hmb;
+          enc_operand_h<BKM>(sB, lane, (int)rank, x.crb, b0, b1, hmb);
+          if (AKM) {
+            if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
+          } else {
+            if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
+          }
+          // own half into the staged tile and into the partner's mailbox (lanes 0..3 hold two
+          // k-slots each for a K-major B, lanes 0..7 one each for an MN-major B)
+          if (gs >= STAGES && lane == 0) mbar_wait_acq_cluster(&tl.mfree[slot], ((gs / STAGES) - 1) & 1);
+          __syncwarp();
+          const uint32_t pmail = mapa_u32(smem_u32(&tl.mail[slot][0]), rank ^ 1u);
+          if (BKM) {
+            if (lane < 4) {
+              *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 8 * (int)rank + 2 * lane)) = make_double2(b0, b1);
+              st_cluster_f64(pmail + 8u * (2 * lane), b0);
+              st_cluster_f64(pmail + 8u * (2 * lane + 1), b1);
+            }
+          } else {
+            if (lane < 8) {
+              sB[sidx<false>(x.crb, 8 * (int)rank + lane)] = b0;
+              st_cluster_f64(pmail + 8u * lane, b0);
+            }
+          }
+          if (lane == 0) st_cluster_u32(mapa_u32(smem_u32(&tl.mail_hm[slot]), rank ^ 1u), hmb);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tl.mfull[slot]), rank ^ 1u));
+          // the partner's half
+          if (lane == 0) mbar_wait_acq_cluster(&tl.mfull[slot], (gs / STAGES) & 1);
+          __syncwarp();
+          if (lane < 8) sB[sidx<BKM>(x.crb, 8 * (int)(rank ^ 1u) + lane)] = tl.mail[slot][lane];
+          bmax_hi = max(bmax_hi, max(hmb, tl.mail_hm[slot]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tl.mfree[slot]), rank ^ 1u));
         } else if (!(P.dev_mode & 2)) {
           enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           enc_operand<BKM>(sB, lane, x.crb, b0, b1, bmax_hi);  // B_J e over the 127 data columns
         }
-        if (!P.Ac) {
+        if (!P.Ac && !share) {
           if (AKM) {
             if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
           } else {
@@ -805,14 +1005,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // Grouped raster: CTAs run in bands of RASTER_G tile rows, column by column inside a band,
   // so that one wave of 148 CTAs touches ~12 A row panels and ~12 B column panels (L2 reuse)
   // instead of 148 A panels and one B panel.
-  int ti, tj;
-  {
-    const int L = blockIdx.x % P.ntiles, band_tiles = RASTER_G * P.tiles_n, band = L / band_tiles;
+  auto map_tile = [&](int Lg, int &ti_, int &tj_, int &t_) {
+    const int L = Lg % P.ntiles, band_tiles = RASTER_G * P.tiles_n, band = L / band_tiles;
     const int within = L - band * band_tiles, rows = min(RASTER_G, P.tiles_m - band * RASTER_G);
-    ti = band * RASTER_G + within % rows;
-    tj = within / rows;
+    ti_ = band * RASTER_G + within % rows;
+    tj_ = within / rows;
+    t_ = P.t_base + Lg / P.ntiles;
+  };
+  const int Lg = (int)blockIdx.x;
+  const bool ghost = P.cluster2 && Lg >= P.total;  // pads an odd grid to whole clusters
+  int ti, tj, tt;
+  map_tile(ghost ? Lg - 1 : Lg, ti, tj, tt);
+  // Cluster pair (2c, 2c+1): share the B_J encode when both are real tiles of the same tile
+  // column and interval (a band with an odd row count pairs across columns: no sharing).
+  bool share = false;
+  if (FT && P.cluster2 && !P.Ac && !ghost && (Lg ^ 1) < P.total) {
+    int pti, ptj, ptt;
+    map_tile(Lg ^ 1, pti, ptj, ptt);
+    share = ptj == tj && ptt == tt;
   }
-  x.t = P.t_base + (int)(blockIdx.x / P.ntiles);  // verification interval
+  x.t = tt;  // verification interval
   x.tile = ti + tj * P.tiles_m + x.t * P.ntiles;  // fault bucket key: (tile, interval)
   x.k0 = (int64_t)x.t * P.Kc;
   x.k1 = min64(x.k0 + P.Kc, P.k);
@@ -847,6 +1059,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tl.first_row = 0x7fffffff;
     tl.first_col = 0x7fffffff;
     tl.retry = 0;
+    tl.share = share ? 1 : 0;
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&tl.mfull[s], 1);
+      mbar_init(&tl.mfree[s], 1);
+    }
     fence_mbar_init();
   }
   // Faults of this tile: [f_lo, f_hi) in the (tile, stage)-sorted list.
@@ -860,6 +1078,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     x.f_hi = lo;
   }
   __syncthreads();
+  if (P.cluster2) cluster_sync_all();  // partners' mailbox barriers are initialised
+  if (ghost) return;
 
   // The two roles never re-converge, so ptxas can give each its own register budget.
   if (is_cs_warp(x.warp)) {
@@ -869,6 +1089,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     setmaxnreg_inc<REG_MMA>();
     mma_role<AKM, BKM, FT>(P, x);
   }
+  // A sharing pair stays resident until the partner has made its last remote access.
+  if (share) cluster_sync_all();
 }
 
 // Intervals (NEXT-1): C = alpha * sum_{t < G} W_t + (first ? beta * C0 : C), the increments

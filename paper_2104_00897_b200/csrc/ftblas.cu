@@ -49,7 +49,7 @@ bool is_n(char c) { return c == 'N' || c == 'n'; }
 bool is_t(char c) { return c == 'T' || c == 't' || c == 'C' || c == 'c'; }
 
 template <bool AKM, bool BKM, bool FT>
-int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &p, dim3 grid, cudaStream_t st) {
+int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &p0, dim3 grid, cudaStream_t st) {
   auto kfn = ftk::dgemm_abft_kernel<AKM, BKM, FT>;
   static bool attr_set[64] = {false};  // per instantiation and device
   int dev = 0;
@@ -58,6 +58,28 @@ int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ftk::SMEM_BYTES));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
+  ftk::Params p = p0;
+  p.total = (int)grid.x;
+  // Fused encode: 2-CTA clusters share the B_J encode (cluster size 2 packs all 148 SMs).
+  if (FT && !p.Ac && !(p.dev_mode & 128)) {
+    p.cluster2 = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((grid.x + 1) & ~1u);
+    cfg.blockDim = dim3(ftk::NTHREADS);
+    cfg.dynamicSmemBytes = ftk::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kfn, ta, tb, p));
+    ++tl_launches;
+    return 0;
+  }
+  p.cluster2 = 0;
   kfn<<<grid, ftk::NTHREADS, ftk::SMEM_BYTES, st>>>(ta, tb, p);
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());

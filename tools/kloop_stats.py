@@ -3,7 +3,8 @@ non-DMMA instructions, local-memory spills).  usage: python tools/kloop_stats.py
 import glob, os, re, subprocess, sys, tempfile
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(sys.argv[1])], cwd=d, capture_output=True)
-txt = subprocess.run(["nvdisasm", "-c", glob.glob(os.path.join(d, "*.cubin"))[0]], capture_output=True, text=True).stdout
+txt = "".join(subprocess.run(["nvdisasm", "-c", c], capture_output=True, text=True).stdout
+              for c in sorted(glob.glob(os.path.join(d, "*.cubin"))))
 funcs, cur = {}, None
 for l in txt.splitlines():
     m = re.search(r'\.text\.(\S+):', l)

@@ -5,8 +5,8 @@ from collections import Counter
 lib = sys.argv[1]
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
-cub = glob.glob(os.path.join(d, "*.cubin"))[0]
-txt = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+txt = "".join(subprocess.run(["nvdisasm", "-g", "-c", c], capture_output=True, text=True).stdout
+              for c in sorted(glob.glob(os.path.join(d, "*.cubin"))))
 cur = curline = None
 per = {}
 for l in txt.splitlines():
