@@ -117,7 +117,13 @@ int ftblas_dgemm_unfused(char transA, char transB, int64_t m, int64_t n, int64_t
 
 /* Same as ftblas_dgemm / ftblas_dgemm_noft but A, B, C are HOST pointers (pinned memory
  * recommended).  Copies op inputs host->device, computes, copies C device->host and
- * synchronises the stream before returning.  Device staging is library-owned. */
+ * synchronises the stream before returning.  Device staging is library-owned: all of op(B)
+ * plus two row panels of op(A) and C.  Large problems (m >= 16 * 254) run as ~8 row panels
+ * (multiples of 254 rows) with copies overlapped with compute on two library streams; the
+ * first and last panels run in column chunks (multiples of 254 columns) so compute starts
+ * once the first chunk of op(B) has arrived and the last result returns chunk by chunk.
+ * Chunk and panel edges are multiples of the verification unit, so the report (units,
+ * events with global (i, j)) equals that of one ftblas_dgemm call on the whole problem. */
 int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
                       const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                       double *C, int64_t ldc, ftblas_err_report_t *err);

@@ -96,6 +96,7 @@ struct Params {
                                   // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
+  int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
   EventDev *events;
   long long ev_cap;
 };
@@ -858,9 +859,9 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
         atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
         const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
         if ((long long)slot < P.ev_cap)
-          P.events[slot] = multi ? EventDev{(long long)(x.i0 + P.ev_row_off), (long long)x.j0, 2, x.t, nfr ? tl.dres[128 + fr] : 0.0,
+          P.events[slot] = multi ? EventDev{(long long)(x.i0 + P.ev_row_off), (long long)(x.j0 + P.ev_col_off), 2, x.t, nfr ? tl.dres[128 + fr] : 0.0,
                                             nfc ? tl.dres[fc] : 0.0}
-                                 : EventDev{(long long)(x.i0 + fr + P.ev_row_off), (long long)(x.j0 + fc), 1, x.t, tl.dres[128 + fr],
+                                 : EventDev{(long long)(x.i0 + fr + P.ev_row_off), (long long)(x.j0 + fc + P.ev_col_off), 1, x.t, tl.dres[128 + fr],
                                             tl.dres[fc]};
       }
       if (vt == 0) tl.retry = multi ? 1 : 0;

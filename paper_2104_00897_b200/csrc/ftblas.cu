@@ -234,6 +234,7 @@ struct ReportSink {
   int64_t ev_cap;
   int64_t row_off;  // global row of this piece's row 0
   int64_t units;    // out: accumulated units checked
+  int64_t col_off = 0;  // global column of this piece's column 0
 };
 
 // The core entry: device pointers, protected (FT) or not, explicit fault list.
@@ -325,6 +326,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.events = sink ? sink->events : reinterpret_cast<ftk::EventDev *>(scratch + cnt_bytes);
   p.ev_cap = sink ? sink->ev_cap : ev_cap;
   p.ev_row_off = sink ? sink->row_off : 0;
+  p.ev_col_off = sink ? sink->col_off : 0;
   if (sink && ft) sink->units += (int64_t)p.ntiles * T;
   p.faults = fd.empty() ? nullptr : reinterpret_cast<const ftk::FaultDev *>(scratch + cnt_bytes + ev_bytes);
   p.nfaults = (int)fd.size();
@@ -493,12 +495,17 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   return 0;
 }
 
+int num_sms();
+
 // Host-buffer variant (the end-to-end API).  B goes to the device once; C is processed in row
 // panels (multiples of the 127-row unit, so the verification units are those of one call)
 // through a three-stream pipeline: the H2D copy of panel r+1's op(A) rows (and C0 rows) and
-// the D2H copy of panel r-1's result overlap the protected GEMM of panel r.  Faults are routed
-// to their panel with local rows; counters and events accumulate on the device (events carry
-// global rows) and the report is filled once at the end.
+// the D2H copy of panel r-1's result overlap the protected GEMM of panel r.  The first and the
+// last panel run in column chunks (edges multiples of 2 x 127 columns): the first panel starts
+// as soon as its op(A) rows and the first chunk of op(B) are on the device, the rest of B
+// streaming in behind it chunk by chunk; the last panel returns its result chunk by chunk.
+// Faults are routed to their panel / chunk with local indices; counters and events accumulate
+// on the device (events carry global indices) and the report is filled once at the end.
 int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
                     const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                     double *C, int64_t ldc, ftblas_err_report_t *err) {
@@ -539,6 +546,29 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   const int64_t npan = (m + P - 1) / P;
   const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
 
+  // Column chunks of a panel of pr rows: 2..8 chunks minimising the number of 148-CTA waves
+  // (ties: more chunks, i.e. a shorter pipeline start); one chunk when there is one panel.
+  auto chunking = [&](int64_t pr) {
+    std::vector<int64_t> best{0, n};
+    if (npan < 2) return best;
+    const int64_t tile = ft ? ftk::TN : ftk::BN, trows = (pr + (ft ? ftk::TM : ftk::BM) - 1) / (ft ? ftk::TM : ftk::BM);
+    const int64_t sms = num_sms();
+    int64_t best_waves = INT64_MAX;
+    for (int64_t c = 2; c <= 8; ++c) {
+      const int64_t w = ((n + c - 1) / c + unit2 - 1) / unit2 * unit2;
+      if (w >= n) continue;
+      std::vector<int64_t> e{0};
+      int64_t waves = 0;
+      for (int64_t c0 = 0; c0 < n; c0 += w) {
+        const int64_t cw = std::min(w, n - c0);
+        waves += (trows * ((cw + tile - 1) / tile) + sms - 1) / sms;
+        e.push_back(c0 + cw);
+      }
+      if (waves <= best_waves) { best_waves = waves; best = e; }
+    }
+    return best;
+  };
+
   cudaStream_t sh = nullptr, sd = nullptr;
   CUDA_TRY(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
@@ -569,13 +599,16 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   fail(cudaStreamWaitEvent(sd, ev_b, 0));
   ReportSink sink{reinterpret_cast<unsigned long long *>(rep_base),
                   reinterpret_cast<ftk::EventDev *>(rep_base + 256), ev_cap, 0, 0};
-  if (r == 0) {
-    fail(cudaMemsetAsync(rep_base, 0, cnt_bytes, st));
-    fail(cudaMemcpy2DAsync(dB, sizeof(double) * br, B, sizeof(double) * ldb, sizeof(double) * br, bc,
-                           cudaMemcpyHostToDevice, sh));
-    fail(cudaEventRecord(ev_b, sh));
-    fail(cudaStreamWaitEvent(st, ev_b, 0));
-  }
+  if (r == 0) fail(cudaMemsetAsync(rep_base, 0, cnt_bytes, st));
+  // op(B) columns [c0, c1) -> device (dB keeps the stored layout, leading dimension br).
+  auto upload_b = [&](int64_t c0, int64_t c1) {
+    if (is_n(tb))
+      fail(cudaMemcpy2DAsync(dB + c0 * br, sizeof(double) * br, B + c0 * ldb, sizeof(double) * ldb,
+                             sizeof(double) * br, c1 - c0, cudaMemcpyHostToDevice, sh));
+    else
+      fail(cudaMemcpy2DAsync(dB + c0, sizeof(double) * br, B + c0, sizeof(double) * ldb, sizeof(double) * (c1 - c0),
+                             bc, cudaMemcpyHostToDevice, sh));
+  };
   for (int64_t pi = 0; pi < npan && r == 0; ++pi) {
     const int q = (int)(pi & 1);
     const int64_t r0 = pi * P, pr = std::min<int64_t>(P, m - r0);
@@ -592,17 +625,40 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
     fail(cudaEventRecord(ev_in[q], sh));
     fail(cudaStreamWaitEvent(st, ev_in[q], 0));
     if (r) break;
-    std::vector<ftblas_fault_t> pf;
-    for (const auto &f : faults)
-      if (f.i >= r0 && f.i < r0 + pr) pf.push_back(ftblas_fault_t{f.i - r0, f.j, f.step, f.delta});
-    sink.row_off = r0;
-    r = dgemm_core(ft, pf, ta, tb, pr, n, k, alpha, dA[q], is_n(ta) ? pr : k, dB, br, beta, dC[q], pr, nullptr,
-                   ft ? &sink : nullptr);
+    const bool first = pi == 0, last = pi == npan - 1;
+    const std::vector<int64_t> edges = (first || last) ? chunking(pr) : std::vector<int64_t>{0, n};
+    for (size_t ci = 0; ci + 1 < edges.size() && r == 0; ++ci) {
+      const int64_t c0 = edges[ci], c1 = edges[ci + 1];
+      if (first) {  // this chunk of op(B) (all of it when unchunked), then compute on it
+        upload_b(c0, c1);
+        fail(cudaEventRecord(ev_b, sh));
+        fail(cudaStreamWaitEvent(st, ev_b, 0));
+        if (r) break;
+      }
+      std::vector<ftblas_fault_t> pf;
+      for (const auto &f : faults)
+        if (f.i >= r0 && f.i < r0 + pr && f.j >= c0 && f.j < c1)
+          pf.push_back(ftblas_fault_t{f.i - r0, f.j - c0, f.step, f.delta});
+      sink.row_off = r0;
+      sink.col_off = c0;
+      const double *Bc = is_n(tb) ? dB + c0 * br : dB + c0;
+      r = dgemm_core(ft, pf, ta, tb, pr, c1 - c0, k, alpha, dA[q], is_n(ta) ? pr : k, Bc, br, beta, dC[q] + c0 * pr,
+                     pr, nullptr, ft ? &sink : nullptr);
+      if (r) break;
+      if (last) {  // return this chunk of the result
+        fail(cudaEventRecord(ev_out[q], st));
+        fail(cudaStreamWaitEvent(sd, ev_out[q], 0));
+        fail(cudaMemcpy2DAsync(C + r0 + c0 * ldc, sizeof(double) * ldc, dC[q] + c0 * pr, sizeof(double) * pr,
+                               sizeof(double) * pr, c1 - c0, cudaMemcpyDeviceToHost, sd));
+      }
+    }
     if (r) break;
-    fail(cudaEventRecord(ev_out[q], st));
-    fail(cudaStreamWaitEvent(sd, ev_out[q], 0));
-    fail(cudaMemcpy2DAsync(C + r0, sizeof(double) * ldc, dC[q], sizeof(double) * pr, sizeof(double) * pr, n,
-                           cudaMemcpyDeviceToHost, sd));
+    if (!last) {
+      fail(cudaEventRecord(ev_out[q], st));
+      fail(cudaStreamWaitEvent(sd, ev_out[q], 0));
+      fail(cudaMemcpy2DAsync(C + r0, sizeof(double) * ldc, dC[q], sizeof(double) * pr, sizeof(double) * pr, n,
+                             cudaMemcpyDeviceToHost, sd));
+    }
     fail(cudaEventRecord(ev_free[q], sd));
   }
   fail(cudaStreamSynchronize(sd));
@@ -761,6 +817,7 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
 }
 
 // ---------------------------------------------------------------- FT-DTRSM (NEXT-3)
+
 // op(A) X = alpha B, side 'L'.  Recursive blocked solve: a block of more than LEAF rows is
 // split (first part a multiple of LEAF), the parts are solved recursively and the coupling
 // is a GEMM update B2 -= op(A)21 X1 (forward, op(A) lower) or B1 -= op(A)12 X2 (backward, op(A)
@@ -770,7 +827,7 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
 // p, or in the leaf when i and p share one LEAF block.
 struct TrsmCtx {
   bool ft, fwd, trans, unit;
-  int64_t leaf;  // diagonal block rows (LEAF; 127 was tried for the protected solve: no faster)
+  int64_t leaf;  // diagonal block rows (LEAF; 127 for the protected solve measured slower)
   const double *A;
   int64_t lda;
   double *B;
@@ -796,16 +853,24 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
   P.nb = (int)mb; P.n = (int)c.n;
   P.A = c.A + r0 + r0 * c.lda; P.lda = c.lda;
   P.B = c.B + r0; P.ldb = c.ldb;
-  P.trans = c.trans; P.unit = c.unit; P.fwd = c.fwd; P.dmr = c.ft;
+  P.trans = c.trans; P.unit = c.unit;
   P.f = df; P.nf = (int)lf.size(); P.cnt = c.leaf_sc->cnt;
-  static bool attr = false;
   const int smem = (int)(sizeof(double) * (ftt::LEAF * ftt::LEAF + 2 * ftt::LEAF));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 15) / 16, (int64_t)num_sms()));
+  using K = void (*)(ftt::LeafParams);
+  // [fwd][dmr][faults]
+  static const K kernels[2][2][2] = {
+      {{ftt::trsm_leaf_kernel<false, false, false>, ftt::trsm_leaf_kernel<false, false, true>},
+       {ftt::trsm_leaf_kernel<false, true, false>, ftt::trsm_leaf_kernel<false, true, true>}},
+      {{ftt::trsm_leaf_kernel<true, false, false>, ftt::trsm_leaf_kernel<true, false, true>},
+       {ftt::trsm_leaf_kernel<true, true, false>, ftt::trsm_leaf_kernel<true, true, true>}}};
+  static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(ftt::trsm_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int a = 0; a < 8; ++a)
+      CUDA_TRY(cudaFuncSetAttribute(kernels[a >> 2][(a >> 1) & 1][a & 1], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 15) / 16, (int64_t)num_sms()));
-  ftt::trsm_leaf_kernel<<<grid, 512, smem, c.st>>>(P);
+  kernels[c.fwd][c.ft][c.ft && P.nf > 0]<<<grid, 512, smem, c.st>>>(P);
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());
   if (df) CUDA_TRY(cudaFreeAsync(df, c.st));

@@ -8,13 +8,18 @@
 // ftblas.cu; this kernel solves one diagonal block S = op(A)[r0:r0+nb, r0:r0+nb], nb <= 128,
 // for all n right-hand sides: X_blk = S^-1 B_blk, in place.
 //
-// Layout: the block is staged in shared memory column-major by op(A) (Sc[i*nb + p] =
-// S(p, i)), so the update of step i reads one contiguous column across the lanes (conflict
-// free).  One warp per right-hand side column (grid-stride); lane l owns rows l, l+32, l+64,
-// l+96.  Forward (lower S): x_i = b_i * rd_i, then b_p -= S(p,i) x_i for p > i; backward
-// (upper S) runs i from nb-1 down.  Every FP64 operation is computed twice (two register
-// copies of the column, two reciprocal tables); the copies are compared bitwise at the end,
-// a warp vote triggers the third computation, which settles each mismatching element.
+// Layout: the block is staged in shared memory column-major by op(A) and padded to LEAF x LEAF
+// with an identity tail (Sc[i*LEAF + p] = S(p, i); rows/columns >= nb are unit rows), so every
+// column runs the same fully static schedule.  One warp per right-hand side column (grid-stride);
+// lane l owns rows l + 32q (q = 0..3, the "slots").  Forward (lower S): for i = 0..nb-1,
+// x_i = b_i * rd_i broadcast from its owner lane, then b_p -= S(p, i) x_i for p > i; backward
+// (upper S) runs i from nb-1 down.  The slot of i is a compile-time constant, so a step touches
+// only the slots below (forward) / above (backward) it unconditionally plus one predicated FMA
+// on its own slot: no register selects, no per-slot predicates.  A lane's own x_p is formed
+// once, after the last step that updates it (the same product its owner step broadcast).  Every
+// FP64 operation is computed twice (two register copies of the column, two reciprocal tables);
+// the copies are compared bitwise at the end, a warp vote triggers the third computation, which
+// settles each mismatching element.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -31,80 +36,105 @@ struct LeafParams {
   int64_t lda;
   double *B;        // B at row r0
   int64_t ldb;
-  bool trans, unit, fwd, dmr;
-  const ftd::DmrFault *f;  // faults of this block: index = local row i, step = local p (p < i fwd)
+  bool trans, unit;
+  const ftd::DmrFault *f;  // faults of this block: index = j * LEAF + local row i, step = local p
   int nf;
   unsigned long long *cnt;  // ftd::D_* counters
 };
+
+// Reciprocal as its own instruction sequence (asm volatile: the two DMR copies are not merged).
+__device__ __forceinline__ double v_rcp(double d) {
+  double r;
+  asm volatile("div.rn.f64 %0, 0d3FF0000000000000, %1;" : "=d"(r) : "d"(d));
+  return r;
+}
 
 __device__ __forceinline__ double leaf_a(const LeafParams &P, int p, int i) {  // S(p, i) = op(A)(p, i)
   return P.trans ? P.A[i + (int64_t)p * P.lda] : P.A[p + (int64_t)i * P.lda];
 }
 
-// One column's solve, both DMR copies in the same pass (two independent dependence chains
-// interleaved: x1 / x2 broadcast by two shuffles per step); the step's column of S is loaded
-// first so the shared-memory latency overlaps the shuffle.  The fault hook (original copy
-// only) adds delta to b_fi after the update from x_fstep.
-template <bool DUAL>
-__device__ __forceinline__ void leaf_column(const LeafParams &P, const double *Sc, const double *rd1,
-                                            const double *rd2, double (&b1)[4], double (&b2)[4], int lane, int fi,
-                                            int fstep, double fdel) {
-  const int nb = P.nb;
-  for (int s = 0; s < nb; ++s) {
-    const int i = P.fwd ? s : nb - 1 - s;
-    const int owner = i & 31, slot = i >> 5;
-    double sv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sv[q] = lane + 32 * q < nb ? Sc[i * nb + lane + 32 * q] : 0.0;
-    double bi1 = b1[0], bi2 = b2[0];
-#pragma unroll
-    for (int q = 1; q < 4; ++q) {
-      bi1 = slot == q ? b1[q] : bi1;
-      if (DUAL) bi2 = slot == q ? b2[q] : bi2;
+// The 32 steps of slot SL (rows i = 32 SL + l), both DMR copies as two interleaved dependence
+// chains.  The fault hook (original copy only) adds fdel to row fi after the update from x_fstep.
+template <int SL, bool FWD, bool DUAL, bool FLT>
+__device__ __forceinline__ void leaf_slot(const double *__restrict__ Sc, double (&b1)[4], double (&b2)[4],
+                                          const double (&r1)[4], const double (&r2)[4], int lane, int fi, int fstep,
+                                          double fdel) {
+#pragma unroll 2
+  for (int s = 0; s < 32; ++s) {
+    const int l = FWD ? s : 31 - s;
+    const double *col = Sc + (32 * SL + l) * LEAF + lane;
+    const double x1 = __shfl_sync(0xffffffffu, ftd::v_mul(b1[SL], r1[SL]), l);
+    const double x2 = DUAL ? __shfl_sync(0xffffffffu, ftd::v_mul(b2[SL], r2[SL]), l) : 0.0;
+    if (FWD ? lane > l : lane < l) {
+      const double a = col[32 * SL];
+      b1[SL] = ftd::v_fma(-a, x1, b1[SL]);
+      if (DUAL) b2[SL] = ftd::v_fma(-a, x2, b2[SL]);
     }
-    const double x1 = __shfl_sync(0xffffffffu, P.unit ? bi1 : ftd::v_mul(bi1, rd1[i]), owner);
-    const double x2 = DUAL ? __shfl_sync(0xffffffffu, P.unit ? bi2 : ftd::v_mul(bi2, rd2[i]), owner) : 0.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int p = lane + 32 * q;
-      if (q == slot && lane == owner) {
-        b1[q] = x1;
-        if (DUAL) b2[q] = x2;
+      if (FWD ? q > SL : q < SL) {
+        const double a = col[32 * q];
+        b1[q] = ftd::v_fma(-a, x1, b1[q]);
+        if (DUAL) b2[q] = ftd::v_fma(-a, x2, b2[q]);
       }
-      const bool upd = P.fwd ? (p > i && p < nb) : (p < i);
-      if (upd) {
-        b1[q] = ftd::v_fma(-sv[q], x1, b1[q]);
-        if (DUAL) b2[q] = ftd::v_fma(-sv[q], x2, b2[q]);
-      }
-      if (p == fi && i == fstep) b1[q] = ftd::v_add(b1[q], fdel);
     }
+    if (FLT && 32 * SL + l == fstep) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q == fi) b1[q] = ftd::v_add(b1[q], fdel);
+    }
+  }
+  b1[SL] = ftd::v_mul(b1[SL], r1[SL]);  // this lane's x of the slot: no later step changes b
+  if (DUAL) b2[SL] = ftd::v_mul(b2[SL], r2[SL]);
+}
+
+template <bool FWD, bool DUAL, bool FLT>
+__device__ __forceinline__ void leaf_column(const double *Sc, double (&b1)[4], double (&b2)[4], const double (&r1)[4],
+                                            const double (&r2)[4], int lane, int nslots, int fi, int fstep,
+                                            double fdel) {
+  if (FWD) {
+    leaf_slot<0, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 1) leaf_slot<1, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 2) leaf_slot<2, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 3) leaf_slot<3, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+  } else {
+    if (nslots > 3) leaf_slot<3, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 2) leaf_slot<2, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 1) leaf_slot<1, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    leaf_slot<0, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
   }
 }
 
+template <bool FWD, bool DMR, bool FLT>
 __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
   extern __shared__ double sm[];
   double *Sc = sm, *rd1 = sm + LEAF * LEAF, *rd2 = rd1 + LEAF;
-  const int nb = P.nb, tid = threadIdx.x, lane = tid & 31;
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, p = e % nb;
-    Sc[i * nb + p] = leaf_a(P, p, i);
+  const int nb = P.nb, tid = threadIdx.x, lane = tid & 31, nslots = (nb + 31) >> 5;
+  for (int e = tid; e < LEAF * LEAF; e += blockDim.x) {
+    const int i = e / LEAF, p = e % LEAF;
+    Sc[e] = p < nb && i < nb ? leaf_a(P, p, i) : (p == i ? 1.0 : 0.0);
   }
   __syncthreads();
-  for (int i = tid; i < nb; i += blockDim.x) {  // packed reciprocals of the diagonal, twice
-    rd1[i] = 1.0 / Sc[i * nb + i];
-    rd2[i] = 1.0 / Sc[i * nb + i];
+  for (int i = tid; i < LEAF; i += blockDim.x) {  // packed reciprocals of the diagonal, twice
+    const double d = Sc[i * LEAF + i];
+    rd1[i] = P.unit ? 1.0 : v_rcp(d);
+    rd2[i] = P.unit ? 1.0 : v_rcp(d);
   }
   __syncthreads();
+  double r1[4], r2[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { r1[q] = rd1[lane + 32 * q]; r2[q] = rd2[lane + 32 * q]; }
   const int warps = blockDim.x >> 5;
   for (int j = blockIdx.x * warps + (tid >> 5); j < P.n; j += gridDim.x * warps) {
     double *col = P.B + (int64_t)j * P.ldb;
     // This lane's fault in column j, if any (at most one per lane is honoured).
     int fi = -1, fstep = -1;
     double fdel = 0.0;
-    for (int e = 0; e < P.nf; ++e) {
-      const int64_t code = P.f[e].index;  // j * LEAF + local row
-      if (code / LEAF == j && (int)(code % LEAF) % 32 == lane) { fi = (int)(code % LEAF); fstep = (int)P.f[e].step; fdel = P.f[e].delta; }
-    }
+    if (FLT)
+      for (int e = 0; e < P.nf; ++e) {
+        const int64_t code = P.f[e].index;  // j * LEAF + local row
+        if (code / LEAF == j && (int)(code % LEAF) % 32 == lane) { fi = (int)(code % LEAF); fstep = (int)P.f[e].step; fdel = P.f[e].delta; }
+      }
     double b1[4], b2[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -112,33 +142,32 @@ __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
       b1[q] = p < nb ? col[p] : 0.0;
       b2[q] = b1[q];
     }
-    if (P.dmr) leaf_column<true>(P, Sc, rd1, rd2, b1, b2, lane, fi, fstep, fdel);
-    else leaf_column<false>(P, Sc, rd1, rd2, b1, b2, lane, -1, -1, 0.0);
-    bool bad = false;
-    if (P.dmr)
+    leaf_column<FWD, DMR, FLT>(Sc, b1, b2, r1, r2, lane, nslots, fi, fstep, fdel);
+    if (DMR) {
+      bool bad = false;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) bad |= (lane + 32 * q < nb) && ftd::differ(b1[q], b2[q]);
-    if (__any_sync(0xffffffffu, bad)) {
-      // Rare: a third computation settles the column (the verification unit of a diagonal
-      // block: one fault propagates to every later row of the column).  Each element takes
-      // the third value; the column is corrected when the third agrees with one copy wherever
-      // the two disagreed.
-      double b3[4];
+      for (int q = 0; q < 4; ++q) bad |= (lane + 32 * q < nb) && ftd::differ(b1[q], b2[q]);
+      if (__any_sync(0xffffffffu, bad)) {
+        // Rare: a third computation settles the column (the verification unit of a diagonal
+        // block: one fault propagates to every later row of the column).  Each element takes
+        // the third value; the column is corrected when the third agrees with one copy wherever
+        // the two disagreed.
+        double b3[4], b4[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) b3[q] = lane + 32 * q < nb ? col[lane + 32 * q] : 0.0;
-      double b4[4];
-      leaf_column<false>(P, Sc, rd2, rd2, b3, b4, lane, -1, -1, 0.0);
-      bool unsettled = false;
+        for (int q = 0; q < 4; ++q) b3[q] = lane + 32 * q < nb ? col[lane + 32 * q] : 0.0;
+        leaf_column<FWD, false, false>(Sc, b3, b4, r2, r2, lane, nslots, -1, -1, 0.0);
+        bool unsettled = false;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (lane + 32 * q < nb && ftd::differ(b1[q], b2[q]))
-          unsettled |= ftd::differ(b3[q], b1[q]) && ftd::differ(b3[q], b2[q]);
-        b1[q] = b3[q];
-      }
-      unsettled = __any_sync(0xffffffffu, unsettled);
-      if (lane == 0) {
-        atomicAdd(&P.cnt[ftd::D_DETECTED], 1ull);
-        atomicAdd(&P.cnt[unsettled ? ftd::D_UNCORRECTABLE : ftd::D_CORRECTED], 1ull);
+        for (int q = 0; q < 4; ++q) {
+          if (lane + 32 * q < nb && ftd::differ(b1[q], b2[q]))
+            unsettled |= ftd::differ(b3[q], b1[q]) && ftd::differ(b3[q], b2[q]);
+          b1[q] = b3[q];
+        }
+        unsettled = __any_sync(0xffffffffu, unsettled);
+        if (lane == 0) {
+          atomicAdd(&P.cnt[ftd::D_DETECTED], 1ull);
+          atomicAdd(&P.cnt[unsettled ? ftd::D_UNCORRECTABLE : ftd::D_CORRECTED], 1ull);
+        }
       }
     }
 #pragma unroll

@@ -240,25 +240,31 @@ def test_host_buffer_api_matches():
     assert np.all(np.abs(C - Co.reshape((n, m)).T) <= bound(None, A, B, C0, 1.5, 0.5, "N", "N", k))
 
 
-def test_host_buffer_pipeline_row_panels():
+@pytest.mark.parametrize("trans", ["NN", "NT", "TT"])
+def test_host_buffer_pipeline_row_panels(trans):
     """m large enough for the row-panel pipeline of the host-buffer API (panels of a multiple
-    of 254 rows, copies overlapped with compute): faults in several panels, events with global
-    rows, counters summed over panels, values within the bound."""
+    of 254 rows, copies overlapped with compute; the first and last panels in column chunks of
+    a multiple of 254 columns): faults in several panels and chunks, events with global rows
+    and columns, counters summed over the pieces, values within the bound."""
+    ta, tb = trans
     rng = np.random.default_rng(112)
-    m, n, k = 4600, 260, 140
+    m, n, k = 4600, 300, 140
     A, B, C0 = rand(rng, m, k), rand(rng, k, n), rand(rng, m, n)
-    faults = [(5, 7, 10, 3.0), (1200, 100, 70, -2.0), (2541, 255, 139, 9.0), (4599, 0, 0, 1.5),
-              (4598, 1, 5, 4.0)]
+    As, Bs = stored(A, ta), stored(B, tb)
+    lda, ldb = As.shape[0], Bs.shape[0]
+    faults = [(5, 7, 10, 3.0), (10, 290, 20, 6.0), (1200, 100, 70, -2.0), (2541, 255, 139, 9.0),
+              (4599, 0, 0, 1.5), (4598, 1, 5, 4.0), (4590, 280, 100, -3.0)]
     C = np.asfortranarray(C0.copy())
     F.ftblas_inject_arm(faults)
-    rep = F.ftblas_dgemm_host("N", "N", m, n, k, 1.25, A, m, B, k, -0.5, C, m)
-    Co, orep = oracle.dgemm_abft("N", "N", m, n, k, 1.25, A, m, B, k, -0.5, C0, m,
+    rep = F.ftblas_dgemm_host(ta, tb, m, n, k, 1.25, As, lda, Bs, ldb, -0.5, C, m)
+    Co, orep = oracle.dgemm_abft(ta, tb, m, n, k, 1.25, As, lda, Bs, ldb, -0.5, C0, m,
                                  BM=rep.unit_rows, BN=rep.unit_cols, BK=rep.step_quantum, faults=faults)
     assert rep.units_checked == orep.units_checked
-    assert_reports_match(rep, orep, A, B, "N", "N", k)
+    assert_reports_match(rep, orep, As, Bs, ta, tb, k)
+    assert rep.detected == 6  # two faults share a unit
     assert np.all(np.abs(C - Co.reshape((n, m)).T) <= bound(None, A, B, C0, 1.25, -0.5, "N", "N", k))
     Ct = np.asfortranarray(np.zeros((m, n)))
-    F.ftblas_dgemm_noft_host("T", "N", m, n, k, 1.0, np.asfortranarray(A.T), k, B, k, 0.0, Ct, m)
+    F.ftblas_dgemm_noft_host(ta, tb, m, n, k, 1.0, As, lda, Bs, ldb, 0.0, Ct, m)
     assert np.all(np.abs(Ct - A @ B) <= bound(None, A, B, np.zeros((m, n)), 1.0, 0.0, "N", "N", k))
 
 

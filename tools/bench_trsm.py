@@ -10,6 +10,9 @@ import torch  # noqa: E402
 
 from paper_2104_00897_b200 import ftblas as F  # noqa: E402
 
+if len(sys.argv) > 1:  # alternative build of the library
+    F.LIB_PATH = sys.argv[1]
+
 R = 5
 
 
