@@ -795,6 +795,8 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
   const TileGeom x = load_geom(tl.geo);
   const int lane = vt & 31;
       // ctile is indexed by staged rows / columns: data row i at i + oa, data column j at j + ob.
+      // The sums run over the data only (a partial tile's checksum row / column sits right after
+      // its data).
       const int cidx = vt & 127;
       const bool is_row = vt >= 128;
       double r = 0.0, cs = 0.0;
@@ -802,12 +804,12 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
         if (is_row) {
           const double *rowp = ctile + (cidx + x.oa);
   #pragma unroll 9
-          for (int j = 0; j < DM; ++j) r += rowp[(j + x.ob) * LDC_S];
+          for (int j = 0; j < x.bn_eff; ++j) r += rowp[(j + x.ob) * LDC_S];
           cs = rowp[x.crb * LDC_S];  // A_I (B_J e)
         } else {
           const double *colp = ctile + (cidx + x.ob) * LDC_S;
   #pragma unroll 9
-          for (int i = 0; i < DM; ++i) r += colp[i + x.oa];
+          for (int i = 0; i < x.bm_eff; ++i) r += colp[i + x.oa];
           cs = colp[x.cra];  // (e^T A_I) B_J
         }
       }
@@ -877,9 +879,18 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   double *const ring = x.ring;
   double *const ctile = ring;  // epilogue reuse of the ring
   const int lane = x.lane, nk = x.nk;
-  const int mw = mma_warp(x.warp), wm = mw >> 2, wn = mw & 3;
+  // Warp w runs on SM sub-partition w & 3.  The 64 x 32 quarter (wm, wn) of warp w has
+  // wn = (w + 2 wm) & 3, so each warp row spans all four sub-partitions and the two warps of a
+  // warp column sit on different ones (a partial edge tile's active warps share the DMMA pipes
+  // of at least two sub-partitions).
+  const int mw = mma_warp(x.warp), wm = mw >> 2, wn = (mw + 2 * wm) & 3;
   const int g = lane >> 2, t = lane & 3;
   const int vt = mw * 32 + lane;  // 0..255
+  // Rows / columns of the MMA tile that carry data or a checksum; in the protected kernel a
+  // warp whose quarter holds none of them (partial edge tiles) waits and releases the stages
+  // without issuing DMMA.  (The unprotected kernel keeps one loop: the split costs its k-loop
+  // codegen and its tiles are only partial at sizes that are not multiples of 128.)
+  const bool active = !FT || (wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1));
   double acc[8][4][2];
   int stage_base = 0;
   for (int attempt = 0;; ++attempt) {
@@ -928,6 +939,14 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     // injection code (which would make the register allocator shuffle accumulators).
     for (int s = 0; s < nk;) {
       const int s_end = __shfl_sync(0xffffffffu, next_stage < nk ? next_stage : nk, 0);
+      if (FT && !active) {  // nothing of this warp's quarter is used: release the stages only
+        for (; s < s_end; ++s) {
+          const int gs = stage_base + s, slot = gs % STAGES;
+          mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tl.empty[slot]);
+        }
+      }
       for (; s < s_end; ++s) {
         const int gs = stage_base + s, slot = gs % STAGES;
         mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
@@ -1041,8 +1060,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   x.bn_eff = (int)min64(tn, P.n - x.j0);
   x.oa = g127 ? (x.i0 & 1) : 0;
   x.ob = g127 ? (x.j0 & 1) : 0;
-  x.cra = x.oa ? 0 : DM;
-  x.crb = x.ob ? 0 : DM;
+  // Checksum row / column: 0 for odd tiles (data in staged rows 1..127), else 127; a partial
+  // even tile at the matrix edge takes the first row / column past its data instead (staged as
+  // TMA's out-of-bounds zeros), so its used rows / columns stay contiguous from 0 and the MMA
+  // warps whose 64 x 32 quarter holds none of them skip the DMMA stream (mma_role).
+  x.cra = x.oa ? 0 : (g127 && x.bm_eff < DM ? x.bm_eff : DM);
+  x.crb = x.ob ? 0 : (g127 && x.bn_eff < DM ? x.bn_eff : DM);
   x.nk = (int)((x.k1 - x.k0 + BK - 1) / BK);
 
   if (x.tid == 0) {

@@ -1,4 +1,5 @@
-"""Dev: FT overhead at 8192^3 NN under FTBLAS_DEV_MODE variants (1 skip pass 2, 2 skip encode, 4 never flag)."""
+"""Dev: FT overhead (NN, m x n x k from env M N K, default 8192^3) under FTBLAS_DEV_MODE variants
+(1 skip pass 2, 2 skip encode, 4 never flag, 32 noft on the 127 grid, 128 no clusters)."""
 import sys, os, json, subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 code = r'''
@@ -7,22 +8,23 @@ sys.path.insert(0, %r)
 import torch
 from paper_2104_00897_b200 import ftblas as F
 N = int(os.environ.get("N", "8192"))
+M, K = int(os.environ.get("M", N)), int(os.environ.get("K", N))
 g = torch.Generator(device="cuda").manual_seed(0)
-A = torch.rand(N * N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
-B = torch.rand(N * N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
-C = torch.zeros(N * N, dtype=torch.float64, device="cuda")
+A = torch.rand(M * K, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+B = torch.rand(K * N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+C = torch.zeros(M * N, dtype=torch.float64, device="cuda")
 res = {}
 for name in ["noft", "ft", "noft", "ft"]:
     ts = []
     for r in range(4):
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
-        if name == "ft": F.ftblas_dgemm("N", "N", N, N, N, 1.0, A, N, B, N, 0.0, C, N, report=False)
-        else: F.ftblas_dgemm_noft("N", "N", N, N, N, 1.0, A, N, B, N, 0.0, C, N)
+        if name == "ft": F.ftblas_dgemm("N", "N", M, N, K, 1.0, A, M, B, K, 0.0, C, M, report=False)
+        else: F.ftblas_dgemm_noft("N", "N", M, N, K, 1.0, A, M, B, K, 0.0, C, M)
         e1.record(); torch.cuda.synchronize()
         if r: ts.append(e0.elapsed_time(e1))
     res[name] = min(ts)
-print(json.dumps({"mode": os.environ.get("FTBLAS_DEV_MODE", "0"), "N": N, "noft_ms": res["noft"], "ft_ms": res["ft"],
+print(json.dumps({"mode": os.environ.get("FTBLAS_DEV_MODE", "0"), "MNK": [M, N, K], "noft_ms": res["noft"], "ft_ms": res["ft"],
                   "overhead_pct": 100 * (res["ft"] - res["noft"]) / res["noft"]}), flush=True)
 ''' % ROOT
 for mode in (sys.argv[1:] or ["0", "5", "6"]):
