@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--seed", type=int, default=1234)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-unfused", action="store_true", help="skip the unfused ABFT baseline timing")
+    p.add_argument("--no-unfused", action="store_true", help="skip the comparison timings (PREPASS encode, unfused baseline, no-fault protected, cuBLAS)")
     p.add_argument("--interval", type=int, default=0,
                    help="verification interval Kc (multiple of 16; 0 = k): ftblas_set_interval")
     p.add_argument("--cpu-sample-units", type=int, default=0)
@@ -287,11 +287,13 @@ def main():
 
     def step(ft=True):
         """ft: True = the fused protected kernel, False = the unprotected twin,
-        "unfused" = the unfused ABFT baseline (NEXT-2), same faults and report."""
+        "unfused" = the unfused ABFT baseline (NEXT-2), same faults and report,
+        "clean" = the fused protected kernel with no fault armed."""
         if beta != 0.0:
             C.copy_(C0)
         if ft:
-            F.ftblas_inject_arm(W["local_faults"])
+            if ft != "clean":
+                F.ftblas_inject_arm(W["local_faults"])
             call = F.ftblas_dgemm_unfused if ft == "unfused" else F.ftblas_dgemm
             rep = call(ta, tb, mloc, n, k, alpha, A, lda, B, ldb, beta, C, mloc, events_capacity=1024)
             counters.copy_(torch.tensor([rep.units_checked, rep.detected, rep.corrected,
@@ -302,26 +304,31 @@ def main():
         F.ftblas_dgemm_noft(ta, tb, mloc, n, k, alpha, A, lda, B, ldb, beta, C, mloc)
         return None
 
-    def timed(ft, steps, warmup):
+    def timed(ft, steps, warmup, label=None):
         for _ in range(warmup):
             step(ft)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         F.ftblas_take_launch_count()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        reps = [step(ft) for _ in range(steps)]
-        e1.record(stream)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record(stream)
+        reps = []
+        for i in range(steps):
+            reps.append(step(ft))
+            ev[i + 1].record(stream)
         torch.cuda.synchronize()
         launches = F.ftblas_take_launch_count()
-        ms = e0.elapsed_time(e1)
+        ms = ev[0].elapsed_time(ev[-1])
+        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
         if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([ms] + per, dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms, per = float(t[0].item()), [float(x) for x in t[1:].tolist()]
             dist.barrier()
+        timed.min_ms[label if label is not None else ft] = min(per)
         return ms, launches, reps
+    timed.min_ms = {}
 
     # Kernel-only time of the dominant kernel for the roofline: same launches, events
     # bracketing only the ftblas_dgemm call (report copy excluded) on the launch stream.
@@ -333,7 +340,7 @@ def main():
     if not args.no_unfused:
         F.ftblas_set_encode(F.ENCODE_PREPASS)
         try:
-            ms_pre, _, reps_pre = timed(True, args.steps, max(1, args.warmup // 2))
+            ms_pre, _, reps_pre = timed(True, args.steps, max(1, args.warmup // 2), label="prepass")
         finally:
             F.ftblas_set_encode(F.ENCODE_FUSED)
         rp = reps_pre[-1]
@@ -348,6 +355,30 @@ def main():
                "overhead_pct": 100.0 * (ms_unf - ms_noft) / ms_noft, "unit": "128x128",
                "units_checked": ru.units_checked, "detected": ru.detected, "corrected": ru.corrected,
                "recomputed": ru.recomputed}
+    ms_clean = None
+    if not args.no_unfused:
+        ms_clean, _, _ = timed("clean", args.steps, 1)
+    # cuBLAS DGEMM (torch.matmul on float64) on the same operands: a measuring stick, not a target.
+    ms_cublas = None
+    if not args.no_unfused:
+        Aop = A.view(k, mloc).t() if ta == "N" else A.view(mloc, k)
+        Bop = B.view(n, k).t() if tb == "N" else B.view(k, n)
+        torch.matmul(Aop, Bop)
+        torch.cuda.synchronize()
+        cb = []
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            Ct = torch.matmul(Aop, Bop)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            cb.append(e0.elapsed_time(e1))
+            del Ct
+        ms_cublas = min(cb)
+        if world > 1:
+            t = torch.tensor([ms_cublas], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_cublas = float(t.item())
     kern = []
     for _ in range(max(2, min(args.steps, 3))):
         F.ftblas_inject_arm(W["local_faults"])
@@ -428,7 +459,11 @@ def main():
                  "pct_of_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_TFLOPS),
                  "units_checked": cnt[0], "detected": cnt[1], "corrected": cnt[2],
                  "recomputed": cnt[3], "events": cnt[4],
-                 "prepass_encode": pre, "unfused_baseline": unf},
+                 "prepass_encode": pre, "unfused_baseline": unf,
+                 "ms_per_step_min": {"protected": timed.min_ms.get(True), "unprotected": timed.min_ms.get(False)},
+                 "tflops_protected_no_faults": (flops_total * args.steps / (ms_clean * 1e-3) / 1e12
+                                                if ms_clean else None),
+                 "cublas_dgemm_tflops": flops_total / (ms_cublas * 1e-3) / 1e12 if ms_cublas else None},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": "dgemm_abft_kernel (FT)", "kernel_ms": kern_ms,

@@ -935,6 +935,13 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     // unprotected one for the TMA bytes only.
     // 32-bit shared address of the barrier array to wait on (enc = full + STAGES).
     const uint32_t ready = smem_u32(tl.full) + ((verify && !(P.dev_mode & 8)) ? STAGES * 8u : 0u);
+#ifdef FTBLAS_DEV_TIMELINE
+    long long tl_a = clock64(), tl_b = tl_a;
+    if (attempt == 0 && nk > 0) {
+      mbar_wait_u32(ready + 8u * (stage_base % STAGES), (stage_base / STAGES) & 1);
+      tl_b = clock64();
+    }
+#endif
     // The k-loop runs in segments between fault stages, so that the DMMA loop body carries no
     // injection code (which would make the register allocator shuffle accumulators).
     for (int s = 0; s < nk;) {
@@ -988,7 +995,18 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
 
     // ---- verification, out of line so that its register needs do not shape
     // the allocation of the DMMA k-loop above (the accumulators are dead here: staged in smem).
+#ifdef FTBLAS_DEV_TIMELINE
+    const long long tl_c = clock64();
+#endif
     const bool multi = verify_tile<AKM, BKM>(P, tl, ctile, vt, mw);
+#ifdef FTBLAS_DEV_TIMELINE
+    if (attempt == 0 && vt == 0 && P.dev_prof) {
+      unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + 4) * 2;
+      dp[0] = (unsigned long long)(tl_b - tl_a);
+      dp[1] = (unsigned long long)(tl_c - tl_b);
+      dp[2] = (unsigned long long)(clock64() - tl_c);
+    }
+#endif
     if (!multi) break;
     // Out of the one-error model: recompute the whole tile once (no re-verification).
   }
