@@ -91,9 +91,29 @@ struct Params {
   const double *Ac, *Br;
   int64_t ldac, ldbr;
   const unsigned int *amax_pre, *bmax_pre;
+  // Row-shared fused encode (encode mode FUSED): the tile of tile column 0 encodes e^T A_I from
+  // its staged tiles and publishes it per stage through L2 -- Ash[ti + p*ldash] for the 16
+  // k-slots, the slice's R1' high-word maximum hmA[ti + sg*tiles_m] and a release flag
+  // aflag[ti + sg*tiles_m] = 1 (sg = global stage index).  Every other tile of row I copies a
+  // published stage when its flag is already set and otherwise encodes that stage itself (same
+  // integer encode of the same staged data: bitwise the same checksum), so no CTA ever waits on
+  // another.  Null = every CTA encodes A itself.
+  double *Ash;
+  int64_t ldash;
+  unsigned int *hmA, *aflag;
+  // B_J e the same way along tile columns: the tile of tile row 0 publishes Bsh[tj + p*ldbsh],
+  // hmB[tj + sg*tiles_n] and counts its published stages in bcnt[tj + t*tiles_n]; a tile (or
+  // cluster pair) that finds the count complete when it starts copies every stage, otherwise
+  // it encodes B_J e itself (split within the cluster pair).  Null = no sharing.
+  double *Bsh;
+  int64_t ldbsh;
+  unsigned int *hmB, *bcnt;
   unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
   int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
-                                  // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait
+                                  // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait,
+                                  // 32 unprotected kernel on the 127 grid, 128 no clusters, 256 tiles
+                                  // wait for the published e^T A_I, 512 (with 128) tiles wait for
+                                  // the published B_J e (row/column-shared encode copy paths)
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
@@ -108,6 +128,14 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -185,6 +213,11 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 __device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -601,6 +634,7 @@ struct SmemTail {
   uint32_t mail_hm[STAGES];
   uint64_t mfull[STAGES], mfree[STAGES];
   int share;  // this CTA encodes half of B and swaps it with its cluster partner
+  unsigned bobs, bcopy;  // B_J e published by tile row 0: observed here / taken for this tile
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
   double dres[256];                // residuals: 0..127 columns, 128..255 rows
   double red[NTHREADS / 32];
@@ -688,9 +722,60 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     }
   };
   const uint32_t rank = P.cluster2 ? cluster_rank() : 0u;
+  // e^T A_I of stage s into (a0, a1) (layout of enc_operand); the slice maximum folds into
+  // amax_hi.  Row-shared mode: tile column 0 encodes and publishes, the others copy a published
+  // stage or, if it is not out yet, encode it themselves.
+  const bool a_pub = P.Ash && x.tj == 0, a_sub = P.Ash && x.tj != 0;
+  const bool b_pub = P.Bsh && x.ti == 0;
+  auto enc_a = [&](double *sA, int s, double &a0, double &a1, uint32_t &amax) {
+    const int64_t sg = x.k0 / BK + s;  // global stage index
+    const size_t fi = (size_t)x.ti + (size_t)sg * P.tiles_m;
+    if (a_sub) {
+      unsigned ready = 0;
+      if (lane == 0) {
+        ready = ld_acquire_gpu(P.aflag + fi);
+        // development / tests: dev mode 256 waits for the publication (exercises the copy path)
+        while ((P.dev_mode & 256) && !ready) {
+          __nanosleep(256);
+          ready = ld_acquire_gpu(P.aflag + fi);
+        }
+      }
+      ready = __shfl_sync(0xffffffffu, ready, 0);
+      if (ready) {
+        const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
+        const int64_t pg = x.k0 + (int64_t)s * BK + p;
+        if (AKM) {
+          a0 = lane < 8 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
+          a1 = lane < 8 && pg + 1 < x.k1 ? __ldcg(P.Ash + x.ti + (pg + 1) * P.ldash) : 0.0;
+        } else {
+          a0 = lane < 16 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
+        }
+        amax = max(amax, __ldcg(P.hmA + fi));
+        return;
+      }
+    }
+    uint32_t hm = 0u;
+    enc_operand<AKM>(sA, lane, x.cra, a0, a1, hm);
+    amax = max(amax, hm);
+    if (a_pub) {
+      const int p = AKM ? 2 * lane : lane;
+      const int64_t pg = x.k0 + (int64_t)s * BK + p;
+      if (AKM) {
+        if (lane < 8 && pg < x.k1) P.Ash[x.ti + pg * P.ldash] = a0;
+        if (lane < 8 && pg + 1 < x.k1) P.Ash[x.ti + (pg + 1) * P.ldash] = a1;
+      } else if (lane < 16 && pg < x.k1) {
+        P.Ash[x.ti + pg * P.ldash] = a0;
+      }
+      if (lane == 0) P.hmA[fi] = hm;
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(P.aflag + fi, 1u);
+    }
+  };
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
-    const bool share = verify && tl.share;
+    const bool bcopy = verify && tl.bcopy;
+    const bool share = verify && tl.share && !bcopy;
     if (lane == 0)
       for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
     uint32_t amax_hi = 0u, bmax_hi = 0u;
@@ -710,57 +795,70 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         } else if (P.dev_mode & 1) {  // development: pass 1 only
           amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
           bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
-        } else if (share) {
-          // Cluster pair: all of e^T A_I, the half `rank` of B_J e; swap B halves with the partner.
-          enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);
-          uint32_t hmb;
-          enc_operand_h<BKM>(sB, lane, (int)rank, x.crb, b0, b1, hmb);
+        } else if ((P.dev_mode & 2) && !share && !bcopy) {
+          // development: no encode (checksum rows zero)
+        } else {
+          enc_a(sA, s, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           if (AKM) {
             if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
           } else {
             if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
           }
-          // own half into the staged tile and into the partner's mailbox (lanes 0..3 hold two
-          // k-slots each for a K-major B, lanes 0..7 one each for an MN-major B)
-          if (gs >= STAGES && lane == 0) mbar_wait_acq_cluster(&tl.mfree[slot], ((gs / STAGES) - 1) & 1);
-          __syncwarp();
-          const uint32_t pmail = mapa_u32(smem_u32(&tl.mail[slot][0]), rank ^ 1u);
-          if (BKM) {
-            if (lane < 4) {
-              *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 8 * (int)rank + 2 * lane)) = make_double2(b0, b1);
-              st_cluster_f64(pmail + 8u * (2 * lane), b0);
-              st_cluster_f64(pmail + 8u * (2 * lane + 1), b1);
+          const int64_t sg = x.k0 / BK + s;  // global stage index
+          if (bcopy) {  // B_J e of this stage as published by tile row 0
+            const int64_t pg = x.k0 + (int64_t)s * BK + lane;
+            if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pg < x.k1 ? __ldcg(P.Bsh + x.tj + pg * P.ldbsh) : 0.0;
+            bmax_hi = max(bmax_hi, __ldcg(P.hmB + x.tj + (size_t)sg * P.tiles_n));
+          } else {
+            uint32_t hmb = 0u;
+            if (share) {
+              // Cluster pair: the half `rank` of B_J e here, the other half from the partner.
+              enc_operand_h<BKM>(sB, lane, (int)rank, x.crb, b0, b1, hmb);
+              // own half into the staged tile and into the partner's mailbox (lanes 0..3 hold two
+              // k-slots each for a K-major B, lanes 0..7 one each for an MN-major B)
+              if (gs >= STAGES && lane == 0) mbar_wait_acq_cluster(&tl.mfree[slot], ((gs / STAGES) - 1) & 1);
+              __syncwarp();
+              const uint32_t pmail = mapa_u32(smem_u32(&tl.mail[slot][0]), rank ^ 1u);
+              if (BKM) {
+                if (lane < 4) {
+                  *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 8 * (int)rank + 2 * lane)) = make_double2(b0, b1);
+                  st_cluster_f64(pmail + 8u * (2 * lane), b0);
+                  st_cluster_f64(pmail + 8u * (2 * lane + 1), b1);
+                }
+              } else {
+                if (lane < 8) {
+                  sB[sidx<false>(x.crb, 8 * (int)rank + lane)] = b0;
+                  st_cluster_f64(pmail + 8u * lane, b0);
+                }
+              }
+              if (lane == 0) st_cluster_u32(mapa_u32(smem_u32(&tl.mail_hm[slot]), rank ^ 1u), hmb);
+              __syncwarp();
+              if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tl.mfull[slot]), rank ^ 1u));
+              // the partner's half
+              if (lane == 0) mbar_wait_acq_cluster(&tl.mfull[slot], (gs / STAGES) & 1);
+              __syncwarp();
+              if (lane < 8) sB[sidx<BKM>(x.crb, 8 * (int)(rank ^ 1u) + lane)] = tl.mail[slot][lane];
+              hmb = max(hmb, tl.mail_hm[slot]);
+              __syncwarp();
+              if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tl.mfree[slot]), rank ^ 1u));
+            } else {
+              enc_operand<BKM>(sB, lane, x.crb, b0, b1, hmb);  // B_J e over the 127 data columns
+              if (BKM) {
+                if (lane < 8) *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 2 * lane)) = make_double2(b0, b1);
+              } else {
+                if (lane < 16) sB[sidx<false>(x.crb, lane)] = b0;
+              }
             }
-          } else {
-            if (lane < 8) {
-              sB[sidx<false>(x.crb, 8 * (int)rank + lane)] = b0;
-              st_cluster_f64(pmail + 8u * lane, b0);
+            bmax_hi = max(bmax_hi, hmb);
+            if (b_pub) {  // tile row 0: publish this stage's B_J e for the other tile rows
+              __syncwarp();
+              const int64_t pg = x.k0 + (int64_t)s * BK + lane;
+              if (lane < 16 && pg < x.k1) P.Bsh[x.tj + pg * P.ldbsh] = sB[sidx<BKM>(x.crb, lane)];
+              if (lane == 0) P.hmB[x.tj + (size_t)sg * P.tiles_n] = hmb;
+              __threadfence();
+              __syncwarp();
+              if (lane == 0) atomicAdd(P.bcnt + x.tj + (size_t)x.t * P.tiles_n, 1u);
             }
-          }
-          if (lane == 0) st_cluster_u32(mapa_u32(smem_u32(&tl.mail_hm[slot]), rank ^ 1u), hmb);
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tl.mfull[slot]), rank ^ 1u));
-          // the partner's half
-          if (lane == 0) mbar_wait_acq_cluster(&tl.mfull[slot], (gs / STAGES) & 1);
-          __syncwarp();
-          if (lane < 8) sB[sidx<BKM>(x.crb, 8 * (int)(rank ^ 1u) + lane)] = tl.mail[slot][lane];
-          bmax_hi = max(bmax_hi, max(hmb, tl.mail_hm[slot]));
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tl.mfree[slot]), rank ^ 1u));
-        } else if (!(P.dev_mode & 2)) {
-          enc_operand<AKM>(sA, lane, x.cra, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
-          enc_operand<BKM>(sB, lane, x.crb, b0, b1, bmax_hi);  // B_J e over the 127 data columns
-        }
-        if (!P.Ac && !share) {
-          if (AKM) {
-            if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
-          } else {
-            if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
-          }
-          if (BKM) {
-            if (lane < 8) *reinterpret_cast<double2 *>(sB + sidx<true>(x.crb, 2 * lane)) = make_double2(b0, b1);
-          } else {
-            if (lane < 16) sB[sidx<false>(x.crb, lane)] = b0;
           }
         }
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
@@ -1102,6 +1200,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tl.first_col = 0x7fffffff;
     tl.retry = 0;
     tl.share = share ? 1 : 0;
+    // B_J e fully published by tile row 0 (same interval, same stage count) before this tile
+    // started?  A cluster pair takes the copy only if both CTAs saw it (decided below).
+    tl.bobs = (FT && P.Bsh && ti != 0 && !ghost && ld_acquire_gpu(P.bcnt + tj + (size_t)tt * P.tiles_n) >= (unsigned)x.nk) ? 1u : 0u;
+    tl.bcopy = 0u;
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&tl.mfull[s], 1);
@@ -1122,6 +1224,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (P.cluster2) cluster_sync_all();  // partners' mailbox barriers are initialised
   if (ghost) return;
+  if (FT && P.Bsh) {
+    if (x.tid == 0) {
+      // development / tests: dev mode 512 (with 128, no clusters) waits for tile row 0 to
+      // finish publishing, so every other tile takes the copy path
+      if ((P.dev_mode & 512) && !P.cluster2 && ti != 0) {
+        while (ld_acquire_gpu(P.bcnt + tj + (size_t)tt * P.tiles_n) < (unsigned)x.nk) __nanosleep(1000);
+        tl.bobs = 1u;
+      }
+      tl.bcopy = share ? (tl.bobs & ld_cluster_u32(mapa_u32(smem_u32(&tl.bobs), cluster_rank() ^ 1u))) : tl.bobs;
+    }
+    __syncthreads();
+  }
 
   // The two roles never re-converge, so ptxas can give each its own register budget.
   if (is_cs_warp(x.warp)) {

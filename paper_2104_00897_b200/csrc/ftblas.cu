@@ -309,8 +309,36 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   const size_t base_bytes = al256(cnt_bytes + ev_bytes + f_bytes + 64);
   const size_t hm_bytes = al256(sizeof(unsigned) * (p.tiles_m + p.tiles_n));
   const size_t pre_bytes = prepass ? hm_bytes + sizeof(double) * (size_t)(p.tiles_m + p.tiles_n) * k : 0;
+  // Row-shared fused encode (FUSED with more than one tile column): published e^T A_I, slice
+  // maxima and per-stage flags, one entry per (tile row, global stage).
+  // Tile-column-0 / tile-row-0 publication of e^T A_I / B_J e (encode mode FUSED): the
+  // published sums, the per-stage maxima and flags (A) / stage counts (B).
+  const bool ashare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_n > 1;
+  const bool bshare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_m > 1;
+  const size_t nsg = (size_t)p.nk;  // global stages over the whole k
+  const size_t aflag_bytes = ashare ? al256(sizeof(unsigned) * (size_t)p.tiles_m * nsg) : 0;
+  const size_t ash_bytes = ashare ? 2 * aflag_bytes + al256(sizeof(double) * (size_t)p.tiles_m * (size_t)k) : 0;
+  const size_t bcnt_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * (size_t)T) : 0;
+  const size_t hmb_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * nsg) : 0;
+  const size_t bsh_bytes = bshare ? bcnt_bytes + hmb_bytes + sizeof(double) * (size_t)p.tiles_n * (size_t)k : 0;
   char *scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&scratch, base_bytes + pre_bytes, st));
+  CUDA_TRY(cudaMallocAsync((void **)&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes, st));
+  if (ashare) {
+    char *sb = scratch + base_bytes + pre_bytes;
+    p.aflag = reinterpret_cast<unsigned *>(sb);
+    p.hmA = reinterpret_cast<unsigned *>(sb + aflag_bytes);
+    p.Ash = reinterpret_cast<double *>(sb + 2 * aflag_bytes);
+    p.ldash = p.tiles_m;
+    CUDA_TRY(cudaMemsetAsync(p.aflag, 0, aflag_bytes, st));
+  }
+  if (bshare) {
+    char *sb = scratch + base_bytes + pre_bytes + ash_bytes;
+    p.bcnt = reinterpret_cast<unsigned *>(sb);
+    p.hmB = reinterpret_cast<unsigned *>(sb + bcnt_bytes);
+    p.Bsh = reinterpret_cast<double *>(sb + bcnt_bytes + hmb_bytes);
+    p.ldbsh = p.tiles_n;
+    CUDA_TRY(cudaMemsetAsync(p.bcnt, 0, bcnt_bytes, st));
+  }
   if (prepass) {
     char *pb = scratch + base_bytes;
     auto *hm = reinterpret_cast<unsigned *>(pb);
@@ -1080,7 +1108,7 @@ int ftblas_set_interval(int64_t kc) {
 }
 
 int ftblas_set_encode(int mode) {
-  if (mode != FTBLAS_ENCODE_FUSED && mode != FTBLAS_ENCODE_PREPASS) return 4;
+  if (mode != FTBLAS_ENCODE_FUSED && mode != FTBLAS_ENCODE_PREPASS && mode != FTBLAS_ENCODE_FUSED_LOCAL) return 4;
   tl_encode = mode;
   return 0;
 }

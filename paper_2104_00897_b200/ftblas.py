@@ -314,7 +314,7 @@ def ftblas_set_correction(mode: int):
 
 
 def ftblas_set_encode(mode: int):
-    """ENCODE_FUSED (0, default) or ENCODE_PREPASS (1); thread-local."""
+    """ENCODE_FUSED (0, default), ENCODE_PREPASS (1) or ENCODE_FUSED_LOCAL (2); thread-local."""
     _check("ftblas_set_encode", load().ftblas_set_encode(mode))
 
 
@@ -344,5 +344,6 @@ def ftblas_finalize():
 
 ENCODE_FUSED = 0
 ENCODE_PREPASS = 1
+ENCODE_FUSED_LOCAL = 2
 CORRECT_RECOMPUTE = 0
 CORRECT_SUBTRACT = 1

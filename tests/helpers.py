@@ -2,6 +2,9 @@
 and the comparison of GPU and oracle reports.  No method arithmetic lives here."""
 from __future__ import annotations
 
+import contextlib
+import os
+
 import numpy as np
 
 U = 2.0 ** -53
@@ -64,3 +67,25 @@ def assert_reports_match(gpu, orc, A=None, B=None, ta="N", tb="N", k=None):
             for gv, ov, tau in ((ge[4], oe[4], tr), (ge[5], oe[5], tc)):
                 if np.isfinite(gv) or np.isfinite(ov):
                     assert abs(gv - ov) <= 4 * tau + 8 * U * abs(ov) * k, (ge, oe, tau)
+
+
+@contextlib.contextmanager
+def encode_mode(F, name):
+    """Encode mode of ftblas_dgemm for the duration: "fused" (e^T A_I shared along tile rows,
+    B_J e along tile columns, as scheduled), "fused_copy" (the same, every tile waiting for the
+    published copies: dev modes 256 | 512 | 128), "fused_local" (every CTA encodes itself) or
+    "prepass"."""
+    mode = {"fused": F.ENCODE_FUSED, "fused_copy": F.ENCODE_FUSED, "fused_local": F.ENCODE_FUSED_LOCAL,
+            "prepass": F.ENCODE_PREPASS}[name]
+    old = os.environ.get("FTBLAS_DEV_MODE")
+    if name == "fused_copy":
+        os.environ["FTBLAS_DEV_MODE"] = str(256 | 512 | 128)
+    F.ftblas_set_encode(mode)
+    try:
+        yield
+    finally:
+        F.ftblas_set_encode(F.ENCODE_FUSED)
+        if old is None:
+            os.environ.pop("FTBLAS_DEV_MODE", None)
+        else:
+            os.environ["FTBLAS_DEV_MODE"] = old

@@ -5,23 +5,22 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.helpers import assert_reports_match, bound, events_key, from_dev, op, to_dev
+from tests.helpers import assert_reports_match, bound, encode_mode, events_key, from_dev, op, to_dev
 
 pytestmark = pytest.mark.gpu
 
 F = None
 
 
-@pytest.fixture(scope="module", autouse=True, params=["fused", "prepass"])
+@pytest.fixture(scope="module", autouse=True, params=["fused", "fused_copy", "fused_local", "prepass"])
 def _lib(request):
     global F
     from paper_2104_00897_b200 import ftblas
     ftblas.load()
     F = ftblas
-    F.ftblas_set_encode(F.ENCODE_FUSED if request.param == "fused" else F.ENCODE_PREPASS)
-    yield
+    with encode_mode(F, request.param):
+        yield
     F.ftblas_set_interval(0)
-    F.ftblas_set_encode(F.ENCODE_FUSED)
     F.ftblas_set_correction(F.CORRECT_RECOMPUTE)
 
 

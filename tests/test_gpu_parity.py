@@ -6,25 +6,27 @@ import pytest
 
 import oracle
 import synth
-from tests.helpers import (U, assert_reports_match, bound, events_key, from_dev, op, to_dev)
+from tests.helpers import (U, assert_reports_match, bound, encode_mode, events_key, from_dev, op,
+                           to_dev)
 
 pytestmark = pytest.mark.gpu
 
 F = None
 
 
-@pytest.fixture(scope="module", autouse=True, params=["fused", "prepass"])
+@pytest.fixture(scope="module", autouse=True, params=["fused", "fused_copy", "fused_local", "prepass"])
 def _lib(request):
-    """Every parity test runs under both encode modes of ftblas_dgemm (in-kernel fused encode,
-    and the pre-encoded checksums copied into the staged tiles)."""
+    """Every parity test runs under each encode mode of ftblas_dgemm: in-kernel fused encode
+    with e^T A_I shared along tile rows (as scheduled, and with every tile forced to take the
+    published copy: dev mode 256), every CTA encoding itself, and the pre-encoded checksums
+    copied into the staged tiles."""
     global F
     from paper_2104_00897_b200 import ftblas
     ftblas.load()
     F = ftblas
-    F.ftblas_set_encode(F.ENCODE_FUSED if request.param == "fused" else F.ENCODE_PREPASS)
-    yield
+    with encode_mode(F, request.param):
+        yield
     F.ftblas_set_correction(F.CORRECT_RECOMPUTE)
-    F.ftblas_set_encode(F.ENCODE_FUSED)
 
 
 def geometry():
