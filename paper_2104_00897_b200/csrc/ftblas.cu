@@ -574,25 +574,28 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   const int64_t npan = (m + P - 1) / P;
   const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
 
-  // Column chunks of a panel of pr rows: 2..8 chunks minimising the number of 148-CTA waves
-  // (ties: more chunks, i.e. a shorter pipeline start); one chunk when there is one panel.
+  // Column chunks of a panel of pr rows: uniform chunks of t tile columns (t even, so chunk
+  // edges are multiples of 2 tiles: units intact, 16-byte aligned bases), t chosen to minimise
+  // the panel's total number of 148-CTA waves (at most 16 chunks), ties to the narrowest t, so
+  // that the first chunk of op(B) -- the pipeline's start-up copy -- is as small as the wave
+  // count allows.  One chunk when there is one panel.
   auto chunking = [&](int64_t pr) {
     std::vector<int64_t> best{0, n};
     if (npan < 2) return best;
-    const int64_t tile = ft ? ftk::TN : ftk::BN, trows = (pr + (ft ? ftk::TM : ftk::BM) - 1) / (ft ? ftk::TM : ftk::BM);
-    const int64_t sms = num_sms();
+    const int64_t tw = ft ? ftk::TN : ftk::BN, th = ft ? ftk::TM : ftk::BM;
+    const int64_t trows = (pr + th - 1) / th, tcols = (n + tw - 1) / tw, sms = num_sms();
     int64_t best_waves = INT64_MAX;
-    for (int64_t c = 2; c <= 8; ++c) {
-      const int64_t w = ((n + c - 1) / c + unit2 - 1) / unit2 * unit2;
-      if (w >= n) continue;
-      std::vector<int64_t> e{0};
+    for (int64_t t = 2; t < tcols; t += 2) {
+      const int64_t nch = (tcols + t - 1) / t;
+      if (nch > 16) continue;
       int64_t waves = 0;
-      for (int64_t c0 = 0; c0 < n; c0 += w) {
-        const int64_t cw = std::min(w, n - c0);
-        waves += (trows * ((cw + tile - 1) / tile) + sms - 1) / sms;
-        e.push_back(c0 + cw);
+      std::vector<int64_t> e{0};
+      for (int64_t c0 = 0; c0 < n; c0 += t * tw) {
+        const int64_t c1 = std::min(n, c0 + t * tw);
+        waves += (trows * ((c1 - c0 + tw - 1) / tw) + sms - 1) / sms;
+        e.push_back(c1);
       }
-      if (waves <= best_waves) { best_waves = waves; best = e; }
+      if (waves < best_waves) { best_waves = waves; best = e; }
     }
     return best;
   };
@@ -628,6 +631,17 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   ReportSink sink{reinterpret_cast<unsigned long long *>(rep_base),
                   reinterpret_cast<ftk::EventDev *>(rep_base + 256), ev_cap, 0, 0};
   if (r == 0) fail(cudaMemsetAsync(rep_base, 0, cnt_bytes, st));
+  // development only (FTBLAS_DEV_E2E): stream-event timeline of the pipeline, printed at the end
+  const bool dev_e2e = std::getenv("FTBLAS_DEV_E2E") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> dev_ev;
+  auto mark = [&](const std::string &what, cudaStream_t s) {
+    if (!dev_e2e) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    dev_ev.emplace_back(what, e);
+  };
+  mark("start(st)", st);
   // op(B) columns [c0, c1) -> device (dB keeps the stored layout, leading dimension br).
   auto upload_b = [&](int64_t c0, int64_t c1) {
     if (is_n(tb))
@@ -652,6 +666,7 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
                              cudaMemcpyHostToDevice, sh));
     fail(cudaEventRecord(ev_in[q], sh));
     fail(cudaStreamWaitEvent(st, ev_in[q], 0));
+    mark("A" + std::to_string(pi) + " in(sh)", sh);
     if (r) break;
     const bool first = pi == 0, last = pi == npan - 1;
     const std::vector<int64_t> edges = (first || last) ? chunking(pr) : std::vector<int64_t>{0, n};
@@ -659,6 +674,7 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
       const int64_t c0 = edges[ci], c1 = edges[ci + 1];
       if (first) {  // this chunk of op(B) (all of it when unchunked), then compute on it
         upload_b(c0, c1);
+        mark("B chunk " + std::to_string(ci) + " in(sh)", sh);
         fail(cudaEventRecord(ev_b, sh));
         fail(cudaStreamWaitEvent(st, ev_b, 0));
         if (r) break;
@@ -670,8 +686,10 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
       sink.row_off = r0;
       sink.col_off = c0;
       const double *Bc = is_n(tb) ? dB + c0 * br : dB + c0;
+      mark("p" + std::to_string(pi) + "c" + std::to_string(ci) + " begin(st)", st);
       r = dgemm_core(ft, pf, ta, tb, pr, c1 - c0, k, alpha, dA[q], is_n(ta) ? pr : k, Bc, br, beta, dC[q] + c0 * pr,
                      pr, nullptr, ft ? &sink : nullptr);
+      mark("p" + std::to_string(pi) + "c" + std::to_string(ci) + " end(st)", st);
       if (r) break;
       if (last) {  // return this chunk of the result
         fail(cudaEventRecord(ev_out[q], st));
@@ -689,7 +707,17 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
     }
     fail(cudaEventRecord(ev_free[q], sd));
   }
+  mark("last D2H(sd)", sd);
   fail(cudaStreamSynchronize(sd));
+  if (dev_e2e) {
+    cudaDeviceSynchronize();
+    for (auto &pe : dev_ev) {
+      float ms = 0.f;
+      const cudaError_t ee = cudaEventElapsedTime(&ms, dev_ev[0].second, pe.second);
+      std::fprintf(stderr, "[e2e] %8.2f ms  %s%s\n", ms, pe.first.c_str(), ee == cudaSuccess ? "" : cudaGetErrorString(ee));
+    }
+    for (auto &pe : dev_ev) cudaEventDestroy(pe.second);
+  }
   fail(cudaStreamSynchronize(sh));
   fail(cudaStreamSynchronize(st));
   if (r == 0 && err && ft) r = finish_report(err, sink.counters, sink.events, ev_cap, sink.units, st);
