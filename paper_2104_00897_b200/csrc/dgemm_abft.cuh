@@ -741,6 +741,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         }
       }
       ready = __shfl_sync(0xffffffffu, ready, 0);
+      __syncwarp();  // orders the other lanes' loads after lane 0's acquire
       if (ready) {
         const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
         const int64_t pg = x.k0 + (int64_t)s * BK + p;

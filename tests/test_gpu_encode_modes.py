@@ -41,3 +41,27 @@ def test_row_shared_encode_bitwise_equals_local(trans):
         assert (r.units_checked, r.detected, r.corrected, r.recomputed) == \
             (r_ref.units_checked, r_ref.detected, r_ref.corrected, r_ref.recomputed)
         assert [tuple(e) for e in r.events] == [tuple(e) for e in r_ref.events], name
+
+
+def test_row_shared_encode_multi_wave_bitwise():
+    """Several waves of tiles: later waves find e^T A_I / B_J e published by earlier tiles and copy
+    them, the first wave races its producers; either way the result is bitwise the local encode."""
+    from paper_2104_00897_b200 import ftblas as F
+    F.load()
+    rng = np.random.default_rng(990)
+    m, n, k = 3000, 2600, 200  # 24 x 21 tiles: 3.4 waves of 148 CTAs
+    A, B = rng.uniform(-1, 1, (m, k)), rng.standard_normal((k, n))
+    faults = [(int(i), int(j), int(s), float(d)) for i, j, s, d in
+              zip(rng.integers(0, m, 12), rng.integers(0, n, 12), rng.integers(0, k, 12), rng.uniform(1, 9, 12))]
+    out = {}
+    for name in ("fused_local", "fused"):
+        with encode_mode(F, name):
+            dC = to_dev(np.zeros((m, n)))
+            F.ftblas_inject_arm(faults)
+            rep = F.ftblas_dgemm("N", "N", m, n, k, 1.0, to_dev(A), m, to_dev(B), k, 0.0, dC, m)
+            out[name] = (from_dev(dC, m, n), rep)
+    (C0, r0), (C1, r1) = out["fused_local"], out["fused"]
+    assert np.array_equal(C0.view(np.int64), C1.view(np.int64))
+    assert r0.detected == r1.detected >= 11 and r0.corrected == r1.corrected
+    assert [tuple(e) for e in r0.events] == [tuple(e) for e in r1.events]
+    assert np.allclose(C1, A @ B, rtol=0, atol=4 * k * 2.0 ** -53 * (np.abs(A) @ np.abs(B)).max())
