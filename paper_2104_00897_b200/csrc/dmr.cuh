@@ -152,6 +152,127 @@ __global__ void __launch_bounds__(256, resident_ctas(DMR)) daxpy_kernel(int64_t 
   }
 }
 
+// ---------------------------------------------------------------- unit-stride fast paths
+// x (and y) contiguous and 16-byte aligned: every thread owns VU 16-byte pairs of one block's
+// 2 VU * 256-element chunk (pair u at u * 256 + threadIdx.x: one LDG.128 per pair, a warp reads
+// 512 contiguous bytes), all loads issued before any FP64 work; one chunk per CTA, so the
+// hardware overlaps the tail of a block with the next block's loads (no loop-carried
+// dependence through a grid-stride loop).  Same DMR arithmetic and fault hook per element.
+constexpr int VU = 4;                   // 16-byte pairs per thread
+constexpr int VCHUNK = 2 * VU * 256;    // elements per CTA
+
+template <bool DMR, bool FLT>
+__device__ __forceinline__ double dmr_scal1(double alpha, double xv, int64_t i, const DmrFault *f, int nf, bool &bad) {
+  double r = v_mul(alpha, xv);
+  if (DMR) {
+    if (FLT) { const double d = fault_delta(f, nf, i, 0); if (d != 0.0) r = v_add(r, d); }
+    bad |= differ(r, v_mul(alpha, xv));  // the duplicate
+  }
+  return r;
+}
+template <bool DMR, bool FLT>
+__device__ __forceinline__ double dmr_axpy1(double alpha, double xv, double yv, int64_t i, const DmrFault *f, int nf,
+                                            bool &bad) {
+  double r = v_fma(alpha, xv, yv);
+  if (DMR) {
+    if (FLT) { const double d = fault_delta(f, nf, i, 0); if (d != 0.0) r = v_add(r, d); }
+    bad |= differ(r, v_fma(alpha, xv, yv));  // the duplicate
+  }
+  return r;
+}
+
+template <bool DMR, bool FLT>
+__global__ void __launch_bounds__(256) dscal_vec_kernel(int64_t n, double alpha, double *__restrict__ x,
+                                                        const DmrFault *__restrict__ f, int nf,
+                                                        unsigned long long *__restrict__ cnt) {
+  const int64_t c0 = (int64_t)blockIdx.x * VCHUNK;
+  double2 *x2 = reinterpret_cast<double2 *>(x + c0);
+  const bool full = c0 + VCHUNK <= n;
+  double2 xv[VU];
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int64_t i = c0 + 2 * (u * 256 + threadIdx.x);
+    if (full) xv[u] = x2[u * 256 + threadIdx.x];
+    else xv[u] = make_double2(i < n ? x[i] : 0.0, i + 1 < n ? x[i + 1] : 0.0);
+  }
+  double2 r[VU];
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int64_t i = c0 + 2 * (u * 256 + threadIdx.x);
+    r[u].x = dmr_scal1<DMR, FLT>(alpha, xv[u].x, i, f, nf, bad);
+    r[u].y = dmr_scal1<DMR, FLT>(alpha, xv[u].y, i + 1, f, nf, bad);
+  }
+  if (DMR && __any_sync(0xffffffffu, bad)) {  // rare: redo the duplicate, settle by a third
+#pragma unroll
+    for (int u = 0; u < VU; ++u) {
+      double r2 = v_mul(alpha, xv[u].x);
+      if (differ(r[u].x, r2)) r[u].x = settle(r[u].x, r2, v_mul(alpha, xv[u].x), cnt);
+      r2 = v_mul(alpha, xv[u].y);
+      if (differ(r[u].y, r2)) r[u].y = settle(r[u].y, r2, v_mul(alpha, xv[u].y), cnt);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int64_t i = c0 + 2 * (u * 256 + threadIdx.x);
+    if (full) {
+      x2[u * 256 + threadIdx.x] = r[u];
+    } else {
+      if (i < n) x[i] = r[u].x;
+      if (i + 1 < n) x[i + 1] = r[u].y;
+    }
+  }
+}
+
+template <bool DMR, bool FLT>
+__global__ void __launch_bounds__(256) daxpy_vec_kernel(int64_t n, double alpha, const double *__restrict__ x,
+                                                        double *__restrict__ y, const DmrFault *__restrict__ f, int nf,
+                                                        unsigned long long *__restrict__ cnt) {
+  const int64_t c0 = (int64_t)blockIdx.x * VCHUNK;
+  const double2 *x2 = reinterpret_cast<const double2 *>(x + c0);
+  double2 *y2 = reinterpret_cast<double2 *>(y + c0);
+  const bool full = c0 + VCHUNK <= n;
+  double2 xv[VU], yv[VU];
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int64_t i = c0 + 2 * (u * 256 + threadIdx.x);
+    if (full) {
+      xv[u] = x2[u * 256 + threadIdx.x];
+      yv[u] = y2[u * 256 + threadIdx.x];
+    } else {
+      xv[u] = make_double2(i < n ? x[i] : 0.0, i + 1 < n ? x[i + 1] : 0.0);
+      yv[u] = make_double2(i < n ? y[i] : 0.0, i + 1 < n ? y[i + 1] : 0.0);
+    }
+  }
+  double2 r[VU];
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int64_t i = c0 + 2 * (u * 256 + threadIdx.x);
+    r[u].x = dmr_axpy1<DMR, FLT>(alpha, xv[u].x, yv[u].x, i, f, nf, bad);
+    r[u].y = dmr_axpy1<DMR, FLT>(alpha, xv[u].y, yv[u].y, i + 1, f, nf, bad);
+  }
+  if (DMR && __any_sync(0xffffffffu, bad)) {
+#pragma unroll
+    for (int u = 0; u < VU; ++u) {
+      double r2 = v_fma(alpha, xv[u].x, yv[u].x);
+      if (differ(r[u].x, r2)) r[u].x = settle(r[u].x, r2, v_fma(alpha, xv[u].x, yv[u].x), cnt);
+      r2 = v_fma(alpha, xv[u].y, yv[u].y);
+      if (differ(r[u].y, r2)) r[u].y = settle(r[u].y, r2, v_fma(alpha, xv[u].y, yv[u].y), cnt);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int64_t i = c0 + 2 * (u * 256 + threadIdx.x);
+    if (full) {
+      y2[u * 256 + threadIdx.x] = r[u];
+    } else {
+      if (i < n) y[i] = r[u].x;
+      if (i + 1 < n) y[i + 1] = r[u].y;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- DGEMV
 // 'N': y_i = alpha sum_j A_ij x_j + beta y_i.  A CTA of GN_W = 16 warps owns 32 rows (one
 // per lane); warp w accumulates the columns j = w (mod 16) (coalesced 256-byte column
@@ -266,6 +387,29 @@ __device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, i
   }
   double a1 = 0.0, a2 = 0.0;
   int64_t i = lane;
+  if (!FLT && P.incx == 1 && ((reinterpret_cast<uintptr_t>(Aj) | reinterpret_cast<uintptr_t>(P.x)) & 15) == 0) {
+    // Unit-stride, 16-byte aligned column and x: 8 LDG.128 of A (and of x) in flight per lane,
+    // 512 elements per warp step; the remainder below continues from the first unread element.
+    int64_t b = 0;
+    for (; b + 512 <= P.m; b += 512) {
+      double2 av[8], xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        av[u] = *reinterpret_cast<const double2 *>(Aj + b + 64 * u + 2 * lane);
+        xv[u] = *reinterpret_cast<const double2 *>(P.x + b + 64 * u + 2 * lane);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a1 = v_fma(av[u].x, xv[u].x, a1);
+        a1 = v_fma(av[u].y, xv[u].y, a1);
+        if (DMR) {
+          a2 = v_fma(av[u].x, xv[u].x, a2);
+          a2 = v_fma(av[u].y, xv[u].y, a2);
+        }
+      }
+    }
+    i = b + lane;
+  }
   for (; i + 96 < P.m; i += 128) {
     double av[4], xv[4];
 #pragma unroll
@@ -305,8 +449,9 @@ __device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, i
   if (lane == 0) *yj = r1;
 }
 
+constexpr int GT_CTAS = 4;  // resident 256-thread CTAs per SM of dgemv_t (64 registers: 16 loads in flight)
 template <bool DMR, bool FLT>
-__global__ void __launch_bounds__(256, resident_ctas(DMR)) dgemv_t_kernel(const GemvParams P) {
+__global__ void __launch_bounds__(256, GT_CTAS) dgemv_t_kernel(const GemvParams P) {
   const int lane = threadIdx.x & 31;
   for (int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); j < P.n; j += (int64_t)gridDim.x * 8)
     dgemv_t_column<DMR, FLT>(P, j, lane);

@@ -790,6 +790,7 @@ int num_sms() {
   }
   return sms;
 }
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 int l1_grid(int64_t n, bool dmr) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, (int64_t)num_sms() * ftd::resident_ctas(dmr)));
 }
@@ -805,7 +806,12 @@ int dscal_impl(bool ft, int64_t n, double alpha, double *x, int64_t incx, ftblas
   cudaStream_t st = tl_stream;
   DmrScratch sc;
   if (int e = dmr_prepare(ft, faults, n, 0, sc, st)) return e;
-  if (ft && sc.nf) ftd::dscal_kernel<true, true><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, sc.f, sc.nf, sc.cnt);
+  if (incx == 1 && aligned16(x)) {  // unit stride: one 16-byte-vectorised chunk per CTA
+    const unsigned g = (unsigned)((n + ftd::VCHUNK - 1) / ftd::VCHUNK);
+    if (ft && sc.nf) ftd::dscal_vec_kernel<true, true><<<g, 256, 0, st>>>(n, alpha, x, sc.f, sc.nf, sc.cnt);
+    else if (ft) ftd::dscal_vec_kernel<true, false><<<g, 256, 0, st>>>(n, alpha, x, nullptr, 0, sc.cnt);
+    else ftd::dscal_vec_kernel<false, false><<<g, 256, 0, st>>>(n, alpha, x, nullptr, 0, sc.cnt);
+  } else if (ft && sc.nf) ftd::dscal_kernel<true, true><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, sc.f, sc.nf, sc.cnt);
   else if (ft) ftd::dscal_kernel<true, false><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, nullptr, 0, sc.cnt);
   else ftd::dscal_kernel<false, false><<<l1_grid(n, false), 256, 0, st>>>(n, alpha, x, incx, nullptr, 0, sc.cnt);
   ++tl_launches;
@@ -826,7 +832,12 @@ int daxpy_impl(bool ft, int64_t n, double alpha, const double *x, int64_t incx, 
   cudaStream_t st = tl_stream;
   DmrScratch sc;
   if (int e = dmr_prepare(ft, faults, n, 0, sc, st)) return e;
-  if (ft && sc.nf) ftd::daxpy_kernel<true, true><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, y, incy, sc.f, sc.nf, sc.cnt);
+  if (incx == 1 && incy == 1 && aligned16(x) && aligned16(y)) {  // unit stride: vectorised chunks
+    const unsigned g = (unsigned)((n + ftd::VCHUNK - 1) / ftd::VCHUNK);
+    if (ft && sc.nf) ftd::daxpy_vec_kernel<true, true><<<g, 256, 0, st>>>(n, alpha, x, y, sc.f, sc.nf, sc.cnt);
+    else if (ft) ftd::daxpy_vec_kernel<true, false><<<g, 256, 0, st>>>(n, alpha, x, y, nullptr, 0, sc.cnt);
+    else ftd::daxpy_vec_kernel<false, false><<<g, 256, 0, st>>>(n, alpha, x, y, nullptr, 0, sc.cnt);
+  } else if (ft && sc.nf) ftd::daxpy_kernel<true, true><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, y, incy, sc.f, sc.nf, sc.cnt);
   else if (ft) ftd::daxpy_kernel<true, false><<<l1_grid(n, true), 256, 0, st>>>(n, alpha, x, incx, y, incy, nullptr, 0, sc.cnt);
   else ftd::daxpy_kernel<false, false><<<l1_grid(n, false), 256, 0, st>>>(n, alpha, x, incx, y, incy, nullptr, 0, sc.cnt);
   ++tl_launches;
@@ -863,7 +874,7 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
     else if (ft) ftd::dgemv_n_kernel<true, false><<<g, ftd::GN_W * 32, 0, st>>>(P);
     else ftd::dgemv_n_kernel<false, false><<<g, ftd::GN_W * 32, 0, st>>>(P);
   } else {
-    const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * ftd::resident_ctas(ft));
+    const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * ftd::GT_CTAS);
     if (ft && sc.nf) ftd::dgemv_t_kernel<true, true><<<g, 256, 0, st>>>(P);
     else if (ft) ftd::dgemv_t_kernel<true, false><<<g, 256, 0, st>>>(P);
     else ftd::dgemv_t_kernel<false, false><<<g, 256, 0, st>>>(P);

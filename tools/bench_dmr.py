@@ -1,5 +1,6 @@
 """DMR Level-1/2 benchmark: achieved HBM bandwidth of the protected
-routines and their unprotected twins, DMR overhead %, with and without injected faults.
+routines and their unprotected twins, DMR overhead %, with and without injected faults, and
+the same operation through torch (cuBLAS / torch elementwise kernels) as a measuring stick.
 CUDA events on the launch stream, best of R after warm-up; inputs larger than L2.
 Prints one JSON object per routine."""
 import json
@@ -30,9 +31,10 @@ def timed(fn):
     return best
 
 
-def line(name, nbytes, t_ft, t_noft, t_inj, rep):
+def line(name, nbytes, t_ft, t_noft, t_inj, rep, t_torch):
     print(json.dumps({"routine": name, "bytes": nbytes, "ms_dmr": t_ft, "ms_noft": t_noft, "ms_dmr_faults": t_inj,
                       "gbs_dmr": nbytes / t_ft / 1e6, "gbs_noft": nbytes / t_noft / 1e6,
+                      "gbs_torch": nbytes / t_torch / 1e6,
                       "frac_hbm_dmr": nbytes / t_ft / 1e6 / PEAK, "overhead_pct": 100 * (t_ft - t_noft) / t_noft,
                       "faults_report": rep.__dict__ if rep else None}), flush=True)
 
@@ -53,12 +55,12 @@ def main():
     t0 = timed(lambda: F.ftblas_dscal_noft(n, 1.0000001, x, 1))
     ti = timed(inj(lambda: F.ftblas_dscal(n, 1.0000001, x, 1, report=False)))
     F.ftblas_inject_arm(faults)
-    line("dscal", 16 * n, t1, t0, ti, F.ftblas_dscal(n, 1.0, x, 1))
+    line("dscal", 16 * n, t1, t0, ti, F.ftblas_dscal(n, 1.0, x, 1), timed(lambda: x.mul_(1.0000001)))
     t1 = timed(lambda: F.ftblas_daxpy(n, 1e-9, x, 1, y, 1, report=False))
     t0 = timed(lambda: F.ftblas_daxpy_noft(n, 1e-9, x, 1, y, 1))
     ti = timed(inj(lambda: F.ftblas_daxpy(n, 1e-9, x, 1, y, 1, report=False)))
     F.ftblas_inject_arm(faults)
-    line("daxpy", 24 * n, t1, t0, ti, F.ftblas_daxpy(n, 0.0, x, 1, y, 1))
+    line("daxpy", 24 * n, t1, t0, ti, F.ftblas_daxpy(n, 0.0, x, 1, y, 1), timed(lambda: y.add_(x, alpha=1e-9)))
     del x, y
     m = k = 16384
     A = torch.rand(m * k, dtype=torch.float64, device="cuda", generator=g)
@@ -76,8 +78,12 @@ def main():
             call()
         ti = timed(ci)
         F.ftblas_inject_arm(gf)
+        Am = A.view(k, m).t()  # the column-major m x k matrix as a torch view
+        op = Am if tr == "N" else Am.t()
+        xin, yout = (v[:k], w[:m]) if tr == "N" else (v[:m], w[:k])
+        t_t = timed(lambda: torch.addmv(yout, op, xin, beta=0.5, alpha=1.0, out=yout))
         line(f"dgemv_{tr}", 8 * (m * k + 2 * m + k), t1, t0, ti,
-             F.ftblas_dgemv(tr, m, k, 1.0, A, m, v, 1, 0.5, w, 1))
+             F.ftblas_dgemv(tr, m, k, 1.0, A, m, v, 1, 0.5, w, 1), t_t)
 
 
 if __name__ == "__main__":
