@@ -507,18 +507,6 @@ __device__ __forceinline__ double2 enc_ld_h(const double *s, int lane, int hsel,
   return v;
 }
 
-template <bool KM>
-__device__ __forceinline__ float enc_pass1_h(const double *s, int lane, int hsel, int cr) {
-  float m0 = 0.f, m1 = 0.f;
-#pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    const double2 v = enc_ld_h<KM>(s, lane, hsel, j, cr), w = enc_ld_h<KM>(s, lane, hsel, j + 1, cr);
-    m0 = fmax3_abs_nan(m0, hi_f(v.x), hi_f(v.y));
-    m1 = fmax3_abs_nan(m1, hi_f(w.x), hi_f(w.y));
-  }
-  return fmax_nan(m0, m1);
-}
-
 template <bool KM, bool EXACT>
 __device__ __forceinline__ void enc_pass2_h(const double *s, int lane, int hsel, int cr, uint32_t C, long long &q0,
                                             long long &q1) {
@@ -554,18 +542,6 @@ __device__ __forceinline__ void enc_pass2_h(const double *s, int lane, int hsel,
   q1 = a1;
 }
 
-// Exact max |high word| of a half slice (rare path).
-template <bool KM>
-__device__ __noinline__ uint32_t enc_exact_hmax_h(const double *s, int lane, int hsel, int cr) {
-  uint32_t hm = 0;
-  for (int j = 0; j < 16; ++j) {
-    const double2 v = enc_ld_h<KM>(s, lane, hsel, j, cr);
-    hm = max(hm, max((uint32_t)__double2hiint(v.x) & 0x7FFFFFFFu, (uint32_t)__double2hiint(v.y) & 0x7FFFFFFFu));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-  return hm;
-}
 template <bool KM>
 __device__ __noinline__ void enc_pass2_h_exact(const double *s, int lane, int hsel, int cr, uint32_t C, long long &q0,
                                                long long &q1) {
@@ -574,11 +550,14 @@ __device__ __noinline__ void enc_pass2_h_exact(const double *s, int lane, int hs
 
 // Encode the half slice hsel: sum0 (sum1) = e^T X for this lane's k-slot(s) (valid in the
 // lanes q == 0 / g == 0); hm_half returns the half's R1' high-word maximum.
+// The fixed-point scale comes from the maximum of the WHOLE slice (both halves: pass 1 is
+// cheap), so each k-slot's sum is bitwise the one a single CTA encoding the whole slice forms
+// (the sum of exact fixed-point terms at a common scale does not depend on who adds them).
 template <bool KM>
 __device__ __forceinline__ void enc_operand_h(const double *s, int lane, int hsel, int cr, double &sum0, double &sum1,
                                               uint32_t &hm_half) {
-  uint32_t hm = (uint32_t)__float_as_int(warp_max_nan(enc_pass1_h<KM>(s, lane, hsel, cr)));
-  if (hm >= 0x7F800000u) hm = enc_exact_hmax_h<KM>(s, lane, hsel, cr);
+  uint32_t hm = (uint32_t)__float_as_int(warp_max_nan(enc_pass1<KM>(s, lane, cr)));
+  if (hm >= 0x7F800000u) hm = enc_exact_hmax<KM>(s, lane, cr);
   hm_half = min(hm, 0x7FEFFFFFu);
   const uint32_t c = hm >> 20;
   if (c >= 2047u) {
@@ -722,43 +701,55 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     }
   };
   const uint32_t rank = P.cluster2 ? cluster_rank() : 0u;
-  // e^T A_I of stage s into (a0, a1) (layout of enc_operand); the slice maximum folds into
-  // amax_hi.  Row-shared mode: tile column 0 encodes and publishes, the others copy a published
-  // stage or, if it is not out yet, encode it themselves.
+  // e^T A_I of stage s: tile column 0 encodes it and publishes it; another tile copies the
+  // published stage if its flag is already set and otherwise encodes the stage itself.  The
+  // flag and the published sums are fetched before the stage's TMA bytes are waited for, so
+  // the L2 round trips overlap the TMA latency.
   const bool a_pub = P.Ash && x.tj == 0, a_sub = P.Ash && x.tj != 0;
   const bool b_pub = P.Bsh && x.ti == 0;
-  auto enc_a = [&](double *sA, int s, double &a0, double &a1, uint32_t &amax) {
+  struct PubA { bool ok; double a0, a1; uint32_t am; };
+  auto fetch_a = [&](int s) {
+    PubA f{false, 0.0, 0.0, 0u};
+    if (!a_sub) return f;
     const int64_t sg = x.k0 / BK + s;  // global stage index
     const size_t fi = (size_t)x.ti + (size_t)sg * P.tiles_m;
-    if (a_sub) {
-      unsigned ready = 0;
-      if (lane == 0) {
+    unsigned ready = 0;
+    if (lane == 0) {
+      ready = ld_acquire_gpu(P.aflag + fi);
+      // development / tests: dev mode 256 waits for the publication (exercises the copy path)
+      while ((P.dev_mode & 256) && !ready) {
+        __nanosleep(256);
         ready = ld_acquire_gpu(P.aflag + fi);
-        // development / tests: dev mode 256 waits for the publication (exercises the copy path)
-        while ((P.dev_mode & 256) && !ready) {
-          __nanosleep(256);
-          ready = ld_acquire_gpu(P.aflag + fi);
-        }
       }
-      ready = __shfl_sync(0xffffffffu, ready, 0);
-      __syncwarp();  // orders the other lanes' loads after lane 0's acquire
-      if (ready) {
-        const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
-        const int64_t pg = x.k0 + (int64_t)s * BK + p;
-        if (AKM) {
-          a0 = lane < 8 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
-          a1 = lane < 8 && pg + 1 < x.k1 ? __ldcg(P.Ash + x.ti + (pg + 1) * P.ldash) : 0.0;
-        } else {
-          a0 = lane < 16 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
-        }
-        amax = max(amax, __ldcg(P.hmA + fi));
-        return;
+    }
+    f.ok = __shfl_sync(0xffffffffu, ready, 0) != 0;
+    __syncwarp();  // orders the other lanes' loads after lane 0's acquire
+    if (f.ok) {
+      const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
+      const int64_t pg = x.k0 + (int64_t)s * BK + p;
+      if (AKM) {
+        f.a0 = lane < 8 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
+        f.a1 = lane < 8 && pg + 1 < x.k1 ? __ldcg(P.Ash + x.ti + (pg + 1) * P.ldash) : 0.0;
+      } else {
+        f.a0 = lane < 16 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
       }
+      f.am = __ldcg(P.hmA + fi);
+    }
+    return f;
+  };
+  auto enc_a = [&](double *sA, int s, const PubA &f, double &a0, double &a1, uint32_t &amax) {
+    if (f.ok) {
+      a0 = f.a0;
+      a1 = f.a1;
+      amax = max(amax, f.am);
+      return;
     }
     uint32_t hm = 0u;
     enc_operand<AKM>(sA, lane, x.cra, a0, a1, hm);
     amax = max(amax, hm);
     if (a_pub) {
+      const int64_t sg = x.k0 / BK + s;
+      const size_t fi = (size_t)x.ti + (size_t)sg * P.tiles_m;
       const int p = AKM ? 2 * lane : lane;
       const int64_t pg = x.k0 + (int64_t)s * BK + p;
       if (AKM) {
@@ -784,6 +775,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
+        const PubA pa = (P.Ac || (P.dev_mode & 3)) ? PubA{false, 0.0, 0.0, 0u} : fetch_a(s);
         if (!(P.dev_mode & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
@@ -799,7 +791,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         } else if ((P.dev_mode & 2) && !share && !bcopy) {
           // development: no encode (checksum rows zero)
         } else {
-          enc_a(sA, s, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
+          enc_a(sA, s, pa, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           if (AKM) {
             if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
           } else {
@@ -1090,6 +1082,14 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         }
     }
     bar_sync(BAR_CTILE, 256);
+#ifdef FTBLAS_DEV_TIMELINE
+    if (!verify && attempt == 0 && vt == 0 && P.dev_prof) {
+      unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + 4) * 2;
+      dp[0] = (unsigned long long)(tl_b - tl_a);
+      dp[1] = (unsigned long long)(clock64() - tl_b);
+      dp[2] = 0ull;
+    }
+#endif
     if (!verify) break;
 
     // ---- verification, out of line so that its register needs do not shape
@@ -1142,12 +1142,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // Grouped raster: CTAs run in bands of RASTER_G tile rows, column by column inside a band,
   // so that one wave of 148 CTAs touches ~12 A row panels and ~12 B column panels (L2 reuse)
   // instead of 148 A panels and one B panel.
+  // With checksums shared through L2 (R22) the publishing tiles come first: tile row 0 (B_J e)
+  // and tile column 0 (e^T A_I) in the first waves, then the rest of the grid in grouped
+  // raster, so nearly every other tile finds both checksums published when it runs.
   auto map_tile = [&](int Lg, int &ti_, int &tj_, int &t_) {
-    const int L = Lg % P.ntiles, band_tiles = RASTER_G * P.tiles_n, band = L / band_tiles;
-    const int within = L - band * band_tiles, rows = min(RASTER_G, P.tiles_m - band * RASTER_G);
-    ti_ = band * RASTER_G + within % rows;
-    tj_ = within / rows;
+    int L = Lg % P.ntiles;
     t_ = P.t_base + Lg / P.ntiles;
+    int r0 = 0, c0 = 0;
+    if (FT && P.Ash && P.Bsh) {
+      if (L < P.tiles_n) { ti_ = 0; tj_ = L; return; }
+      L -= P.tiles_n;
+      if (L < P.tiles_m - 1) { ti_ = 1 + L; tj_ = 0; return; }
+      L -= P.tiles_m - 1;
+      r0 = c0 = 1;
+    }
+    const int tm = P.tiles_m - r0, tn = P.tiles_n - c0;
+    const int band_tiles = RASTER_G * tn, band = L / band_tiles;
+    const int within = L - band * band_tiles, rows = min(RASTER_G, tm - band * RASTER_G);
+    ti_ = r0 + band * RASTER_G + within % rows;
+    tj_ = c0 + within / rows;
   };
   const int Lg = (int)blockIdx.x;
   const bool ghost = P.cluster2 && Lg >= P.total;  // pads an odd grid to whole clusters
