@@ -174,14 +174,27 @@ std::vector<ftblas_fault_t> take_armed() {
 // (interval, i, j)).  Synchronises the stream.
 int finish_report(ftblas_err_report_t *err, const unsigned long long *d_counters, const void *d_events,
                   int64_t ev_cap, int64_t units_checked, cudaStream_t st) {
-  unsigned long long cnt[ftk::CNT_N];
-  CUDA_TRY(cudaMemcpyAsync(cnt, d_counters, sizeof cnt, cudaMemcpyDeviceToHost, st));
+  // One device->host copy for the counters and (when they follow the counters closely) the
+  // first E0 events; a second one only when more events were recorded.
+  constexpr int64_t E0 = 32;
+  const ptrdiff_t gap = reinterpret_cast<const char *>(d_events) - reinterpret_cast<const char *>(d_counters);
+  const bool joint = gap >= (ptrdiff_t)(sizeof(unsigned long long) * ftk::CNT_N) && gap <= 256;
+  const int64_t e0 = joint ? std::min<int64_t>(E0, ev_cap) : 0;
+  std::vector<char> head((size_t)(joint ? gap : 0) + sizeof(ftk::EventDev) * (size_t)e0 + sizeof(unsigned long long) * ftk::CNT_N);
+  CUDA_TRY(cudaMemcpyAsync(head.data(), d_counters, joint ? (size_t)gap + sizeof(ftk::EventDev) * (size_t)e0
+                                                          : sizeof(unsigned long long) * ftk::CNT_N,
+                           cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  unsigned long long cnt[ftk::CNT_N];
+  std::memcpy(cnt, head.data(), sizeof cnt);
   const int64_t nev = (int64_t)cnt[ftk::CNT_EVENTS];
   const int64_t nstore = std::min<int64_t>(nev, ev_cap);
   std::vector<ftk::EventDev> ev((size_t)nstore);
-  if (nstore > 0) {
-    CUDA_TRY(cudaMemcpyAsync(ev.data(), d_events, sizeof(ftk::EventDev) * nstore, cudaMemcpyDeviceToHost, st));
+  const int64_t have = std::min<int64_t>(nstore, e0);
+  if (have > 0) std::memcpy(ev.data(), head.data() + gap, sizeof(ftk::EventDev) * (size_t)have);
+  if (nstore > have) {
+    CUDA_TRY(cudaMemcpyAsync(ev.data() + have, reinterpret_cast<const ftk::EventDev *>(d_events) + have,
+                             sizeof(ftk::EventDev) * (size_t)(nstore - have), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
   }
   std::sort(ev.begin(), ev.end(), [](const ftk::EventDev &a, const ftk::EventDev &b) {
@@ -300,45 +313,47 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   });
 
   const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
-  const size_t cnt_bytes = sizeof(unsigned long long) * ftk::CNT_N;
+  static_assert(sizeof(unsigned long long) * ftk::CNT_N <= 64, "counters fit their 64-byte slot");
   const size_t ev_bytes = sizeof(ftk::EventDev) * (size_t)ev_cap;
   const size_t f_bytes = sizeof(ftk::FaultDev) * fd.size();
   // Encode mode PREPASS: e^T A_I, B_J e and the block maxima from two memory passes.
   const bool prepass = ft && tl_encode == FTBLAS_ENCODE_PREPASS;
   auto al256 = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t base_bytes = al256(cnt_bytes + ev_bytes + f_bytes + 64);
-  const size_t hm_bytes = al256(sizeof(unsigned) * (p.tiles_m + p.tiles_n));
-  const size_t pre_bytes = prepass ? hm_bytes + sizeof(double) * (size_t)(p.tiles_m + p.tiles_n) * k : 0;
-  // Row-shared fused encode (FUSED with more than one tile column): published e^T A_I, slice
-  // maxima and per-stage flags, one entry per (tile row, global stage).
-  // Tile-column-0 / tile-row-0 publication of e^T A_I / B_J e (encode mode FUSED): the
-  // published sums, the per-stage maxima and flags (A) / stage counts (B).
+  // Tile-column-0 / tile-row-0 publication of e^T A_I / B_J e (encode mode FUSED): per-stage
+  // flags (A) / per-interval stage counts (B), the slice maxima and the published sums.
   const bool ashare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_n > 1;
   const bool bshare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_m > 1;
   const size_t nsg = (size_t)p.nk;  // global stages over the whole k
   const size_t aflag_bytes = ashare ? al256(sizeof(unsigned) * (size_t)p.tiles_m * nsg) : 0;
-  const size_t ash_bytes = ashare ? 2 * aflag_bytes + al256(sizeof(double) * (size_t)p.tiles_m * (size_t)k) : 0;
   const size_t bcnt_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * (size_t)T) : 0;
+  // Scratch: [aflag | bcnt | counters (64 B) | events | faults] ... the first three zeroed by one
+  // memset, counters and the first events read back by one copy (finish_report).
+  const size_t zero_bytes = aflag_bytes + bcnt_bytes + 64;
+  const size_t base_bytes = al256(zero_bytes + ev_bytes + f_bytes);
+  const size_t hm_bytes = al256(sizeof(unsigned) * (p.tiles_m + p.tiles_n));
+  const size_t pre_bytes = prepass ? hm_bytes + sizeof(double) * (size_t)(p.tiles_m + p.tiles_n) * k : 0;
+  const size_t hma_bytes = ashare ? aflag_bytes : 0;
+  const size_t ash_bytes = ashare ? hma_bytes + al256(sizeof(double) * (size_t)p.tiles_m * (size_t)k) : 0;
   const size_t hmb_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * nsg) : 0;
-  const size_t bsh_bytes = bshare ? bcnt_bytes + hmb_bytes + sizeof(double) * (size_t)p.tiles_n * (size_t)k : 0;
+  const size_t bsh_bytes = bshare ? hmb_bytes + sizeof(double) * (size_t)p.tiles_n * (size_t)k : 0;
   char *scratch = nullptr;
   CUDA_TRY(cudaMallocAsync((void **)&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes, st));
+  char *const cnt_ptr = scratch + aflag_bytes + bcnt_bytes;
   if (ashare) {
     char *sb = scratch + base_bytes + pre_bytes;
-    p.aflag = reinterpret_cast<unsigned *>(sb);
-    p.hmA = reinterpret_cast<unsigned *>(sb + aflag_bytes);
-    p.Ash = reinterpret_cast<double *>(sb + 2 * aflag_bytes);
+    p.aflag = reinterpret_cast<unsigned *>(scratch);
+    p.hmA = reinterpret_cast<unsigned *>(sb);
+    p.Ash = reinterpret_cast<double *>(sb + hma_bytes);
     p.ldash = p.tiles_m;
-    CUDA_TRY(cudaMemsetAsync(p.aflag, 0, aflag_bytes, st));
   }
   if (bshare) {
     char *sb = scratch + base_bytes + pre_bytes + ash_bytes;
-    p.bcnt = reinterpret_cast<unsigned *>(sb);
-    p.hmB = reinterpret_cast<unsigned *>(sb + bcnt_bytes);
-    p.Bsh = reinterpret_cast<double *>(sb + bcnt_bytes + hmb_bytes);
+    p.bcnt = reinterpret_cast<unsigned *>(scratch + aflag_bytes);
+    p.hmB = reinterpret_cast<unsigned *>(sb);
+    p.Bsh = reinterpret_cast<double *>(sb + hmb_bytes);
     p.ldbsh = p.tiles_n;
-    CUDA_TRY(cudaMemsetAsync(p.bcnt, 0, bcnt_bytes, st));
   }
+  CUDA_TRY(cudaMemsetAsync(scratch, 0, zero_bytes, st));
   if (prepass) {
     char *pb = scratch + base_bytes;
     auto *hm = reinterpret_cast<unsigned *>(pb);
@@ -350,17 +365,16 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
     p.Ac = Ac; p.Br = Br; p.ldac = p.tiles_m; p.ldbr = p.tiles_n;
     p.amax_pre = hm; p.bmax_pre = hm + p.tiles_m;
   }
-  p.counters = sink ? sink->counters : reinterpret_cast<unsigned long long *>(scratch);
-  p.events = sink ? sink->events : reinterpret_cast<ftk::EventDev *>(scratch + cnt_bytes);
+  p.counters = sink ? sink->counters : reinterpret_cast<unsigned long long *>(cnt_ptr);
+  p.events = sink ? sink->events : reinterpret_cast<ftk::EventDev *>(cnt_ptr + 64);
   p.ev_cap = sink ? sink->ev_cap : ev_cap;
   p.ev_row_off = sink ? sink->row_off : 0;
   p.ev_col_off = sink ? sink->col_off : 0;
   if (sink && ft) sink->units += (int64_t)p.ntiles * T;
-  p.faults = fd.empty() ? nullptr : reinterpret_cast<const ftk::FaultDev *>(scratch + cnt_bytes + ev_bytes);
+  p.faults = fd.empty() ? nullptr : reinterpret_cast<const ftk::FaultDev *>(cnt_ptr + 64 + ev_bytes);
   p.nfaults = (int)fd.size();
-  if (!sink) CUDA_TRY(cudaMemsetAsync(scratch, 0, cnt_bytes, st));
   if (!fd.empty())  // pageable source: the call returns once the source has been staged
-    CUDA_TRY(cudaMemcpyAsync(scratch + cnt_bytes + ev_bytes, fd.data(), f_bytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(cnt_ptr + 64 + ev_bytes, fd.data(), f_bytes, cudaMemcpyHostToDevice, st));
 
   const bool akm = is_t(ta), bkm = is_n(tb);
   // TMA needs 16-byte aligned bases and leading dimensions: repack otherwise (device copy
