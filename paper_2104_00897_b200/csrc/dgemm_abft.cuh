@@ -981,7 +981,13 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   // warp whose quarter holds none of them (partial edge tiles) waits and releases the stages
   // without issuing DMMA.  (The unprotected kernel keeps one loop: the split costs its k-loop
   // codegen and its tiles are only partial at sizes that are not multiples of 128.)
-  const bool active = !FT || (wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1));
+  // SKIP: whether this instantiation has the idle-warp loop.  The protected kernel always; the
+  // unprotected K-major-A / MN-major-B one too (ptxas allocates its DMMA loop better with it:
+  // 106 instead of 186 non-DMMA instructions per stage, tools/kloop_stats.py); the other
+  // unprotected ones keep their single loop.
+  constexpr bool SKIP = FT || (AKM && !BKM);
+  const bool active = FT ? (wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1))
+                         : (!SKIP || (wm * 64 < x.bm_eff && wn * 32 < x.bn_eff));
   double acc[8][4][2];
   int stage_base = 0;
   for (int attempt = 0;; ++attempt) {
@@ -1037,7 +1043,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     // injection code (which would make the register allocator shuffle accumulators).
     for (int s = 0; s < nk;) {
       const int s_end = __shfl_sync(0xffffffffu, next_stage < nk ? next_stage : nk, 0);
-      if (FT && !active) {  // nothing of this warp's quarter is used: release the stages only
+      if (SKIP && !active) {  // nothing of this warp's quarter is used: release the stages only
         for (; s < s_end; ++s) {
           const int gs = stage_base + s, slot = gs % STAGES;
           mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
