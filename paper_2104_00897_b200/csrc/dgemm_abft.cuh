@@ -92,17 +92,17 @@ struct Params {
   int64_t ldac, ldbr;
   const unsigned int *amax_pre, *bmax_pre;
   // Row-shared fused encode (encode mode FUSED): the tile of tile column 0 encodes e^T A_I from
-  // its staged tiles and publishes it per stage through L2 -- Ash[ti + p*ldash] for the 16
-  // k-slots, the slice's R1' high-word maximum hmA[ti + sg*tiles_m] and a release flag
-  // aflag[ti + sg*tiles_m] = 1 (sg = global stage index).  Every other tile of row I copies a
+  // its staged tiles and publishes it per stage through L2 -- Ash[ti*ldash + p] for the 16
+  // k-slots (k contiguous: one 128-byte line per stage), the slice's R1' high-word maximum
+  // hmA[ti*nk + sg] and a release flag aflag[ti*nk + sg] = 1 (sg = global stage index).  Every other tile of row I copies a
   // published stage when its flag is already set and otherwise encodes that stage itself (same
   // integer encode of the same staged data: bitwise the same checksum), so no CTA ever waits on
   // another.  Null = every CTA encodes A itself.
   double *Ash;
   int64_t ldash;
   unsigned int *hmA, *aflag;
-  // B_J e the same way along tile columns: the tile of tile row 0 publishes Bsh[tj + p*ldbsh],
-  // hmB[tj + sg*tiles_n] and counts its published stages in bcnt[tj + t*tiles_n]; a tile (or
+  // B_J e the same way along tile columns: the tile of tile row 0 publishes Bsh[tj*ldbsh + p],
+  // hmB[tj*nk + sg] and counts its published stages in bcnt[tj + t*tiles_n]; a tile (or
   // cluster pair) that finds the count complete when it starts copies every stage, otherwise
   // it encodes B_J e itself (split within the cluster pair).  Null = no sharing.
   double *Bsh;
@@ -712,7 +712,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     PubA f{false, 0.0, 0.0, 0u};
     if (!a_sub) return f;
     const int64_t sg = x.k0 / BK + s;  // global stage index
-    const size_t fi = (size_t)x.ti + (size_t)sg * P.tiles_m;
+    const size_t fi = (size_t)x.ti * P.nk + sg;
     unsigned ready = 0;
     if (lane == 0) {
       ready = ld_acquire_gpu(P.aflag + fi);
@@ -728,10 +728,10 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
       const int64_t pg = x.k0 + (int64_t)s * BK + p;
       if (AKM) {
-        f.a0 = lane < 8 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
-        f.a1 = lane < 8 && pg + 1 < x.k1 ? __ldcg(P.Ash + x.ti + (pg + 1) * P.ldash) : 0.0;
+        f.a0 = lane < 8 && pg < x.k1 ? __ldcg(P.Ash + x.ti * P.ldash + pg) : 0.0;
+        f.a1 = lane < 8 && pg + 1 < x.k1 ? __ldcg(P.Ash + x.ti * P.ldash + pg + 1) : 0.0;
       } else {
-        f.a0 = lane < 16 && pg < x.k1 ? __ldcg(P.Ash + x.ti + pg * P.ldash) : 0.0;
+        f.a0 = lane < 16 && pg < x.k1 ? __ldcg(P.Ash + x.ti * P.ldash + pg) : 0.0;
       }
       f.am = __ldcg(P.hmA + fi);
     }
@@ -749,14 +749,14 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     amax = max(amax, hm);
     if (a_pub) {
       const int64_t sg = x.k0 / BK + s;
-      const size_t fi = (size_t)x.ti + (size_t)sg * P.tiles_m;
+      const size_t fi = (size_t)x.ti * P.nk + sg;
       const int p = AKM ? 2 * lane : lane;
       const int64_t pg = x.k0 + (int64_t)s * BK + p;
       if (AKM) {
-        if (lane < 8 && pg < x.k1) P.Ash[x.ti + pg * P.ldash] = a0;
-        if (lane < 8 && pg + 1 < x.k1) P.Ash[x.ti + (pg + 1) * P.ldash] = a1;
+        if (lane < 8 && pg < x.k1) P.Ash[x.ti * P.ldash + pg] = a0;
+        if (lane < 8 && pg + 1 < x.k1) P.Ash[x.ti * P.ldash + pg + 1] = a1;
       } else if (lane < 16 && pg < x.k1) {
-        P.Ash[x.ti + pg * P.ldash] = a0;
+        P.Ash[x.ti * P.ldash + pg] = a0;
       }
       if (lane == 0) P.hmA[fi] = hm;
       __threadfence();
@@ -800,8 +800,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           const int64_t sg = x.k0 / BK + s;  // global stage index
           if (bcopy) {  // B_J e of this stage as published by tile row 0
             const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-            if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pg < x.k1 ? __ldcg(P.Bsh + x.tj + pg * P.ldbsh) : 0.0;
-            bmax_hi = max(bmax_hi, __ldcg(P.hmB + x.tj + (size_t)sg * P.tiles_n));
+            if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pg < x.k1 ? __ldcg(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
+            bmax_hi = max(bmax_hi, __ldcg(P.hmB + (size_t)x.tj * P.nk + sg));
           } else {
             uint32_t hmb = 0u;
             if (share) {
@@ -846,8 +846,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
             if (b_pub) {  // tile row 0: publish this stage's B_J e for the other tile rows
               __syncwarp();
               const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-              if (lane < 16 && pg < x.k1) P.Bsh[x.tj + pg * P.ldbsh] = sB[sidx<BKM>(x.crb, lane)];
-              if (lane == 0) P.hmB[x.tj + (size_t)sg * P.tiles_n] = hmb;
+              if (lane < 16 && pg < x.k1) P.Bsh[x.tj * P.ldbsh + pg] = sB[sidx<BKM>(x.crb, lane)];
+              if (lane == 0) P.hmB[(size_t)x.tj * P.nk + sg] = hmb;
               __threadfence();
               __syncwarp();
               if (lane == 0) atomicAdd(P.bcnt + x.tj + (size_t)x.t * P.tiles_n, 1u);

@@ -344,14 +344,14 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
     p.aflag = reinterpret_cast<unsigned *>(scratch);
     p.hmA = reinterpret_cast<unsigned *>(sb);
     p.Ash = reinterpret_cast<double *>(sb + hma_bytes);
-    p.ldash = p.tiles_m;
+    p.ldash = k;
   }
   if (bshare) {
     char *sb = scratch + base_bytes + pre_bytes + ash_bytes;
     p.bcnt = reinterpret_cast<unsigned *>(scratch + aflag_bytes);
     p.hmB = reinterpret_cast<unsigned *>(sb);
     p.Bsh = reinterpret_cast<double *>(sb + hmb_bytes);
-    p.ldbsh = p.tiles_n;
+    p.ldbsh = k;
   }
   CUDA_TRY(cudaMemsetAsync(scratch, 0, zero_bytes, st));
   if (prepass) {
