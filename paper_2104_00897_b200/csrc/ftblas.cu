@@ -937,7 +937,8 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
   P.trans = c.trans; P.unit = c.unit;
   P.f = df; P.nf = (int)lf.size(); P.cnt = c.leaf_sc->cnt;
   const int smem = (int)(sizeof(double) * (ftt::LEAF * ftt::LEAF + 2 * ftt::LEAF));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 15) / 16, (int64_t)num_sms()));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 16 * ftt::LEAF_NCOL - 1) / (16 * ftt::LEAF_NCOL),
+                                                              (int64_t)num_sms()));
   using K = void (*)(ftt::LeafParams);
   // [fwd][dmr][faults]
   static const K kernels[2][2][2] = {

@@ -53,57 +53,74 @@ __device__ __forceinline__ double leaf_a(const LeafParams &P, int p, int i) {  /
   return P.trans ? P.A[i + (int64_t)p * P.lda] : P.A[p + (int64_t)i * P.lda];
 }
 
-// The 32 steps of slot SL (rows i = 32 SL + l), both DMR copies as two interleaved dependence
-// chains.  The fault hook (original copy only) adds fdel to row fi after the update from x_fstep.
-template <int SL, bool FWD, bool DUAL, bool FLT>
-__device__ __forceinline__ void leaf_slot(const double *__restrict__ Sc, double (&b1)[4], double (&b2)[4],
-                                          const double (&r1)[4], const double (&r2)[4], int lane, int fi, int fstep,
-                                          double fdel) {
+// The 32 steps of slot SL (rows i = 32 SL + l) for NCH independent dependence chains at once:
+// NCOL right-hand sides, and with DUAL both DMR copies of each (chain c = DUAL ? 2 col + copy :
+// col; copy 1 uses the second reciprocal table).  The chains share each step's column of S
+// and hide each other's shuffle / FP64 latency.  The fault hook (copy 0 only) adds fdel[col]
+// to row fi[col] after the update from x_fstep[col].
+template <int SL, bool FWD, int NCOL, bool DUAL, bool FLT>
+__device__ __forceinline__ void leaf_slot(const double *__restrict__ Sc, double (&b)[NCOL * (DUAL ? 2 : 1)][4],
+                                          const double (&r1)[4], const double (&r2)[4], int lane, const int (&fi)[NCOL],
+                                          const int (&fstep)[NCOL], const double (&fdel)[NCOL]) {
+  constexpr int NCH = NCOL * (DUAL ? 2 : 1);
 #pragma unroll 2
   for (int s = 0; s < 32; ++s) {
     const int l = FWD ? s : 31 - s;
     const double *col = Sc + (32 * SL + l) * LEAF + lane;
-    const double x1 = __shfl_sync(0xffffffffu, ftd::v_mul(b1[SL], r1[SL]), l);
-    const double x2 = DUAL ? __shfl_sync(0xffffffffu, ftd::v_mul(b2[SL], r2[SL]), l) : 0.0;
+    // All chains' products first, then all broadcasts (the FP64 ops are volatile asm, so their
+    // program order is their issue order: interleaving keeps each shuffle off its product's
+    // latency).
+    double x[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) x[c] = ftd::v_mul(b[c][SL], (DUAL && (c & 1)) ? r2[SL] : r1[SL]);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) x[c] = __shfl_sync(0xffffffffu, x[c], l);
     if (FWD ? lane > l : lane < l) {
       const double a = col[32 * SL];
-      b1[SL] = ftd::v_fma(-a, x1, b1[SL]);
-      if (DUAL) b2[SL] = ftd::v_fma(-a, x2, b2[SL]);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) b[c][SL] = ftd::v_fma(-a, x[c], b[c][SL]);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (FWD ? q > SL : q < SL) {
         const double a = col[32 * q];
-        b1[q] = ftd::v_fma(-a, x1, b1[q]);
-        if (DUAL) b2[q] = ftd::v_fma(-a, x2, b2[q]);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) b[c][q] = ftd::v_fma(-a, x[c], b[c][q]);
       }
     }
-    if (FLT && 32 * SL + l == fstep) {
+    if (FLT) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (lane + 32 * q == fi) b1[q] = ftd::v_add(b1[q], fdel);
+      for (int cc = 0; cc < NCOL; ++cc)
+        if (32 * SL + l == fstep[cc]) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (lane + 32 * q == fi[cc]) b[DUAL ? 2 * cc : cc][q] = ftd::v_add(b[DUAL ? 2 * cc : cc][q], fdel[cc]);
+        }
     }
   }
-  b1[SL] = ftd::v_mul(b1[SL], r1[SL]);  // this lane's x of the slot: no later step changes b
-  if (DUAL) b2[SL] = ftd::v_mul(b2[SL], r2[SL]);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)  // this lane's x of the slot: no later step changes b
+    b[c][SL] = ftd::v_mul(b[c][SL], (DUAL && (c & 1)) ? r2[SL] : r1[SL]);
 }
 
-template <bool FWD, bool DUAL, bool FLT>
-__device__ __forceinline__ void leaf_column(const double *Sc, double (&b1)[4], double (&b2)[4], const double (&r1)[4],
-                                            const double (&r2)[4], int lane, int nslots, int fi, int fstep,
-                                            double fdel) {
+template <bool FWD, int NCOL, bool DUAL, bool FLT>
+__device__ __forceinline__ void leaf_solve(const double *Sc, double (&b)[NCOL * (DUAL ? 2 : 1)][4], const double (&r1)[4],
+                                           const double (&r2)[4], int lane, int nslots, const int (&fi)[NCOL],
+                                           const int (&fstep)[NCOL], const double (&fdel)[NCOL]) {
   if (FWD) {
-    leaf_slot<0, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
-    if (nslots > 1) leaf_slot<1, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
-    if (nslots > 2) leaf_slot<2, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
-    if (nslots > 3) leaf_slot<3, true, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    leaf_slot<0, true, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 1) leaf_slot<1, true, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 2) leaf_slot<2, true, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 3) leaf_slot<3, true, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
   } else {
-    if (nslots > 3) leaf_slot<3, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
-    if (nslots > 2) leaf_slot<2, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
-    if (nslots > 1) leaf_slot<1, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
-    leaf_slot<0, false, DUAL, FLT>(Sc, b1, b2, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 3) leaf_slot<3, false, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 2) leaf_slot<2, false, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
+    if (nslots > 1) leaf_slot<1, false, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
+    leaf_slot<0, false, NCOL, DUAL, FLT>(Sc, b, r1, r2, lane, fi, fstep, fdel);
   }
 }
+
+constexpr int LEAF_NCOL = 2;  // right-hand sides per warp pass
 
 template <bool FWD, bool DMR, bool FLT>
 __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
@@ -124,55 +141,75 @@ __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
   double r1[4], r2[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) { r1[q] = rd1[lane + 32 * q]; r2[q] = rd2[lane + 32 * q]; }
+  constexpr int NCOL = LEAF_NCOL, NCH = NCOL * (DMR ? 2 : 1);
   const int warps = blockDim.x >> 5;
-  for (int j = blockIdx.x * warps + (tid >> 5); j < P.n; j += gridDim.x * warps) {
-    double *col = P.B + (int64_t)j * P.ldb;
-    // This lane's fault in column j, if any (at most one per lane is honoured).
-    int fi = -1, fstep = -1;
-    double fdel = 0.0;
+  for (int j0 = (blockIdx.x * warps + (tid >> 5)) * NCOL; j0 < P.n; j0 += gridDim.x * warps * NCOL) {
+    // This lane's fault in each column, if any (at most one per lane and column is honoured).
+    int fi[NCOL], fstep[NCOL];
+    double fdel[NCOL];
+#pragma unroll
+    for (int cc = 0; cc < NCOL; ++cc) { fi[cc] = -1; fstep[cc] = -1; fdel[cc] = 0.0; }
     if (FLT)
       for (int e = 0; e < P.nf; ++e) {
         const int64_t code = P.f[e].index;  // j * LEAF + local row
-        if (code / LEAF == j && (int)(code % LEAF) % 32 == lane) { fi = (int)(code % LEAF); fstep = (int)P.f[e].step; fdel = P.f[e].delta; }
+        const int64_t cc = code / LEAF - j0;
+        if (cc >= 0 && cc < NCOL && (int)(code % LEAF) % 32 == lane)
+#pragma unroll
+          for (int c = 0; c < NCOL; ++c)
+            if (c == cc) { fi[c] = (int)(code % LEAF); fstep[c] = (int)P.f[e].step; fdel[c] = P.f[e].delta; }
       }
-    double b1[4], b2[4];
+    double b[NCH][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int p = lane + 32 * q;
-      b1[q] = p < nb ? col[p] : 0.0;
-      b2[q] = b1[q];
-    }
-    leaf_column<FWD, DMR, FLT>(Sc, b1, b2, r1, r2, lane, nslots, fi, fstep, fdel);
-    if (DMR) {
-      bool bad = false;
+    for (int cc = 0; cc < NCOL; ++cc) {
+      const bool jv = j0 + cc < P.n;
+      const double *col = P.B + (int64_t)(j0 + cc) * P.ldb;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) bad |= (lane + 32 * q < nb) && ftd::differ(b1[q], b2[q]);
-      if (__any_sync(0xffffffffu, bad)) {
-        // Rare: a third computation settles the column (the verification unit of a diagonal
-        // block: one fault propagates to every later row of the column).  Each element takes
-        // the third value; the column is corrected when the third agrees with one copy wherever
-        // the two disagreed.
-        double b3[4], b4[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) b3[q] = lane + 32 * q < nb ? col[lane + 32 * q] : 0.0;
-        leaf_column<FWD, false, false>(Sc, b3, b4, r2, r2, lane, nslots, -1, -1, 0.0);
-        bool unsettled = false;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (lane + 32 * q < nb && ftd::differ(b1[q], b2[q]))
-            unsettled |= ftd::differ(b3[q], b1[q]) && ftd::differ(b3[q], b2[q]);
-          b1[q] = b3[q];
-        }
-        unsettled = __any_sync(0xffffffffu, unsettled);
-        if (lane == 0) {
-          atomicAdd(&P.cnt[ftd::D_DETECTED], 1ull);
-          atomicAdd(&P.cnt[unsettled ? ftd::D_UNCORRECTABLE : ftd::D_CORRECTED], 1ull);
-        }
+      for (int q = 0; q < 4; ++q) {
+        const int p = lane + 32 * q;
+        b[DMR ? 2 * cc : cc][q] = jv && p < nb ? col[p] : 0.0;
+        if (DMR) b[2 * cc + 1][q] = b[2 * cc][q];
       }
     }
+    leaf_solve<FWD, NCOL, DMR, FLT>(Sc, b, r1, r2, lane, nslots, fi, fstep, fdel);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (lane + 32 * q < nb) col[lane + 32 * q] = b1[q];
+    for (int cc = 0; cc < NCOL; ++cc) {
+      const int j = j0 + cc;
+      if (j >= P.n) break;
+      double *col = P.B + (int64_t)j * P.ldb;
+      double *out = b[DMR ? 2 * cc : cc];
+      if (DMR) {
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bad |= (lane + 32 * q < nb) && ftd::differ(b[2 * cc][q], b[2 * cc + 1][q]);
+        if (__any_sync(0xffffffffu, bad)) {
+          // Rare: a third computation settles the column (the verification unit of a diagonal
+          // block: one fault propagates to every later row of the column).  Each element takes
+          // the third value; the column is corrected when the third agrees with one copy
+          // wherever the two disagreed.
+          double b3[1][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) b3[0][q] = lane + 32 * q < nb ? col[lane + 32 * q] : 0.0;
+          const int nfi[1] = {-1}, nfs[1] = {-1};
+          const double nfd[1] = {0.0};
+          leaf_solve<FWD, 1, false, false>(Sc, b3, r2, r2, lane, nslots, nfi, nfs, nfd);
+          bool unsettled = false;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (lane + 32 * q < nb && ftd::differ(b[2 * cc][q], b[2 * cc + 1][q]))
+              unsettled |= ftd::differ(b3[0][q], b[2 * cc][q]) && ftd::differ(b3[0][q], b[2 * cc + 1][q]);
+            out[q] = b3[0][q];
+          }
+          unsettled = __any_sync(0xffffffffu, unsettled);
+          if (lane == 0) {
+            atomicAdd(&P.cnt[ftd::D_DETECTED], 1ull);
+            atomicAdd(&P.cnt[unsettled ? ftd::D_UNCORRECTABLE : ftd::D_CORRECTED], 1ull);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < nb) col[lane + 32 * q] = out[q];
+    }
   }
 }
 
