@@ -580,25 +580,37 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   const int64_t Kc = (ft && tl_interval > 0 && tl_interval < k) ? tl_interval : k;
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
 
-  // Panels: ~m/8 rows, a multiple of 2 x 127 (units intact, even leading dimensions); one
-  // panel when the problem is small.
+  // Panels: about m/8 rows, a multiple of 2 x 127 (units intact, even leading dimensions),
+  // chosen within [m/11, m/6] to minimise the total number of 148-CTA waves over the panels
+  // (ties: closest to m/8); one panel when the problem is small.
   const int64_t unit2 = 2 * ftk::TM;
   int64_t P = m;
-  if (m >= 16 * unit2) P = ((m + 7) / 8 + unit2 - 1) / unit2 * unit2;
+  if (m >= 16 * unit2) {
+    const int64_t th = ft ? ftk::TM : ftk::BM, tw = ft ? ftk::TN : ftk::BN, sms = num_sms();
+    const int64_t tcols = (n + tw - 1) / tw, target = (m + 7) / 8;
+    int64_t best_waves = INT64_MAX, best_dist = INT64_MAX;
+    for (int64_t c = (m / 11 + unit2 - 1) / unit2 * unit2; c <= m / 6; c += unit2) {
+      int64_t waves = 0;
+      for (int64_t r0 = 0; r0 < m; r0 += c) waves += (((std::min(c, m - r0) + th - 1) / th) * tcols + sms - 1) / sms;
+      const int64_t dist = c > target ? c - target : target - c;
+      if (waves < best_waves || (waves == best_waves && dist < best_dist)) { best_waves = waves; best_dist = dist; P = c; }
+    }
+    if (P == m) P = (target + unit2 - 1) / unit2 * unit2;
+  }
   const int64_t npan = (m + P - 1) / P;
   const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
 
   // Column chunks of a panel of pr rows: uniform chunks of t tile columns (t even, so chunk
-  // edges are multiples of 2 tiles: units intact, 16-byte aligned bases), t chosen to minimise
-  // the panel's total number of 148-CTA waves (at most 16 chunks), ties to the narrowest t, so
-  // that the first chunk of op(B) -- the pipeline's start-up copy -- is as small as the wave
-  // count allows.  One chunk when there is one panel.
+  // edges are multiples of 2 tiles: units intact, 16-byte aligned bases), t minimising the
+  // panel's time in 148-CTA waves plus the copy of one chunk of op(B) (the pipeline's start-up:
+  // a k-deep column takes ~1.2e-3 of a k-deep wave over PCIe Gen5 against the FP64 DMMA rate),
+  // at most 16 chunks.  One chunk when there is one panel.
   auto chunking = [&](int64_t pr) {
     std::vector<int64_t> best{0, n};
     if (npan < 2) return best;
     const int64_t tw = ft ? ftk::TN : ftk::BN, th = ft ? ftk::TM : ftk::BM;
     const int64_t trows = (pr + th - 1) / th, tcols = (n + tw - 1) / tw, sms = num_sms();
-    int64_t best_waves = INT64_MAX;
+    double best_cost = 1e300;
     for (int64_t t = 2; t < tcols; t += 2) {
       const int64_t nch = (tcols + t - 1) / t;
       if (nch > 16) continue;
@@ -609,7 +621,8 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
         waves += (trows * ((c1 - c0 + tw - 1) / tw) + sms - 1) / sms;
         e.push_back(c1);
       }
-      if (waves < best_waves) { best_waves = waves; best = e; }
+      const double cost = (double)waves + 1.2e-3 * (double)(t * tw);
+      if (cost < best_cost) { best_cost = cost; best = e; }
     }
     return best;
   };
