@@ -1149,8 +1149,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // so that one wave of 148 CTAs touches ~12 A row panels and ~12 B column panels (L2 reuse)
   // instead of 148 A panels and one B panel.
   // With checksums shared through L2 (R22) the publishing tiles come first: tile row 0 (B_J e)
-  // and tile column 0 (e^T A_I) in the first waves, then the rest of the grid in grouped
-  // raster, so nearly every other tile finds both checksums published when it runs.
+  // and tile column 0 (e^T A_I) in the first waves, so nearly every other tile finds both
+  // checksums published when it runs.  A partial last tile row / column (cheap: its idle warps
+  // skip the DMMA stream) goes last, so the final waves are made of short tiles.
+  const int tstr_m = (FT || (P.dev_mode & 32)) ? TM : BM, tstr_n = (FT || (P.dev_mode & 32)) ? TN : BN;
+  const bool prow = P.tiles_m > 1 && (P.m % tstr_m) != 0, pcol = P.tiles_n > 1 && (P.n % tstr_n) != 0;
   auto map_tile = [&](int Lg, int &ti_, int &tj_, int &t_) {
     int L = Lg % P.ntiles;
     t_ = P.t_base + Lg / P.ntiles;
@@ -1162,11 +1165,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       L -= P.tiles_m - 1;
       r0 = c0 = 1;
     }
-    const int tm = P.tiles_m - r0, tn = P.tiles_n - c0;
-    const int band_tiles = RASTER_G * tn, band = L / band_tiles;
-    const int within = L - band * band_tiles, rows = min(RASTER_G, tm - band * RASTER_G);
-    ti_ = r0 + band * RASTER_G + within % rows;
-    tj_ = c0 + within / rows;
+    const int rend = P.tiles_m - (prow ? 1 : 0), cend = P.tiles_n - (pcol ? 1 : 0);
+    const int tm = rend - r0, tn = cend - c0;  // interior, in grouped raster
+    if (tm > 0 && tn > 0 && L < tm * tn) {
+      const int band_tiles = RASTER_G * tn, band = L / band_tiles;
+      const int within = L - band * band_tiles, rows = min(RASTER_G, tm - band * RASTER_G);
+      ti_ = r0 + band * RASTER_G + within % rows;
+      tj_ = c0 + within / rows;
+      return;
+    }
+    L -= max(tm, 0) * max(tn, 0);
+    if (prow) {
+      if (L < cend - c0) { ti_ = P.tiles_m - 1; tj_ = c0 + L; return; }
+      L -= cend - c0;
+    }
+    ti_ = r0 + L;  // partial last tile column, its rows top to bottom
+    tj_ = P.tiles_n - 1;
   };
   const int Lg = (int)blockIdx.x;
   const bool ghost = P.cluster2 && Lg >= P.total;  // pads an odd grid to whole clusters
