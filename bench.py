@@ -327,8 +327,10 @@ def main():
             ms, per = float(t[0].item()), [float(x) for x in t[1:].tolist()]
             dist.barrier()
         timed.min_ms[label if label is not None else ft] = min(per)
+        timed.per[label if label is not None else ft] = per
         return ms, launches, reps
     timed.min_ms = {}
+    timed.per = {}
 
     # Kernel-only time of the dominant kernel for the roofline: same launches, events
     # bracketing only the ftblas_dgemm call (report copy excluded) on the launch stream.
@@ -465,6 +467,7 @@ def main():
                  "recomputed": cnt[3], "events": cnt[4],
                  "prepass_encode": pre, "unfused_baseline": unf,
                  "ms_per_step_min": {"protected": timed.min_ms.get(True), "unprotected": timed.min_ms.get(False)},
+                 "ms_per_step_all": {"protected": timed.per.get(True), "unprotected": timed.per.get(False)},
                  "tflops_protected_no_faults": (flops_total * args.steps / (ms_clean * 1e-3) / 1e12
                                                 if ms_clean else None),
                  "cublas_dgemm_tflops": flops_total / (ms_cublas * 1e-3) / 1e12 if ms_cublas else None},
