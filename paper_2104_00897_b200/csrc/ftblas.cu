@@ -13,6 +13,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -51,12 +52,12 @@ bool is_t(char c) { return c == 'T' || c == 't' || c == 'C' || c == 'c'; }
 template <bool AKM, bool BKM, bool FT>
 int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &p0, dim3 grid, cudaStream_t st) {
   auto kfn = ftk::dgemm_abft_kernel<AKM, BKM, FT>;
-  static bool attr_set[64] = {false};  // per instantiation and device
+  static std::atomic<bool> attr_set[64];  // per instantiation and device (idempotent if raced)
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+  if (dev < 0 || dev >= 64 || !attr_set[dev].load(std::memory_order_acquire)) {
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ftk::SMEM_BYTES));
-    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    if (dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
   }
   ftk::Params p = p0;
   p.total = (int)grid.x;
@@ -959,11 +960,13 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
        {ftt::trsm_leaf_kernel<false, true, false>, ftt::trsm_leaf_kernel<false, true, true>}},
       {{ftt::trsm_leaf_kernel<true, false, false>, ftt::trsm_leaf_kernel<true, false, true>},
        {ftt::trsm_leaf_kernel<true, true, false>, ftt::trsm_leaf_kernel<true, true, true>}}};
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<bool> attr_set[64];  // per device (idempotent if raced)
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev].load(std::memory_order_acquire)) {
     for (int a = 0; a < 8; ++a)
       CUDA_TRY(cudaFuncSetAttribute(kernels[a >> 2][(a >> 1) & 1][a & 1], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    if (dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
   }
   kernels[c.fwd][c.ft][c.ft && P.nf > 0]<<<grid, 512, smem, c.st>>>(P);
   ++tl_launches;
