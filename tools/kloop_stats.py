@@ -18,7 +18,10 @@ for name, ins in funcs.items():
     if 'dgemm_abft_kernel' not in name:
         continue
     idx = [i for i, t in enumerate(ins) if 'DMMA' in t]
-    loop = ins[idx[0]:idx[127] + 1]
+    # the main k-loop body: the densest window of 128 consecutive DMMAs (thin / segment loops
+    # with fewer DMMAs per stage come first in the function)
+    w = min(range(len(idx) - 127), key=lambda a: idx[a + 127] - idx[a])
+    loop = ins[idx[w]:idx[w + 127] + 1]
     dc = sum(1 for t in loop if (m := re.search(r'DMMA\.8x8x4 (R\d+), R\d+, R\d+, (R\d+)', t)) and m.group(1) != m.group(2))
     other = sum(1 for t in loop if 'DMMA' not in t)
     ldl = sum(1 for t in loop if 'LDL' in t or 'STL' in t)
