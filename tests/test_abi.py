@@ -93,3 +93,17 @@ def test_paper_overhead_model_closed_form():
     assert predict_unfused_overhead(14, 14, 14, 1.0, 1.0) == pytest.approx(8 / 14)
     with pytest.raises(ValueError):
         predict_unfused_overhead(10, 10, 20, 1.0, 1.0)
+
+
+def test_option_setters_validate_without_a_gpu():
+    """Thread-local options: encode modes FUSED / PREPASS / FUSED_LOCAL accepted, others -> 4;
+    the interval must be a non-negative multiple of the step quantum."""
+    L = F.load()
+    for mode in (F.ENCODE_FUSED, F.ENCODE_PREPASS, F.ENCODE_FUSED_LOCAL):
+        assert L.ftblas_set_encode(mode) == 0
+    assert L.ftblas_set_encode(3) == 4 and L.ftblas_set_encode(-1) == 4
+    assert L.ftblas_set_encode(F.ENCODE_FUSED) == 0
+    assert L.ftblas_set_interval(32) == 0 and L.ftblas_set_interval(0) == 0
+    assert L.ftblas_set_interval(20) == 4 and L.ftblas_set_interval(-16) == 4
+    assert L.ftblas_set_correction(1) == 0 and L.ftblas_set_correction(0) == 0
+    assert L.ftblas_set_correction(2) == 4
