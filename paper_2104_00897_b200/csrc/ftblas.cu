@@ -61,8 +61,11 @@ int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &
   }
   ftk::Params p = p0;
   p.total = (int)grid.x;
-  // Fused encode: 2-CTA clusters share the B_J encode (cluster size 2 packs all 148 SMs).
-  if (FT && !p.Ac && !(p.dev_mode & 128)) {
+  // Encode mode FUSED_LOCAL: 2-CTA clusters share the B_J encode (cluster size 2 packs all 148
+  // SMs).  With the checksums shared through L2 (FUSED, R22) nearly every tile copies B_J e, and
+  // pair co-scheduling costs more than the split saves (C5-like 4.0% -> 3.9%, C4a 9.2% -> 7.8%),
+  // so those launches are plain.
+  if (FT && !p.Ac && !p.Ash && !p.Bsh && !(p.dev_mode & 128)) {
     p.cluster2 = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((grid.x + 1) & ~1u);
