@@ -776,6 +776,14 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
         const PubA pa = (P.Ac || (P.dev_mode & 3)) ? PubA{false, 0.0, 0.0, 0u} : fetch_a(s);
+        // B_J e copy (whole tile decided at its start): fetched before the TMA wait as well
+        double pb = 0.0;
+        uint32_t pbm = 0u;
+        if (bcopy) {
+          const int64_t pg = x.k0 + (int64_t)s * BK + lane;
+          pb = lane < 16 && pg < x.k1 ? __ldcg(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
+          pbm = __ldcg(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
+        }
         if (!(P.dev_mode & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
@@ -799,9 +807,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           }
           const int64_t sg = x.k0 / BK + s;  // global stage index
           if (bcopy) {  // B_J e of this stage as published by tile row 0
-            const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-            if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pg < x.k1 ? __ldcg(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
-            bmax_hi = max(bmax_hi, __ldcg(P.hmB + (size_t)x.tj * P.nk + sg));
+            if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pb;
+            bmax_hi = max(bmax_hi, pbm);
           } else {
             uint32_t hmb = 0u;
             if (share) {
