@@ -112,8 +112,8 @@ struct Params {
   int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
                                   // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait,
                                   // 32 unprotected kernel on the 127 grid, 128 no clusters, 256 tiles
-                                  // wait for the published e^T A_I, 512 (with 128) tiles wait for
-                                  // the published B_J e (row/column-shared encode copy paths)
+                                  // wait for the published e^T A_I, 512 tiles wait for the
+                                  // published B_J e (row/column-shared encode copy paths)
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
@@ -213,11 +213,6 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
 }
 __device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -613,7 +608,6 @@ struct SmemTail {
   uint32_t mail_hm[STAGES];
   uint64_t mfull[STAGES], mfree[STAGES];
   int share;  // this CTA encodes half of B and swaps it with its cluster partner
-  unsigned bobs, bcopy;  // B_J e published by tile row 0: observed here / taken for this tile
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
   double dres[256];                // residuals: 0..127 columns, 128..255 rows
   double red[NTHREADS / 32];
@@ -766,10 +760,30 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   };
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
-    const bool bcopy = verify && tl.bcopy;
-    const bool share = verify && tl.share && !bcopy;
     if (lane == 0)
       for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
+    // (after the first TMA loads are in flight) B_J e fully published by tile row 0 (same
+    // interval, same stage count) when this encoder warp starts?  Then it copies every one of
+    // its stages; otherwise it encodes them (bitwise the same checksum, so the four encoder
+    // warps need not agree).  Publication only happens in launches without clusters, so a
+    // cluster pair never mixes the two.
+    bool bcopy = false;
+    if (verify && P.Bsh && x.ti != 0) {
+      unsigned done = 0;
+      if (lane == 0) {
+        const unsigned *cnt = P.bcnt + x.tj + (size_t)x.t * P.tiles_n;
+        done = ld_acquire_gpu(cnt) >= (unsigned)nk;
+        // development / tests: dev mode 512 waits for tile row 0 to finish publishing, so
+        // every other tile takes the copy path
+        while ((P.dev_mode & 512) && !done) {
+          __nanosleep(1000);
+          done = ld_acquire_gpu(cnt) >= (unsigned)nk;
+        }
+      }
+      bcopy = __shfl_sync(0xffffffffu, done, 0) != 0;
+      __syncwarp();  // orders the other lanes' copies after lane 0's acquire
+    }
+    const bool share = verify && tl.share && !bcopy;
     uint32_t amax_hi = 0u, bmax_hi = 0u;
     for (int s = warp; s < nk; s += N_ENC_WARPS) {
       if (verify) {
@@ -1241,10 +1255,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tl.first_col = 0x7fffffff;
     tl.retry = 0;
     tl.share = share ? 1 : 0;
-    // B_J e fully published by tile row 0 (same interval, same stage count) before this tile
-    // started?  A cluster pair takes the copy only if both CTAs saw it (decided below).
-    tl.bobs = (FT && P.Bsh && ti != 0 && !ghost && ld_acquire_gpu(P.bcnt + tj + (size_t)tt * P.tiles_n) >= (unsigned)x.nk) ? 1u : 0u;
-    tl.bcopy = 0u;
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&tl.mfull[s], 1);
@@ -1265,18 +1275,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (P.cluster2) cluster_sync_all();  // partners' mailbox barriers are initialised
   if (ghost) return;
-  if (FT && P.Bsh) {
-    if (x.tid == 0) {
-      // development / tests: dev mode 512 (with 128, no clusters) waits for tile row 0 to
-      // finish publishing, so every other tile takes the copy path
-      if ((P.dev_mode & 512) && !P.cluster2 && ti != 0) {
-        while (ld_acquire_gpu(P.bcnt + tj + (size_t)tt * P.tiles_n) < (unsigned)x.nk) __nanosleep(1000);
-        tl.bobs = 1u;
-      }
-      tl.bcopy = share ? (tl.bobs & ld_cluster_u32(mapa_u32(smem_u32(&tl.bobs), cluster_rank() ^ 1u))) : tl.bobs;
-    }
-    __syncthreads();
-  }
 
   // The two roles never re-converge, so ptxas can give each its own register budget.
   if (is_cs_warp(x.warp)) {
