@@ -19,6 +19,7 @@ number goes through ftblas_dgemm_host (pinned host buffers, H2D + D2H in the reg
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -315,6 +316,8 @@ def main():
         if world > 1:
             dist.barrier()
         F.ftblas_take_launch_count()
+        gc.collect()
+        gc.disable()  # no collector pause inside the timed region (the reported call syncs per step)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         ev[0].record(stream)
         reps = []
@@ -322,6 +325,7 @@ def main():
             reps.append(step(ft))
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
+        gc.enable()
         launches = F.ftblas_take_launch_count()
         ms = ev[0].elapsed_time(ev[-1])
         per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
