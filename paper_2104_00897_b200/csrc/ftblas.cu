@@ -550,6 +550,8 @@ int num_sms();
 // last panel run in column chunks (edges multiples of 2 x 127 columns): the first panel starts
 // as soon as its op(A) rows and the first chunk of op(B) are on the device, the rest of B
 // streaming in behind it chunk by chunk; the last panel returns its result chunk by chunk.
+// When m is small against n (column mode) there is one panel: all of op(A), then op(B) and
+// the result in column chunks.
 // Faults are routed to their panel / chunk with local indices; counters and events accumulate
 // on the device (events carry global indices) and the report is filled once at the end.
 int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha,
@@ -601,6 +603,18 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
     }
     if (P == m) P = (target + unit2 - 1) / unit2 * unit2;
   }
+  // Column mode: all of op(A) first, then op(B) in column chunks over one panel of m rows.  It
+  // wins when waiting for all of op(B) behind the first row panel costs more start-up than
+  // copying all of op(A) (m small against n: the row panels of a multi-GPU run).  Estimated in
+  // bytes, with ~636 FP64 flops of DMMA time per byte of PCIe Gen5 copy.
+  bool colmode = false;
+  if (P < m) {
+    const double f_per_b = 636.0;
+    const double row_idle = 8.0 * (double)P * (double)k +
+                            std::max(0.0, 8.0 * (double)k * (double)n - 2.0 * (double)P * (double)n * (double)k / f_per_b);
+    const double col_idle = 8.0 * (double)m * (double)k;
+    if (col_idle < row_idle) { colmode = true; P = m; }
+  }
   const int64_t npan = (m + P - 1) / P;
   const int64_t br = is_n(tb) ? k : n, bc = is_n(tb) ? n : k;
 
@@ -611,7 +625,7 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   // at most 16 chunks.  One chunk when there is one panel.
   auto chunking = [&](int64_t pr) {
     std::vector<int64_t> best{0, n};
-    if (npan < 2) return best;
+    if (npan < 2 && !colmode) return best;
     const int64_t tw = ft ? ftk::TN : ftk::BN, th = ft ? ftk::TM : ftk::BM;
     const int64_t trows = (pr + th - 1) / th, tcols = (n + tw - 1) / tw, sms = num_sms();
     double best_cost = 1e300;

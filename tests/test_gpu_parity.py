@@ -270,6 +270,30 @@ def test_host_buffer_pipeline_row_panels(trans):
     assert np.all(np.abs(Ct - A @ B) <= bound(None, A, B, np.zeros((m, n)), 1.0, 0.0, "N", "N", k))
 
 
+@pytest.mark.parametrize("trans", ["NN", "TT"])
+def test_host_buffer_pipeline_column_mode(trans):
+    """m small against n: the host-buffer pipeline copies all of op(A), then streams op(B) and
+    the result in column chunks over one panel (column mode).  Faults in several chunks;
+    report and values as one call on the whole problem."""
+    ta, tb = trans
+    rng = np.random.default_rng(113)
+    m, n, k = 4100, 8000, 300
+    A, B, C0 = rand(rng, m, k), rand(rng, k, n), rand(rng, m, n)
+    As, Bs = stored(A, ta), stored(B, tb)
+    lda, ldb = As.shape[0], Bs.shape[0]
+    faults = [(5, 7, 10, 3.0), (4099, 7999, 299, -4.0), (2000, 3500, 150, 2.0), (100, 6000, 0, 8.0),
+              (3000, 1200, 300, -1.5)]
+    C = np.asfortranarray(C0.copy())
+    F.ftblas_inject_arm(faults)
+    rep = F.ftblas_dgemm_host(ta, tb, m, n, k, 0.5, As, lda, Bs, ldb, 1.0, C, m)
+    Co, orep = oracle.dgemm_abft(ta, tb, m, n, k, 0.5, As, lda, Bs, ldb, 1.0, C0, m,
+                                 BM=rep.unit_rows, BN=rep.unit_cols, BK=rep.step_quantum, faults=faults)
+    assert rep.units_checked == orep.units_checked
+    assert_reports_match(rep, orep, As, Bs, ta, tb, k)
+    assert rep.detected == 5 and rep.corrected == 5
+    assert np.all(np.abs(C - Co.reshape((n, m)).T) <= bound(None, A, B, C0, 0.5, 1.0, "N", "N", k))
+
+
 def test_nondefault_stream():
     import torch
     rng = np.random.default_rng(111)
