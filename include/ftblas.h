@@ -122,6 +122,8 @@ int ftblas_dgemm_unfused(char transA, char transB, int64_t m, int64_t n, int64_t
  * (multiples of 254 rows) with copies overlapped with compute on two library streams; the
  * first and last panels run in column chunks (multiples of 254 columns) so compute starts
  * once the first chunk of op(B) has arrived and the last result returns chunk by chunk.
+ * When m is small against n (e.g. one rank's row panel of a multi-GPU run) all of op(A) is
+ * copied first and op(B) and C stream in column chunks over a single panel instead.
  * Chunk and panel edges are multiples of the verification unit, so the report (units,
  * events with global (i, j)) equals that of one ftblas_dgemm call on the whole problem. */
 int ftblas_dgemm_host(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
