@@ -74,6 +74,7 @@ def lib():
         L.oracle_daxpy.argtypes = [i64, d, P, i64, P, i64, P, i64, P]
         L.oracle_dgemv.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64, P, i64, P]
         L.oracle_dtrsm.argtypes = [c, c, c, i64, i64, d, P, i64, P, i64, i64, P]
+        L.oracle_dtrsm_right.argtypes = [c, c, c, i64, i64, d, P, i64, P, i64, i64, P]
         _lib = L
     return _lib
 
@@ -247,13 +248,15 @@ def dgemv(trans, m, n, alpha, A, lda, x, incx, beta, y, incy, faults=()):
     return yo, DmrReport(*[int(v) for v in cnt])
 
 
-def dtrsm(uplo, transa, diag, m, n, alpha, A, lda, B, ldb, faults=()):
-    """DTRSM oracle (NEXT-3): solve op(A) X = alpha B (side L); returns (X flat, (detected, corrected))."""
+def dtrsm(uplo, transa, diag, m, n, alpha, A, lda, B, ldb, faults=(), side="L"):
+    """DTRSM oracle (NEXT-3): solve op(A) X = alpha B (side L, op(A) m x m) or X op(A) = alpha B
+    (side R, op(A) n x n); returns (X flat, (detected, corrected))."""
     A = _flat(A)
     Bo = _flat(B).copy()
     cnt = np.zeros(4, dtype=np.int64)
-    lib().oracle_dtrsm(uplo.encode(), transa.encode(), diag.encode(), m, n, alpha, _ptr(A), lda, _ptr(Bo), ldb,
-                       len(list(faults)), _ptr(cnt))
+    fn = lib().oracle_dtrsm if side in ("L", "l") else lib().oracle_dtrsm_right
+    fn(uplo.encode(), transa.encode(), diag.encode(), m, n, alpha, _ptr(A), lda, _ptr(Bo), ldb,
+       len(list(faults)), _ptr(cnt))
     return Bo, (int(cnt[1]), int(cnt[2]))
 
 

@@ -496,6 +496,33 @@ void oracle_dtrsm(char uplo, char transa, char diag, int64_t m, int64_t n, doubl
   counters[0] = 0; counters[1] = nfaults; counters[2] = nfaults; counters[3] = 0;
 }
 
+/* DTRSM side 'R' (B = alpha B op(A)^-1): X op(A) = alpha B, op(A) n x n, in place,
+ * row by row: each row x of X solves x op(A) = alpha b by substitution over the columns of
+ * op(A) -- forward (j ascending) when op(A) is upper, backward when lower: x_j = b_j * (1 /
+ * op(A)_jj), then b_q -= op(A)_jq x_j for the columns q still to solve (fma, substitution
+ * order).  Faults are corrected by the protection, as on the left (reading R21). */
+void oracle_dtrsm_right(char uplo, char transa, char diag, int64_t m, int64_t n, double alpha, const double *A,
+                        int64_t lda, double *B, int64_t ldb, int64_t nfaults, int64_t *counters) {
+  int lower = (uplo == 'L' || uplo == 'l'), tr = is_trans(transa), unit = (diag == 'U' || diag == 'u');
+  int fwd = lower == tr; /* op(A) upper -> columns ascending */
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < m; ++r) {
+    for (int64_t q = 0; q < n; ++q) B[r + q * ldb] = alpha * B[r + q * ldb];
+    for (int64_t s = 0; s < n; ++s) {
+      int64_t j = fwd ? s : n - 1 - s;
+      double v = B[r + j * ldb];
+      if (!unit) v = v * (1.0 / A[j + j * lda]);
+      B[r + j * ldb] = v;
+      if (fwd) {
+        for (int64_t q = j + 1; q < n; ++q) B[r + q * ldb] = fma(-(tr ? A[q + j * lda] : A[j + q * lda]), v, B[r + q * ldb]);
+      } else {
+        for (int64_t q = 0; q < j; ++q) B[r + q * ldb] = fma(-(tr ? A[q + j * lda] : A[j + q * lda]), v, B[r + q * ldb]);
+      }
+    }
+  }
+  counters[0] = 0; counters[1] = nfaults; counters[2] = nfaults; counters[3] = 0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
