@@ -234,18 +234,21 @@ int ftblas_dgemv_noft(char trans, int64_t m, int64_t n, double alpha, const doub
                       const double *x, int64_t incx, double beta, double *y, int64_t incy);
 
 /* ---------------------------------------------------------------------------------------
- * FT-DTRSM (§III.C.3, 440, 476): solve
- * op(A) X = alpha B in place (B := X), side 'L' (the paper's B = alpha op(A)^-1 B; side 'R'
- * returns -1), uplo 'L'/'U', transa 'N'/'T'/'C', diag 'N'/'U' (unit diagonal: not read);
- * A m x m, B m x n, device pointers, column-major.  Recursive blocked algorithm: diagonal
- * blocks of <= 128 rows starting at multiples of 128 are solved by a DMR kernel that multiplies by packed reciprocals of
- * the diagonal, the coupling updates B2 -= op(A)21 X1 run on the protected
+ * FT-DTRSM (§III.C.3, 440, 476): in place (B := X),
+ *   side 'L': op(A) X = alpha B (the paper's B = alpha op(A)^-1 B), A m x m;
+ *   side 'R': X op(A) = alpha B (B = alpha B op(A)^-1), A n x n;
+ * uplo 'L'/'U', transa 'N'/'T'/'C', diag 'N'/'U' (unit diagonal: not read); B m x n; device
+ * pointers, column-major.  Recursive blocked algorithm along the solve (B's rows for side L,
+ * its columns for side R): diagonal blocks of <= 128 starting at multiples of 128 are solved by
+ * a DMR kernel that multiplies by packed reciprocals of the diagonal, the
+ * coupling updates (B2 -= op(A)21 X1, or B2 -= X1 op(A)12 on the right) run on the protected
  * DMMA kernel (fused ABFT, this library's ftblas_dgemm path).  err (nullable) sums both: the
- * ABFT units / events of the GEMM updates (event rows global) plus the DMR detections of the
- * diagonal solves (detected/corrected; uncorrectable ones are counted in `recomputed`).
- * An armed fault (i, j, step = p) perturbs the update of B(i, j) by X(p, j); it must satisfy
- * p < i when op(A) is lower (forward substitution) or p > i when op(A) is upper (status 3
- * otherwise).  Status codes as ftblas_dgemm with positions in this list. */
+ * ABFT units / events of the GEMM updates (event indices global) plus the DMR detections of
+ * the diagonal solves (detected/corrected; uncorrectable ones are counted in `recomputed`).
+ * An armed fault (i, j, step = p) perturbs the update of B(i, j) by X(p, j) (side L; p must
+ * precede i in the substitution order: p < i when op(A) is lower, p > i when upper) or by
+ * X(i, p) (side R; p must precede j: p < j when op(A) is upper, p > j when lower); status 3
+ * otherwise.  Status codes as ftblas_dgemm with positions in this list. */
 int ftblas_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
                  const double *A, int64_t lda, double *B, int64_t ldb, ftblas_err_report_t *err);
 int ftblas_dtrsm_noft(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,

@@ -939,23 +939,31 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
 // p, or in the leaf when i and p share one LEAF block.
 struct TrsmCtx {
   bool ft, fwd, trans, unit;
+  bool right;    // side 'R': X op(A) = B, the solve runs over B's columns, each row an RHS
   int64_t leaf;  // diagonal block rows (LEAF; 127 for the protected solve measured slower)
   const double *A;
   int64_t lda;
   double *B;
-  int64_t ldb, n;
+  int64_t ldb, n;  // n: number of right-hand sides (side L: B's columns, side R: B's rows)
   const std::vector<ftblas_fault_t> *faults;
   ReportSink *sink;
   DmrScratch *leaf_sc;  // leaf DMR counters
   cudaStream_t st;
 };
 
+// A fault (i, j, step) as (element along the solve, right-hand side): side L (row i of column
+// j), side R (column j of row i).
+inline int64_t f_elem(const TrsmCtx &c, const ftblas_fault_t &f) { return c.right ? f.j : f.i; }
+inline int64_t f_rhs(const TrsmCtx &c, const ftblas_fault_t &f) { return c.right ? f.i : f.j; }
+
 int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
   std::vector<ftd::DmrFault> lf;
   if (c.ft)
-    for (const auto &f : *c.faults)
-      if (f.i >= r0 && f.i < r0 + mb && f.step >= r0 && f.step < r0 + mb)
-        lf.push_back(ftd::DmrFault{f.j * ftt::LEAF + (f.i - r0), f.step - r0, f.delta});
+    for (const auto &f : *c.faults) {
+      const int64_t e = f_elem(c, f);
+      if (e >= r0 && e < r0 + mb && f.step >= r0 && f.step < r0 + mb)
+        lf.push_back(ftd::DmrFault{f_rhs(c, f) * ftt::LEAF + (e - r0), f.step - r0, f.delta});
+    }
   ftd::DmrFault *df = nullptr;
   if (!lf.empty()) {
     CUDA_TRY(cudaMallocAsync((void **)&df, sizeof(ftd::DmrFault) * lf.size(), c.st));
@@ -964,8 +972,12 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
   ftt::LeafParams P{};
   P.nb = (int)mb; P.n = (int)c.n;
   P.A = c.A + r0 + r0 * c.lda; P.lda = c.lda;
-  P.B = c.B + r0; P.ldb = c.ldb;
-  P.trans = c.trans; P.unit = c.unit;
+  // side L: element p of right-hand side j at B[(r0 + p) + j ldb]; side R: at B[j + (r0 + p) ldb],
+  // and the block is solved transposed (x S = b  <=>  S^T x^T = b^T)
+  P.es = c.right ? c.ldb : 1;
+  P.rs = c.right ? 1 : c.ldb;
+  P.B = c.B + r0 * P.es;
+  P.trans = c.right ? !c.trans : c.trans; P.unit = c.unit;
   P.f = df; P.nf = (int)lf.size(); P.cnt = c.leaf_sc->cnt;
   const int smem = (int)(sizeof(double) * (ftt::LEAF * ftt::LEAF + 2 * ftt::LEAF));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 16 * ftt::LEAF_NCOL - 1) / (16 * ftt::LEAF_NCOL),
@@ -996,13 +1008,23 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
 int trsm_update(TrsmCtx &c, int64_t R0, int64_t mr, int64_t K0, int64_t mk) {
   std::vector<ftblas_fault_t> gf;
   if (c.ft)
-    for (const auto &f : *c.faults)
-      if (f.i >= R0 && f.i < R0 + mr && f.step >= K0 && f.step < K0 + mk)
-        gf.push_back(ftblas_fault_t{f.i - R0, f.j, f.step - K0, f.delta});
-  const double *Asub = c.trans ? c.A + K0 + R0 * c.lda : c.A + R0 + K0 * c.lda;
-  if (c.sink) c.sink->row_off = R0;
-  return dgemm_core(c.ft, gf, c.trans ? 'T' : 'N', 'N', mr, c.n, mk, -1.0, Asub, c.lda, c.B + K0, c.ldb, 1.0,
-                    c.B + R0, c.ldb, nullptr, c.ft ? c.sink : nullptr);
+    for (const auto &f : *c.faults) {
+      const int64_t e = f_elem(c, f);
+      if (e >= R0 && e < R0 + mr && f.step >= K0 && f.step < K0 + mk)
+        gf.push_back(c.right ? ftblas_fault_t{f.i, e - R0, f.step - K0, f.delta}
+                             : ftblas_fault_t{e - R0, f.j, f.step - K0, f.delta});
+    }
+  if (!c.right) {  // B[R0.., :] -= op(A)[R0.., K0..] X[K0.., :]
+    const double *Asub = c.trans ? c.A + K0 + R0 * c.lda : c.A + R0 + K0 * c.lda;
+    if (c.sink) { c.sink->row_off = R0; c.sink->col_off = 0; }
+    return dgemm_core(c.ft, gf, c.trans ? 'T' : 'N', 'N', mr, c.n, mk, -1.0, Asub, c.lda, c.B + K0, c.ldb, 1.0,
+                      c.B + R0, c.ldb, nullptr, c.ft ? c.sink : nullptr);
+  }
+  // side R: B[:, R0..] -= X[:, K0..] op(A)[K0.., R0..]
+  const double *Asub = c.trans ? c.A + R0 + K0 * c.lda : c.A + K0 + R0 * c.lda;
+  if (c.sink) { c.sink->row_off = 0; c.sink->col_off = R0; }
+  return dgemm_core(c.ft, gf, 'N', c.trans ? 'T' : 'N', c.n, mr, mk, -1.0, c.B + K0 * c.ldb, c.ldb, Asub, c.lda, 1.0,
+                    c.B + R0 * c.ldb, c.ldb, nullptr, c.ft ? c.sink : nullptr);
 }
 
 int trsm_rec(TrsmCtx &c, int64_t r0, int64_t m) {
@@ -1021,7 +1043,8 @@ int trsm_rec(TrsmCtx &c, int64_t r0, int64_t m) {
 int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
                const double *A, int64_t lda, double *B, int64_t ldb, ftblas_err_report_t *err) {
   std::vector<ftblas_fault_t> faults = take_armed();
-  if (side != 'L' && side != 'l') return -1;
+  const bool right = side == 'R' || side == 'r';
+  if (!right && side != 'L' && side != 'l') return -1;
   const bool lower = uplo == 'L' || uplo == 'l';
   if (!lower && uplo != 'U' && uplo != 'u') return -2;
   if (!is_n(transa) && !is_t(transa)) return -3;
@@ -1029,20 +1052,25 @@ int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m,
   if (!unit && diag != 'N' && diag != 'n') return -4;
   if (m < 0) return -5;
   if (n < 0) return -6;
+  const int64_t na = right ? n : m;  // order of op(A)
   if (m > 0 && n > 0 && alpha != 0.0 && A == nullptr) return -8;
-  if (lda < std::max<int64_t>(1, m)) return -9;
+  if (lda < std::max<int64_t>(1, na)) return -9;
   if (m > 0 && n > 0 && B == nullptr) return -10;
   if (ldb < std::max<int64_t>(1, m)) return -11;
-  zero_report(err, m);
+  zero_report(err, na);
   if (err) { err->unit_k = 0; }
   if (m == 0 || n == 0) return 0;
   if (int e = ensure_device_init()) return e;
   cudaStream_t st = tl_stream;
   const bool trans = is_t(transa);
-  const bool fwd = lower != trans;  // op(A) lower -> forward substitution
-  for (const auto &f : faults)
-    if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step >= m || (fwd ? f.step >= f.i : f.step <= f.i))
+  // Substitution order along the solve: side L runs over rows and goes forward when op(A) is
+  // lower; side R runs over columns and goes forward when op(A) is upper.
+  const bool fwd = right ? lower == trans : lower != trans;
+  for (const auto &f : faults) {
+    const int64_t e = right ? f.j : f.i;
+    if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step >= na || (fwd ? f.step >= e : f.step <= e))
       return 3;
+  }
   if (alpha != 1.0) {
     const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, (int64_t)num_sms() * 16);
     ftt::scale_b_kernel<<<blocks, 256, 0, st>>>(m, n, alpha, B, ldb);
@@ -1058,8 +1086,8 @@ int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m,
   std::vector<ftblas_fault_t> none;
   DmrScratch lsc;
   if (int e = dmr_prepare(false, none, 1, 0, lsc, st)) return e;  // leaf counters only
-  TrsmCtx c{ft, fwd, trans, unit, (int64_t)ftt::LEAF, A, lda, B, ldb, n, &faults, &sink, &lsc, st};
-  int r = trsm_rec(c, 0, m);
+  TrsmCtx c{ft, fwd, trans, unit, right, (int64_t)ftt::LEAF, A, lda, B, ldb, right ? m : n, &faults, &sink, &lsc, st};
+  int r = trsm_rec(c, 0, na);
   if (r == 0 && err && ft) {
     r = finish_report(err, sink.counters, sink.events, ev_cap, sink.units, st);
     unsigned long long lc[ftd::D_N];

@@ -34,8 +34,8 @@ struct LeafParams {
   int nb, n;
   const double *A;  // caller's A at (r0, r0)
   int64_t lda;
-  double *B;        // B at row r0
-  int64_t ldb;
+  double *B;        // the block's first element of right-hand side 0
+  int64_t es, rs;   // element stride within a right-hand side, stride between right-hand sides
   bool trans, unit;
   const ftd::DmrFault *f;  // faults of this block: index = j * LEAF + local row i, step = local p
   int nf;
@@ -162,11 +162,11 @@ __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
 #pragma unroll
     for (int cc = 0; cc < NCOL; ++cc) {
       const bool jv = j0 + cc < P.n;
-      const double *col = P.B + (int64_t)(j0 + cc) * P.ldb;
+      const double *col = P.B + (int64_t)(j0 + cc) * P.rs;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int p = lane + 32 * q;
-        b[DMR ? 2 * cc : cc][q] = jv && p < nb ? col[p] : 0.0;
+        b[DMR ? 2 * cc : cc][q] = jv && p < nb ? col[(int64_t)p * P.es] : 0.0;
         if (DMR) b[2 * cc + 1][q] = b[2 * cc][q];
       }
     }
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
     for (int cc = 0; cc < NCOL; ++cc) {
       const int j = j0 + cc;
       if (j >= P.n) break;
-      double *col = P.B + (int64_t)j * P.ldb;
+      double *col = P.B + (int64_t)j * P.rs;
       double *out = b[DMR ? 2 * cc : cc];
       if (DMR) {
         bool bad = false;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
           // wherever the two disagreed.
           double b3[1][4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) b3[0][q] = lane + 32 * q < nb ? col[lane + 32 * q] : 0.0;
+          for (int q = 0; q < 4; ++q) b3[0][q] = lane + 32 * q < nb ? col[(int64_t)(lane + 32 * q) * P.es] : 0.0;
           const int nfi[1] = {-1}, nfs[1] = {-1};
           const double nfd[1] = {0.0};
           leaf_solve<FWD, 1, false, false>(Sc, b3, r2, r2, lane, nslots, nfi, nfs, nfd);
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (lane + 32 * q < nb) col[lane + 32 * q] = out[q];
+        if (lane + 32 * q < nb) col[(int64_t)(lane + 32 * q) * P.es] = out[q];
     }
   }
 }

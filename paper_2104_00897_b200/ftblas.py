@@ -267,7 +267,8 @@ def ftblas_dgemv_noft(trans, m, n, alpha, A, lda, x, incx, beta, y, incy):
 
 def ftblas_dtrsm(side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, *, report=True,
                  events_capacity=4096):
-    """FT-DTRSM (NEXT-3): B := alpha op(A)^-1 B on device pointers; returns a Report."""
+    """FT-DTRSM (NEXT-3): B := alpha op(A)^-1 B (side 'L') or alpha B op(A)^-1 (side 'R') on
+    device pointers; returns a Report."""
     L = load()
     evbuf = (Event * max(events_capacity, 1))()
     r = ErrReport()

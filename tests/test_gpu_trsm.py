@@ -97,9 +97,55 @@ def test_dtrsm_argument_errors():
     A = to_dev(np.eye(4))
     Bd = to_dev(np.ones((4, 2)))
     with pytest.raises(FtblasError):
-        F.ftblas_dtrsm("R", "L", "N", "N", 4, 2, 1.0, A, 4, Bd, 4)
+        F.ftblas_dtrsm("X", "L", "N", "N", 4, 2, 1.0, A, 4, Bd, 4)
+    with pytest.raises(FtblasError):  # side R: A is n x n, lda >= n
+        F.ftblas_dtrsm("R", "L", "N", "N", 2, 4, 1.0, A, 3, to_dev(np.ones((2, 4))), 2)
     with pytest.raises(FtblasError):
         F.ftblas_dtrsm("L", "X", "N", "N", 4, 2, 1.0, A, 4, Bd, 4)
     F.ftblas_inject_arm([(1, 0, 3, 1.0)])  # forward solve: step must precede the row
     with pytest.raises(FtblasError):
         F.ftblas_dtrsm("L", "L", "N", "N", 4, 2, 1.0, A, 4, Bd, 4)
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("tr", ["N", "T"])
+@pytest.mark.parametrize("diag", ["N", "U"])
+def test_dtrsm_right_side_against_oracle(uplo, tr, diag):
+    """Side R: X op(A) = alpha B, A n x n, every uplo / trans / diag."""
+    rng = np.random.default_rng(hash(("R", uplo, tr, diag)) % 1000)
+    for (m, n) in [(1, 1), (64, 100), (3, 128), (257, 129), (40, 300), (130, 700)]:
+        A = wellcond(rng, n, uplo)
+        B = np.asfortranarray(rng.uniform(-1, 1, (m, n)))
+        dB = to_dev(B)
+        rep = F.ftblas_dtrsm("R", uplo, tr, diag, m, n, -0.5, to_dev(A), n, dB, m)
+        Xg = from_dev(dB, m, n)
+        Xo, _ = oracle.dtrsm(uplo, tr, diag, m, n, -0.5, A, n, B, m, side="R")
+        Xo = Xo.reshape((n, m)).T
+        assert np.max(np.abs(Xg - Xo)) <= 64 * n * U * max(np.max(np.abs(Xo)), 1e-300)
+        assert rep.detected == 0
+
+
+@pytest.mark.parametrize("uplo,tr", [("L", "N"), ("U", "N"), ("L", "T"), ("U", "T")])
+def test_dtrsm_right_side_integer_exact_with_faults(uplo, tr):
+    rng = np.random.default_rng(17)
+    m, n = 260, 300
+    T = rng.integers(-1, 2, (n, n)).astype(float)
+    T = np.asfortranarray((np.tril(T, -1) if uplo == "L" else np.triu(T, 1)) + np.eye(n))
+    X = rng.integers(-3, 4, (m, n)).astype(float)
+    B = np.asfortranarray(X @ (T.T if tr == "T" else T))
+    fwd = (uplo == "L") == (tr == "T")  # side R: op(A) upper -> columns ascending
+    # (i, j, p): row i, column j, step p preceding j in the substitution order; GEMM-update
+    # faults (j and p in different 128-column blocks) and diagonal-block (DMR) faults
+    pairs = [(5, 290, 10), (140, 150, 3), (250, 200, 140), (60, 60, 30), (200, 250, 240)]
+    faults = [((i, j, p, 13.0) if fwd else (i, n - 1 - j, n - 1 - p, -7.0)) for (i, j, p) in pairs]
+    dB = to_dev(B)
+    F.ftblas_inject_arm(faults)
+    rep = F.ftblas_dtrsm("R", uplo, tr, "U", m, n, 1.0, to_dev(T), n, dB, m)
+    assert np.array_equal(from_dev(dB, m, n), X)
+    assert (rep.detected, rep.corrected, rep.recomputed) == (5, 5, 0)
+    L = 128
+    cross = sorted((f[0], f[1]) for f in faults if f[1] // L != f[2] // L)
+    assert len(cross) >= 2 and sorted((e[1], e[2]) for e in rep.events) == cross
+    d2 = to_dev(B)
+    F.ftblas_dtrsm_noft("R", uplo, tr, "U", m, n, 1.0, to_dev(T), n, d2, m)
+    assert np.array_equal(from_dev(d2, m, n), X)
