@@ -67,7 +67,15 @@ def main():
                           "torch_solve_triangular_tflops": flops / t_ref / 1e9,
                           "faults_report": {"detected": rep.detected, "corrected": rep.corrected,
                                             "recomputed": rep.recomputed, "units": rep.units_checked}}), flush=True)
-        del A, Acm, B0, B
+        # side R on the same sizes: X op(A) = B with op(A) = A^T (upper), every row an RHS
+        t_ftr = timed(lambda: F.ftblas_dtrsm("R", "L", "T", "N", m, n, 1.0, Acm, m, B, m, report=False), reset)
+        t_nor = timed(lambda: F.ftblas_dtrsm_noft("R", "L", "T", "N", m, n, 1.0, Acm, m, B, m), reset)
+        t_refr = timed(lambda: torch.linalg.solve_triangular(A.t(), Bt, upper=True, left=False), lambda: None)
+        print(json.dumps({"routine": "dtrsm R L T N", "m": m, "n": n, "ms_ft": t_ftr, "ms_noft": t_nor,
+                          "tflops_ft": flops / t_ftr / 1e9, "tflops_noft": flops / t_nor / 1e9,
+                          "overhead_pct": 100 * (t_ftr - t_nor) / t_nor,
+                          "torch_solve_triangular_tflops": flops / t_refr / 1e9}), flush=True)
+        del A, Acm, B0, B, Bt
 
 
 if __name__ == "__main__":
