@@ -46,21 +46,25 @@ def test_fuzz_against_oracle(seed):
     B = np.asfortranarray(rng.standard_normal((k, n)))
     C0 = np.asfortranarray(rng.uniform(-1, 1, (m, n)))
     As, Bs = stored(A, ta), stored(B, tb)
-    lda, ldb = As.shape[0], Bs.shape[0]
+    # leading dimensions: tight, or padded (odd pads take the library's aligned-repack path)
+    pad_a, pad_b = (int(x) for x in rng.choice([0, 0, 1, 3], 2))
+    lda, ldb = As.shape[0] + pad_a, Bs.shape[0] + pad_b
     F.ftblas_set_interval(kc)
     try:
         with encode_mode(F, mode):
             F.ftblas_inject_arm(faults)
             if host:
                 Cg = np.asfortranarray(C0.copy())
-                rep = F.ftblas_dgemm_host(ta, tb, m, n, k, alpha, As, lda, Bs, ldb, beta, Cg, m)
+                Ap = np.zeros((lda, As.shape[1]), order="F"); Ap[:As.shape[0]] = As
+                Bp = np.zeros((ldb, Bs.shape[1]), order="F"); Bp[:Bs.shape[0]] = Bs
+                rep = F.ftblas_dgemm_host(ta, tb, m, n, k, alpha, Ap, lda, Bp, ldb, beta, Cg, m)
             else:
                 dC = to_dev(C0)
-                rep = F.ftblas_dgemm(ta, tb, m, n, k, alpha, to_dev(As), lda, to_dev(Bs), ldb, beta, dC, m)
+                rep = F.ftblas_dgemm(ta, tb, m, n, k, alpha, to_dev(As, lda), lda, to_dev(Bs, ldb), ldb, beta, dC, m)
                 Cg = from_dev(dC, m, n)
     finally:
         F.ftblas_set_interval(0)
-    Co, orep = oracle.dgemm_abft(ta, tb, m, n, k, alpha, As, lda, Bs, ldb, beta, C0, m,
+    Co, orep = oracle.dgemm_abft(ta, tb, m, n, k, alpha, As, As.shape[0], Bs, Bs.shape[0], beta, C0, m,
                                  BM=rep.unit_rows, BN=rep.unit_cols, BK=rep.step_quantum,
                                  Kc=rep.unit_k, faults=faults)
     Co = Co.reshape((n, m)).T
