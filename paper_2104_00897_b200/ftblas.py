@@ -139,14 +139,25 @@ def _check(fn, status):
         raise FtblasError(fn, status, load().ftblas_status_string(status).decode())
 
 
-def _ptr(x):
+def _ptr(x, where="device"):
+    """Address of an operand: a raw int, a float64 torch tensor, or (host entry points) a
+    float64 numpy array.  where = "device" (CUDA tensors only) or "host" (numpy or CPU
+    tensors).  Marshalling checks only: shapes and leading dimensions are the library's."""
     if x is None:
         return None
     if isinstance(x, int):
         return x
     if hasattr(x, "data_ptr"):  # torch tensor
+        if str(x.dtype) != "torch.float64":
+            raise TypeError(f"float64 tensor expected, got {x.dtype}")
+        if (where == "device") != bool(x.is_cuda):
+            raise ValueError(f"{'CUDA' if where == 'device' else 'host'} tensor expected")
         return x.data_ptr()
     if hasattr(x, "ctypes"):  # numpy array
+        if where == "device":
+            raise ValueError("device entry point: pass a CUDA tensor (or a device address), not a numpy array")
+        if str(x.dtype) != "float64":
+            raise TypeError(f"float64 array expected, got {x.dtype}")
         return x.ctypes.data
     raise TypeError(type(x))
 
@@ -216,15 +227,15 @@ def ftblas_dgemm_host(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, l
     r = ErrReport()
     r.events = evbuf
     r.events_capacity = events_capacity
-    st = L.ftblas_dgemm_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb,
-                             beta, _ptr(C), ldc, ctypes.byref(r) if report else None)
+    st = L.ftblas_dgemm_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A, "host"), lda, _ptr(B, "host"), ldb,
+                             beta, _ptr(C, "host"), ldc, ctypes.byref(r) if report else None)
     _check("ftblas_dgemm_host", st)
     return _report(r, evbuf) if report else None
 
 
 def ftblas_dgemm_noft_host(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc):
-    st = load().ftblas_dgemm_noft_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A), lda,
-                                       _ptr(B), ldb, beta, _ptr(C), ldc)
+    st = load().ftblas_dgemm_noft_host(_c(transA), _c(transB), m, n, k, alpha, _ptr(A, "host"), lda,
+                                       _ptr(B, "host"), ldb, beta, _ptr(C, "host"), ldc)
     _check("ftblas_dgemm_noft_host", st)
 
 
