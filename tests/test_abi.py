@@ -107,3 +107,19 @@ def test_option_setters_validate_without_a_gpu():
     assert L.ftblas_set_interval(20) == 4 and L.ftblas_set_interval(-16) == 4
     assert L.ftblas_set_correction(1) == 0 and L.ftblas_set_correction(0) == 0
     assert L.ftblas_set_correction(2) == 4
+
+
+def test_binding_rejects_wrong_operand_kinds():
+    """Marshalling checks of the binding (no GPU needed): device entry points take CUDA
+    tensors or raw addresses, host entry points numpy arrays or CPU tensors, float64 only."""
+    import numpy as np
+    import torch
+    a64 = np.zeros((4, 4))
+    with pytest.raises(ValueError):
+        F.ftblas_dgemm("N", "N", 4, 4, 4, 1.0, a64, 4, a64, 4, 0.0, a64, 4)
+    with pytest.raises(ValueError):
+        F.ftblas_dgemm_noft("N", "N", 4, 4, 4, 1.0, torch.zeros(16, dtype=torch.float64), 4, 0x1000, 4, 0.0, 0x1000, 4)
+    with pytest.raises(TypeError):
+        F.ftblas_dgemm_host("N", "N", 4, 4, 4, 1.0, a64.astype(np.float32), 4, a64, 4, 0.0, a64, 4)
+    with pytest.raises(TypeError):
+        F.ftblas_dscal(16, 2.0, torch.zeros(16, dtype=torch.float32), 1)
