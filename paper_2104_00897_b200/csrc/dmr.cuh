@@ -293,64 +293,86 @@ struct GemvParams {
   unsigned long long *cnt;
 };
 
-__device__ __forceinline__ double gemv_n_row(const GemvParams &P, int64_t i) {  // third computation
+// LPR lanes share a row (LPR = 1, 2, 4: 32, 16, 8 rows per CTA, so moderate m still fills the
+// machine); lane part q of warp w sums the columns j = w LPR + q (mod GN_W LPR) in order, the
+// LPR parts combine by a fixed xor butterfly (commutative: every lane of the row gets the same
+// value), then the warps in order.
+template <int LPR>
+__device__ __forceinline__ double gemv_n_row(const GemvParams &P, int64_t i) {  // third computation, same order
+  constexpr int S = GN_W * LPR;
   double acc = 0.0;
   for (int w = 0; w < GN_W; ++w) {
-    double part = 0.0;
-    for (int64_t j = w; j < P.n; j += GN_W) part = v_fma(P.A[i + j * P.lda], P.x[vidx(j, P.n, P.incx)], part);
-    acc = w == 0 ? part : v_add(acc, part);
+    double part[LPR];
+#pragma unroll
+    for (int q = 0; q < LPR; ++q) {
+      part[q] = 0.0;
+      for (int64_t j = w * LPR + q; j < P.n; j += S) part[q] = v_fma(P.A[i + j * P.lda], P.x[vidx(j, P.n, P.incx)], part[q]);
+    }
+    double t = part[0];
+    if (LPR == 2) t = v_add(part[0], part[1]);
+    if (LPR == 4) t = v_add(v_add(part[0], part[1]), v_add(part[2], part[3]));
+    acc = w == 0 ? t : v_add(acc, t);
   }
   return acc;
 }
 
-template <bool DMR, bool FLT>
+template <bool DMR, bool FLT, int LPR>
 __global__ void __launch_bounds__(GN_W * 32, 4) dgemv_n_kernel(const GemvParams P) {
-  __shared__ double part[2][GN_W][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  constexpr int RPC = 32 / LPR, S = GN_W * LPR;  // rows per CTA, column stride of a lane part
+  __shared__ double part[2][GN_W][RPC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, r = lane / LPR, q = lane % LPR;
+  const int64_t i = (int64_t)blockIdx.x * RPC + r;
   const bool row_ok = i < P.m;
   const int64_t ir = row_ok ? i : 0;
+  const int64_t j0 = w * LPR + q;  // this lane's first column
   double a1 = 0.0, a2 = 0.0;
-  // This lane's fault (row i, term `step` in this warp's column set), if any.
+  // This lane's fault (row i, term `step` in this lane's column set), if any.
   int64_t fstep = -1;
   double fdel = 0.0;
   if (DMR && FLT && row_ok) {
     int lo = 0, hi = P.nf;
     while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.f[mid].index < i) lo = mid + 1; else hi = mid; }
     for (; lo < P.nf && P.f[lo].index == i; ++lo)
-      if (P.f[lo].step < P.n && (P.f[lo].step % GN_W) == w) { fstep = P.f[lo].step; fdel += P.f[lo].delta; }
+      if (P.f[lo].step < P.n && (P.f[lo].step % S) == j0) { fstep = P.f[lo].step; fdel += P.f[lo].delta; }
   }
   const double *Ai = P.A + ir;
-  int64_t j = w;
-  for (; j + (GN_U - 1) * GN_W < P.n; j += GN_U * GN_W) {  // GN_U columns of this warp's set
+  int64_t j = j0;
+  for (; j + (GN_U - 1) * S < P.n; j += GN_U * S) {  // GN_U columns of this lane's set
     double av[GN_U], xv[GN_U];
 #pragma unroll
     for (int u = 0; u < GN_U; ++u) {
-      av[u] = Ai[(j + GN_W * u) * P.lda];
-      xv[u] = P.x[vidx(j + GN_W * u, P.n, P.incx)];
+      av[u] = Ai[(j + S * u) * P.lda];
+      xv[u] = P.x[vidx(j + S * u, P.n, P.incx)];
     }
 #pragma unroll
     for (int u = 0; u < GN_U; ++u) {
-      if (DMR && FLT && (j + GN_W * u) == fstep) a1 = v_add(a1, fdel);
+      if (DMR && FLT && (j + S * u) == fstep) a1 = v_add(a1, fdel);
       a1 = v_fma(av[u], xv[u], a1);
       if (DMR) a2 = v_fma(av[u], xv[u], a2);
     }
   }
-  for (; j < P.n; j += GN_W) {
+  for (; j < P.n; j += S) {
     const double av = Ai[j * P.lda], xv = P.x[vidx(j, P.n, P.incx)];
     if (DMR && FLT && j == fstep) a1 = v_add(a1, fdel);
     a1 = v_fma(av, xv, a1);
     if (DMR) a2 = v_fma(av, xv, a2);
   }
-  part[0][w][lane] = a1;
-  part[1][w][lane] = a2;
-  __syncthreads();
-  if (w != 0) return;
-  double s1 = part[0][0][lane], s2 = part[1][0][lane];
 #pragma unroll
-  for (int q = 1; q < GN_W; ++q) {
-    s1 = v_add(s1, part[0][q][lane]);
-    if (DMR) s2 = v_add(s2, part[1][q][lane]);
+  for (int o = 1; o < LPR; o <<= 1) {  // the row's lane parts: fixed butterfly
+    a1 = v_add(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+    if (DMR) a2 = v_add(a2, __shfl_xor_sync(0xffffffffu, a2, o));
+  }
+  if (q == 0) {
+    part[0][w][r] = a1;
+    part[1][w][r] = a2;
+  }
+  __syncthreads();
+  if (w != 0 || q != 0) return;
+  double s1 = part[0][0][r], s2 = part[1][0][r];
+#pragma unroll
+  for (int u = 1; u < GN_W; ++u) {
+    s1 = v_add(s1, part[0][u][r]);
+    if (DMR) s2 = v_add(s2, part[1][u][r]);
   }
   if (!row_ok) return;
   if (DMR && FLT) s1 = v_add(s1, fault_delta(P.f, P.nf, i, P.n));  // faults after the last term
@@ -361,7 +383,7 @@ __global__ void __launch_bounds__(GN_W * 32, 4) dgemv_n_kernel(const GemvParams 
     const double yb2 = P.beta != 0.0 ? v_mul(P.beta, *yi) : 0.0;
     const double r2 = v_fma(P.alpha, s2, yb2);
     if (__any_sync(__activemask(), differ(r1, r2)) && differ(r1, r2))
-      r1 = settle(r1, r2, v_fma(P.alpha, gemv_n_row(P, i), yb2), P.cnt);
+      r1 = settle(r1, r2, v_fma(P.alpha, gemv_n_row<LPR>(P, i), yb2), P.cnt);
   }
   *yi = r1;
 }

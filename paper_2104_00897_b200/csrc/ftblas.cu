@@ -13,6 +13,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <cstdlib>
 #include <cmath>
@@ -914,10 +915,19 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
   P.y = y; P.incy = incy; P.f = sc.f; P.nf = sc.nf; P.cnt = sc.cnt;
   if (alpha == 0.0 || len == 0) { P.m = tr ? 0 : m; P.n = tr ? n : 0; }  // y = beta*y: empty dot products
   if (!tr) {
-    const unsigned g = (unsigned)((m + 31) / 32);
-    if (ft && sc.nf) ftd::dgemv_n_kernel<true, true><<<g, ftd::GN_W * 32, 0, st>>>(P);
-    else if (ft) ftd::dgemv_n_kernel<true, false><<<g, ftd::GN_W * 32, 0, st>>>(P);
-    else ftd::dgemv_n_kernel<false, false><<<g, ftd::GN_W * 32, 0, st>>>(P);
+    // lanes per row: the smallest of 1, 2, 4 that gives at least 512 CTAs (~3.5 waves); 4 below
+    // (8 lanes per row measured slower at m = 2048)
+    const int lpr = m >= 512 * 32 ? 1 : (m >= 512 * 16 ? 2 : 4);
+    const unsigned g = (unsigned)((m + 32 / lpr - 1) / (32 / lpr));
+    auto launch = [&](auto lprc) {
+      constexpr int L = decltype(lprc)::value;
+      if (ft && sc.nf) ftd::dgemv_n_kernel<true, true, L><<<g, ftd::GN_W * 32, 0, st>>>(P);
+      else if (ft) ftd::dgemv_n_kernel<true, false, L><<<g, ftd::GN_W * 32, 0, st>>>(P);
+      else ftd::dgemv_n_kernel<false, false, L><<<g, ftd::GN_W * 32, 0, st>>>(P);
+    };
+    if (lpr == 1) launch(std::integral_constant<int, 1>{});
+    else if (lpr == 2) launch(std::integral_constant<int, 2>{});
+    else launch(std::integral_constant<int, 4>{});
   } else {
     const unsigned g = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * ftd::GT_CTAS);
     if (ft && sc.nf) ftd::dgemv_t_kernel<true, true><<<g, 256, 0, st>>>(P);
