@@ -105,6 +105,11 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (process spawn, NVML init) must not overlap the timed region
+            # of a short workload: wait for its first sample (bounded).
+            t_end = time.time() + 5.0
+            while not self.samples and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -310,15 +315,20 @@ def main():
         return None
 
     def timed(ft, steps, warmup, label=None):
+        # Collect before the warm-up (a collection between warm-up and timed region leaves the
+        # GPU idle for milliseconds, and the first timed step of a short workload then pays the
+        # ramp back up), and no collector pause inside the timed region.
+        gc.collect()
+        gc.disable()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        for e in ev:  # create the CUDA events outside the timed region
+            e.record(stream)
         for _ in range(warmup):
             step(ft)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         F.ftblas_take_launch_count()
-        gc.collect()
-        gc.disable()  # no collector pause inside the timed region (the reported call syncs per step)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         ev[0].record(stream)
         reps = []
         for i in range(steps):

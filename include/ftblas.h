@@ -159,12 +159,13 @@ int ftblas_set_correction(int mode);
 /* Where ftblas_dgemm forms the checksums e^T A_I and B_J e:
  *   FTBLAS_ENCODE_FUSED (default): in the kernel, from the very tiles staged for the MMA
  *     (the paper's fused encoding, §V.B), each checksum encoded once where the
- *     hardware lets tiles share it: e^T A_I by the tile of tile column 0 and published per
- *     stage through L2 to the other tiles of row I (a tile whose stage is not published yet
- *     encodes it itself: nothing ever waits), B_J e split between the two CTAs of a cluster
- *     pair.  Library scratch: 8 m/127 k + 8 m/127 ceil(k/16) bytes;
+ *     hardware lets tiles share it: e^T A_I by the tile of tile column 0 and B_J e by the
+ *     tile of tile row 0, published per stage through L2 to the other tiles of row I /
+ *     column J (a tile whose stage is not published yet encodes it itself: nothing ever
+ *     waits; launches of a single wave encode locally).  Library scratch when shared:
+ *     8 (m/127 + n/127) k + 4 (m/127 + n/127) ceil(k/16) bytes;
  *   FTBLAS_ENCODE_FUSED_LOCAL: in the kernel, every CTA encodes both of its operand tiles
- *     itself (B_J e still split within cluster pairs);
+ *     itself (B_J e split between the two CTAs of a cluster pair);
  *   FTBLAS_ENCODE_PREPASS: two memory-bound passes over A and B before the kernel; the
  *     kernel copies the pre-encoded 16 k-slots into the checksum row of each staged tile.
  * All feed the same in-kernel carry (C^f) and fused epilogue verification.  FUSED and

@@ -93,21 +93,21 @@ struct Params {
   const unsigned int *amax_pre, *bmax_pre;
   // Row-shared fused encode (encode mode FUSED): the tile of tile column 0 encodes e^T A_I from
   // its staged tiles and publishes it per stage through L2 -- Ash[ti*ldash + p] for the 16
-  // k-slots (k contiguous: one 128-byte line per stage), the slice's R1' high-word maximum
-  // hmA[ti*nk + sg] and a release flag aflag[ti*nk + sg] = 1 (sg = global stage index).  Every other tile of row I copies a
-  // published stage when its flag is already set and otherwise encodes that stage itself (same
-  // integer encode of the same staged data: bitwise the same checksum), so no CTA ever waits on
-  // another.  Null = every CTA encodes A itself.
+  // k-slots (k contiguous: one 128-byte line per stage) and the slice's R1' high-word maximum
+  // hmA[ti*nk + sg] (sg = global stage index), relaxed stores into buffers the host filled with
+  // all-ones bytes.  Every other tile of row I loads the stage's words before waiting for its
+  // TMA bytes and copies them when none reads all-ones; otherwise it encodes that stage itself
+  // (same integer encode of the same staged data: bitwise the same checksum), so no CTA ever
+  // waits on another.  Null = every CTA encodes A itself.
   double *Ash;
   int64_t ldash;
-  unsigned int *hmA, *aflag;
-  // B_J e the same way along tile columns: the tile of tile row 0 publishes Bsh[tj*ldbsh + p],
-  // hmB[tj*nk + sg] and counts its published stages in bcnt[tj + t*tiles_n]; a tile (or
-  // cluster pair) that finds the count complete when it starts copies every stage, otherwise
-  // it encodes B_J e itself (split within the cluster pair).  Null = no sharing.
+  unsigned int *hmA;
+  // B_J e the same way along tile columns: the tile of tile row 0 publishes Bsh[tj*ldbsh + p]
+  // and hmB[tj*nk + sg]; the other tiles of column J copy or encode per stage.  Null = no
+  // sharing (cluster-pair launches split the B encode instead).
   double *Bsh;
   int64_t ldbsh;
-  unsigned int *hmB, *bcnt;
+  unsigned int *hmB;
   unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
   int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
                                   // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait,
@@ -128,14 +128,30 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+// Relaxed (morally strong, unordered) accesses for the checksum publication (R22): every
+// published word is validated on its own against the all-ones fill, so no flag, fence or
+// acquire is needed and the loads do not block until their values are used.
+__device__ __forceinline__ double ld_relaxed_gpu(const double *p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p));
+  return v;
 }
+__device__ __forceinline__ void st_relaxed_gpu(double *p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned *p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// The publication buffers are filled with all-ones bytes before the launch: an all-ones double
+// is a NaN that fx_to_double never produces, an all-ones maximum has the sign bit that R1'
+// masks off, so a word that reads all-ones is simply not published yet.
+__device__ __forceinline__ bool pub_ok(double v) { return __double_as_longlong(v) != -1ll; }
+__device__ __forceinline__ bool pub_ok(unsigned v) { return v != 0xFFFFFFFFu; }
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -702,34 +718,32 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   const bool a_pub = P.Ash && x.tj == 0, a_sub = P.Ash && x.tj != 0;
   const bool b_pub = P.Bsh && x.ti == 0;
   struct PubA { bool ok; double a0, a1; uint32_t am; };
+  // Relaxed loads of stage s's published e^T A_I words (not used until after the TMA wait).
   auto fetch_a = [&](int s) {
-    PubA f{false, 0.0, 0.0, 0u};
+    PubA f{false, 0.0, 0.0, 0xFFFFFFFFu};
     if (!a_sub) return f;
     const int64_t sg = x.k0 / BK + s;  // global stage index
-    const size_t fi = (size_t)x.ti * P.nk + sg;
-    unsigned ready = 0;
-    if (lane == 0) {
-      ready = ld_acquire_gpu(P.aflag + fi);
-      // development / tests: dev mode 256 waits for the publication (exercises the copy path)
-      while ((P.dev_mode & 256) && !ready) {
-        __nanosleep(256);
-        ready = ld_acquire_gpu(P.aflag + fi);
-      }
+    const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
+    const int64_t pg = x.k0 + (int64_t)s * BK + p;
+    const double *src = P.Ash + x.ti * P.ldash + pg;
+    if (AKM) {
+      f.a0 = lane < 8 && pg < x.k1 ? ld_relaxed_gpu(src) : 0.0;
+      f.a1 = lane < 8 && pg + 1 < x.k1 ? ld_relaxed_gpu(src + 1) : 0.0;
+    } else {
+      f.a0 = lane < 16 && pg < x.k1 ? ld_relaxed_gpu(src) : 0.0;
     }
-    f.ok = __shfl_sync(0xffffffffu, ready, 0) != 0;
-    __syncwarp();  // orders the other lanes' loads after lane 0's acquire
-    if (f.ok) {
-      const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
-      const int64_t pg = x.k0 + (int64_t)s * BK + p;
-      if (AKM) {
-        f.a0 = lane < 8 && pg < x.k1 ? __ldcg(P.Ash + x.ti * P.ldash + pg) : 0.0;
-        f.a1 = lane < 8 && pg + 1 < x.k1 ? __ldcg(P.Ash + x.ti * P.ldash + pg + 1) : 0.0;
-      } else {
-        f.a0 = lane < 16 && pg < x.k1 ? __ldcg(P.Ash + x.ti * P.ldash + pg) : 0.0;
-      }
-      f.am = __ldcg(P.hmA + fi);
-    }
+    f.am = ld_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg);
     return f;
+  };
+  // Whole stage published?  (warp-uniform; dev mode 256 waits for it: tests of the copy path)
+  auto check_a = [&](int s, PubA &f) {
+    if (!a_sub) return;
+    f.ok = __all_sync(0xffffffffu, pub_ok(f.a0) && pub_ok(f.a1) && pub_ok(f.am));
+    while ((P.dev_mode & 256) && !f.ok) {
+      __nanosleep(256);
+      f = fetch_a(s);
+      f.ok = __all_sync(0xffffffffu, pub_ok(f.a0) && pub_ok(f.a1) && pub_ok(f.am));
+    }
   };
   auto enc_a = [&](double *sA, int s, const PubA &f, double &a0, double &a1, uint32_t &amax) {
     if (f.ok) {
@@ -743,62 +757,53 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     amax = max(amax, hm);
     if (a_pub) {
       const int64_t sg = x.k0 / BK + s;
-      const size_t fi = (size_t)x.ti * P.nk + sg;
       const int p = AKM ? 2 * lane : lane;
       const int64_t pg = x.k0 + (int64_t)s * BK + p;
+      double *dst = P.Ash + x.ti * P.ldash + pg;
       if (AKM) {
-        if (lane < 8 && pg < x.k1) P.Ash[x.ti * P.ldash + pg] = a0;
-        if (lane < 8 && pg + 1 < x.k1) P.Ash[x.ti * P.ldash + pg + 1] = a1;
+        if (lane < 8 && pg < x.k1) st_relaxed_gpu(dst, a0);
+        if (lane < 8 && pg + 1 < x.k1) st_relaxed_gpu(dst + 1, a1);
       } else if (lane < 16 && pg < x.k1) {
-        P.Ash[x.ti * P.ldash + pg] = a0;
+        st_relaxed_gpu(dst, a0);
       }
-      if (lane == 0) P.hmA[fi] = hm;
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_gpu(P.aflag + fi, 1u);
+      if (lane == 0) st_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg, hm);
     }
   };
   for (int attempt = 0;; ++attempt) {
     const bool verify = FT && attempt == 0;
     if (lane == 0)
       for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
-    // (after the first TMA loads are in flight) B_J e fully published by tile row 0 (same
-    // interval, same stage count) when this encoder warp starts?  Then it copies every one of
-    // its stages; otherwise it encodes them (bitwise the same checksum, so the four encoder
-    // warps need not agree).  Publication only happens in launches without clusters, so a
-    // cluster pair never mixes the two.
-    bool bcopy = false;
-    if (verify && P.Bsh && x.ti != 0) {
-      unsigned done = 0;
-      if (lane == 0) {
-        const unsigned *cnt = P.bcnt + x.tj + (size_t)x.t * P.tiles_n;
-        done = ld_acquire_gpu(cnt) >= (unsigned)nk;
-        // development / tests: dev mode 512 waits for tile row 0 to finish publishing, so
-        // every other tile takes the copy path
-        while ((P.dev_mode & 512) && !done) {
-          __nanosleep(1000);
-          done = ld_acquire_gpu(cnt) >= (unsigned)nk;
-        }
-      }
-      bcopy = __shfl_sync(0xffffffffu, done, 0) != 0;
-      __syncwarp();  // orders the other lanes' copies after lane 0's acquire
-    }
-    const bool share = verify && tl.share && !bcopy;
+    // B_J e published by tile row 0 is copied per stage like e^T A_I.  Publication only
+    // happens in launches without clusters, so a cluster pair (share) never copies.
+    const bool b_sub = P.Bsh && x.ti != 0;
+    const bool share = verify && tl.share;
     uint32_t amax_hi = 0u, bmax_hi = 0u;
     for (int s = warp; s < nk; s += N_ENC_WARPS) {
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
-        const PubA pa = (P.Ac || (P.dev_mode & 3)) ? PubA{false, 0.0, 0.0, 0u} : fetch_a(s);
-        // B_J e copy (whole tile decided at its start): fetched before the TMA wait as well
+        const bool pubs = !(P.Ac || (P.dev_mode & 3));
+        PubA pa = pubs ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
+        // B_J e words of this stage: relaxed loads before the TMA wait as well
         double pb = 0.0;
-        uint32_t pbm = 0u;
-        if (bcopy) {
+        uint32_t pbm = 0xFFFFFFFFu;
+        auto fetch_b = [&]() {
           const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-          pb = lane < 16 && pg < x.k1 ? __ldcg(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
-          pbm = __ldcg(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
-        }
+          pb = lane < 16 && pg < x.k1 ? ld_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
+          pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
+        };
+        if (pubs && b_sub) fetch_b();
         if (!(P.dev_mode & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
+        if (pubs) check_a(s, pa);
+        bool bcopy = false;
+        if (pubs && b_sub) {
+          bcopy = __all_sync(0xffffffffu, pub_ok(pb) && pub_ok(pbm));
+          while ((P.dev_mode & 512) && !bcopy) {  // tests: wait for tile row 0 (copy path)
+            __nanosleep(256);
+            fetch_b();
+            bcopy = __all_sync(0xffffffffu, pub_ok(pb) && pub_ok(pbm));
+          }
+        }
         const long long t1 = P.dev_prof ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
@@ -810,7 +815,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         } else if (P.dev_mode & 1) {  // development: pass 1 only
           amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
           bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
-        } else if ((P.dev_mode & 2) && !share && !bcopy) {
+        } else if ((P.dev_mode & 2) && !share) {
           // development: no encode (checksum rows zero)
         } else {
           enc_a(sA, s, pa, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
@@ -867,11 +872,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
             if (b_pub) {  // tile row 0: publish this stage's B_J e for the other tile rows
               __syncwarp();
               const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-              if (lane < 16 && pg < x.k1) P.Bsh[x.tj * P.ldbsh + pg] = sB[sidx<BKM>(x.crb, lane)];
-              if (lane == 0) P.hmB[(size_t)x.tj * P.nk + sg] = hmb;
-              __threadfence();
-              __syncwarp();
-              if (lane == 0) atomicAdd(P.bcnt + x.tj + (size_t)x.t * P.tiles_n, 1u);
+              if (lane < 16 && pg < x.k1) st_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg, sB[sidx<BKM>(x.crb, lane)]);
+              if (lane == 0) st_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + sg, hmb);
             }
           }
         }

@@ -62,11 +62,13 @@ int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &
   }
   ftk::Params p = p0;
   p.total = (int)grid.x;
-  // Encode mode FUSED_LOCAL: 2-CTA clusters share the B_J encode (cluster size 2 packs all 148
-  // SMs).  With the checksums shared through L2 (FUSED, R22) nearly every tile copies B_J e, and
-  // pair co-scheduling costs more than the split saves (C5-like 4.0% -> 3.9%, C4a 9.2% -> 7.8%),
-  // so those launches are plain.
-  if (FT && !p.Ac && !p.Ash && !p.Bsh && !(p.dev_mode & 128)) {
+  // Encode mode FUSED_LOCAL (p.cluster2 requested by the caller): 2-CTA clusters share the B_J
+  // encode (cluster size 2 packs all 148 SMs).  With the checksums shared through L2 (FUSED,
+  // R22) nearly every tile copies B_J e, and pair co-scheduling costs more than the split saves
+  // (C5-like 4.0% -> 3.9%, C4a 9.2% -> 7.8%); a single-wave FUSED launch, which skips the
+  // sharing, is also faster plain (1016^2 x 256: first-stage wait 10.2k vs 11.6k clocks), so
+  // FUSED launches are plain.
+  if (FT && p.cluster2 && !p.Ac && !p.Ash && !p.Bsh && !(p.dev_mode & 128)) {
     p.cluster2 = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((grid.x + 1) & ~1u);
@@ -175,6 +177,70 @@ std::vector<ftblas_fault_t> take_armed() {
   return faults;
 }
 
+int num_sms();
+
+// Per-thread pinned host buffer for the report read-back (grown on demand, never shrunk).
+cudaError_t pinned_report_buffer(size_t bytes, char **out) {
+  static thread_local char *buf = nullptr;
+  static thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 4096);
+    const cudaError_t e = cudaHostAlloc((void **)&buf, want, cudaHostAllocPortable);
+    if (e != cudaSuccess) { buf = nullptr; return e; }
+    cap = want;
+  }
+  *out = buf;
+  return cudaSuccess;
+}
+
+// Per-thread pinned staging for the armed-fault list's host->device copy.  The buffer is reused
+// once the event recorded after its last copy has completed (normally long before: the copy is
+// the first thing on the stream in the previous call).
+struct FaultStage {
+  char *buf = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  int dev = -1;
+  bool pending = false;
+};
+thread_local FaultStage tl_fstage;
+cudaError_t pinned_fault_stage(size_t bytes, char **out) {
+  FaultStage &f = tl_fstage;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (f.pending) {
+    if ((e = cudaEventSynchronize(f.done)) != cudaSuccess) return e;
+    f.pending = false;
+  }
+  if (f.done && f.dev != dev) {  // events belong to one device
+    cudaEventDestroy(f.done);
+    f.done = nullptr;
+  }
+  if (!f.done) {
+    if ((e = cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    f.dev = dev;
+  }
+  if (bytes > f.cap) {
+    if (f.buf) cudaFreeHost(f.buf);
+    f.buf = nullptr;
+    f.cap = 0;
+    const size_t want = std::max<size_t>(bytes, 4096);
+    if ((e = cudaHostAlloc((void **)&f.buf, want, cudaHostAllocPortable)) != cudaSuccess) return e;
+    f.cap = want;
+  }
+  *out = f.buf;
+  return cudaSuccess;
+}
+cudaError_t pinned_fault_release(cudaStream_t st) {
+  const cudaError_t e = cudaEventRecord(tl_fstage.done, st);
+  tl_fstage.pending = e == cudaSuccess;
+  return e;
+}
+
 // Copy the device counters / events of one call into the caller's report (events sorted by
 // (interval, i, j)).  Synchronises the stream.
 int finish_report(ftblas_err_report_t *err, const unsigned long long *d_counters, const void *d_events,
@@ -185,18 +251,22 @@ int finish_report(ftblas_err_report_t *err, const unsigned long long *d_counters
   const ptrdiff_t gap = reinterpret_cast<const char *>(d_events) - reinterpret_cast<const char *>(d_counters);
   const bool joint = gap >= (ptrdiff_t)(sizeof(unsigned long long) * ftk::CNT_N) && gap <= 256;
   const int64_t e0 = joint ? std::min<int64_t>(E0, ev_cap) : 0;
-  std::vector<char> head((size_t)(joint ? gap : 0) + sizeof(ftk::EventDev) * (size_t)e0 + sizeof(unsigned long long) * ftk::CNT_N);
-  CUDA_TRY(cudaMemcpyAsync(head.data(), d_counters, joint ? (size_t)gap + sizeof(ftk::EventDev) * (size_t)e0
-                                                          : sizeof(unsigned long long) * ftk::CNT_N,
+  const size_t head_bytes = (size_t)(joint ? gap : 0) + sizeof(ftk::EventDev) * (size_t)e0 + sizeof(unsigned long long) * ftk::CNT_N;
+  // Pinned staging (per thread, grown on demand; safe to reuse because this function
+  // synchronises before returning): a pageable copy costs a driver staging pass per call.
+  char *head = nullptr;
+  CUDA_TRY(pinned_report_buffer(head_bytes, &head));
+  CUDA_TRY(cudaMemcpyAsync(head, d_counters, joint ? (size_t)gap + sizeof(ftk::EventDev) * (size_t)e0
+                                                   : sizeof(unsigned long long) * ftk::CNT_N,
                            cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   unsigned long long cnt[ftk::CNT_N];
-  std::memcpy(cnt, head.data(), sizeof cnt);
+  std::memcpy(cnt, head, sizeof cnt);
   const int64_t nev = (int64_t)cnt[ftk::CNT_EVENTS];
   const int64_t nstore = std::min<int64_t>(nev, ev_cap);
   std::vector<ftk::EventDev> ev((size_t)nstore);
   const int64_t have = std::min<int64_t>(nstore, e0);
-  if (have > 0) std::memcpy(ev.data(), head.data() + gap, sizeof(ftk::EventDev) * (size_t)have);
+  if (have > 0) std::memcpy(ev.data(), head + gap, sizeof(ftk::EventDev) * (size_t)have);
   if (nstore > have) {
     CUDA_TRY(cudaMemcpyAsync(ev.data() + have, reinterpret_cast<const ftk::EventDev *>(d_events) + have,
                              sizeof(ftk::EventDev) * (size_t)(nstore - have), cudaMemcpyDeviceToHost, st));
@@ -297,6 +367,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.wstride = 0;
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
   p.correct_mode = tl_correct;
+  p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL) ? 1 : 0;  // request; launch_one decides
   // development only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
   if (const char *dm = std::getenv("FTBLAS_DEV_MODE")) p.dev_mode = std::atoi(dm);
@@ -324,41 +395,42 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // Encode mode PREPASS: e^T A_I, B_J e and the block maxima from two memory passes.
   const bool prepass = ft && tl_encode == FTBLAS_ENCODE_PREPASS;
   auto al256 = [](size_t b) { return (b + 255) & ~size_t(255); };
-  // Tile-column-0 / tile-row-0 publication of e^T A_I / B_J e (encode mode FUSED): per-stage
-  // flags (A) / per-interval stage counts (B), the slice maxima and the published sums.
-  const bool ashare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_n > 1;
-  const bool bshare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_m > 1;
+  // Tile-column-0 / tile-row-0 publication of e^T A_I / B_J e (encode mode FUSED, R22): the
+  // slice maxima and the published sums, filled with all-ones bytes (= not yet published).
+  // Launches of a single wave skip it (every tile starts together, so a consumer would almost
+  // never find a stage published) unless dev modes 256 / 512 force the copy paths.
+  const bool one_wave = (int64_t)p.ntiles * T <= (int64_t)num_sms() && !(dev_mode & (256 | 512));
+  const bool ashare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_n > 1 && !one_wave;
+  const bool bshare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_m > 1 && !one_wave;
   const size_t nsg = (size_t)p.nk;  // global stages over the whole k
-  const size_t aflag_bytes = ashare ? al256(sizeof(unsigned) * (size_t)p.tiles_m * nsg) : 0;
-  const size_t bcnt_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * (size_t)T) : 0;
-  // Scratch: [aflag | bcnt | counters (64 B) | events | faults] ... the first three zeroed by one
-  // memset, counters and the first events read back by one copy (finish_report).
-  const size_t zero_bytes = aflag_bytes + bcnt_bytes + 64;
-  const size_t base_bytes = al256(zero_bytes + ev_bytes + f_bytes);
+  // Scratch: [counters (64 B) | events | faults | prepass | hmA Ash | hmB Bsh]: the counters
+  // zeroed, the publication region filled with 0xFF; counters and the first events are read
+  // back by one copy (finish_report).
+  const size_t base_bytes = al256(64 + ev_bytes + f_bytes);
   const size_t hm_bytes = al256(sizeof(unsigned) * (p.tiles_m + p.tiles_n));
   const size_t pre_bytes = prepass ? hm_bytes + sizeof(double) * (size_t)(p.tiles_m + p.tiles_n) * k : 0;
-  const size_t hma_bytes = ashare ? aflag_bytes : 0;
+  const size_t hma_bytes = ashare ? al256(sizeof(unsigned) * (size_t)p.tiles_m * nsg) : 0;
   const size_t ash_bytes = ashare ? hma_bytes + al256(sizeof(double) * (size_t)p.tiles_m * (size_t)k) : 0;
   const size_t hmb_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * nsg) : 0;
   const size_t bsh_bytes = bshare ? hmb_bytes + sizeof(double) * (size_t)p.tiles_n * (size_t)k : 0;
   char *scratch = nullptr;
   CUDA_TRY(cudaMallocAsync((void **)&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes, st));
-  char *const cnt_ptr = scratch + aflag_bytes + bcnt_bytes;
+  char *const cnt_ptr = scratch;
   if (ashare) {
     char *sb = scratch + base_bytes + pre_bytes;
-    p.aflag = reinterpret_cast<unsigned *>(scratch);
     p.hmA = reinterpret_cast<unsigned *>(sb);
     p.Ash = reinterpret_cast<double *>(sb + hma_bytes);
     p.ldash = k;
   }
   if (bshare) {
     char *sb = scratch + base_bytes + pre_bytes + ash_bytes;
-    p.bcnt = reinterpret_cast<unsigned *>(scratch + aflag_bytes);
     p.hmB = reinterpret_cast<unsigned *>(sb);
     p.Bsh = reinterpret_cast<double *>(sb + hmb_bytes);
     p.ldbsh = k;
   }
-  CUDA_TRY(cudaMemsetAsync(scratch, 0, zero_bytes, st));
+  CUDA_TRY(cudaMemsetAsync(scratch, 0, 64, st));
+  if (ash_bytes + bsh_bytes)
+    CUDA_TRY(cudaMemsetAsync(scratch + base_bytes + pre_bytes, 0xFF, ash_bytes + bsh_bytes, st));
   if (prepass) {
     char *pb = scratch + base_bytes;
     auto *hm = reinterpret_cast<unsigned *>(pb);
@@ -378,8 +450,13 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   if (sink && ft) sink->units += (int64_t)p.ntiles * T;
   p.faults = fd.empty() ? nullptr : reinterpret_cast<const ftk::FaultDev *>(cnt_ptr + 64 + ev_bytes);
   p.nfaults = (int)fd.size();
-  if (!fd.empty())  // pageable source: the call returns once the source has been staged
-    CUDA_TRY(cudaMemcpyAsync(cnt_ptr + 64 + ev_bytes, fd.data(), f_bytes, cudaMemcpyHostToDevice, st));
+  if (!fd.empty()) {
+    char *stage = nullptr;
+    CUDA_TRY(pinned_fault_stage(f_bytes, &stage));
+    std::memcpy(stage, fd.data(), f_bytes);
+    CUDA_TRY(cudaMemcpyAsync(cnt_ptr + 64 + ev_bytes, stage, f_bytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(pinned_fault_release(st));
+  }
 
   const bool akm = is_t(ta), bkm = is_n(tb);
   // TMA needs 16-byte aligned bases and leading dimensions: repack otherwise (device copy
