@@ -240,7 +240,11 @@ int ftblas_dgemv_noft(char trans, int64_t m, int64_t n, double alpha, const doub
  *   side 'R': X op(A) = alpha B (B = alpha B op(A)^-1), A n x n;
  * uplo 'L'/'U', transa 'N'/'T'/'C', diag 'N'/'U' (unit diagonal: not read); B m x n; device
  * pointers, column-major.  Recursive blocked algorithm along the solve (B's rows for side L,
- * its columns for side R): diagonal blocks of <= 128 starting at multiples of 128 are solved by
+ * its columns for side R): a block of len > 128 positions (in substitution order) is split
+ * into its first len - u positions, solved first, and its last u positions, updated by the
+ * coupling GEMM and then solved: u = 254 j with j = floor((len + 254) / 508) reduced until
+ * u < len, or u = 126 when j = 0 (whole 127-row tiles of the protected kernel, even block
+ * boundaries); diagonal blocks of <= 128 are solved by
  * a DMR kernel that multiplies by packed reciprocals of the diagonal, the
  * coupling updates (B2 -= op(A)21 X1, or B2 -= X1 op(A)12 on the right) run on the protected
  * DMMA kernel (fused ABFT, this library's ftblas_dgemm path).  err (nullable) sums both: the

@@ -1018,7 +1018,7 @@ int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const do
 // ---------------------------------------------------------------- FT-DTRSM (NEXT-3)
 
 // op(A) X = alpha B, side 'L'.  Recursive blocked solve: a block of more than LEAF rows is
-// split (first part a multiple of LEAF), the parts are solved recursively and the coupling
+// split (the updated part a multiple of 127, see trsm_rec), the parts are solved recursively and the coupling
 // is a GEMM update B2 -= op(A)21 X1 (forward, op(A) lower) or B1 -= op(A)12 X2 (backward, op(A)
 // upper) through the protected DMMA kernel (fused ABFT, report accumulated in a sink); the
 // leaves are the DMR diagonal-block kernel of trsm.cuh.  A fault (i, j, step = p) perturbs the
@@ -1116,7 +1116,17 @@ int trsm_update(TrsmCtx &c, int64_t R0, int64_t mr, int64_t K0, int64_t mk) {
 
 int trsm_rec(TrsmCtx &c, int64_t r0, int64_t m) {
   if (m <= c.leaf) return trsm_leaf(c, r0, m);
-  const int64_t m1 = ((m / 2) + c.leaf - 1) / c.leaf * c.leaf, m2 = m - m1;
+  // The part the coupling GEMM updates is u = 254 j rows, j = round(m / 508) (reduced until
+  // u < m), else 126: whole tile rows of the protected kernel's 127-row grid (a power-of-two
+  // split leaves a sliver tile row that costs a wave of its own: 256 x 8192 x 256 87% over
+  // the unprotected kernel, 254 x 8192 x 254 10.5%) and even, so every block boundary keeps
+  // the operands 16-byte aligned for TMA (an odd one costs a repack copy).  The part solved
+  // first takes the rest (leaves <= LEAF).  Both twins use the same split, so their results
+  // stay bitwise equal.
+  int64_t j = (m + 2 * ftk::TM) / (4 * ftk::TM);
+  while (j > 0 && 2 * ftk::TM * j >= m) --j;
+  const int64_t u = j > 0 ? 2 * ftk::TM * j : ftk::TM - 1;
+  const int64_t m1 = c.fwd ? m - u : u, m2 = m - m1;
   if (c.fwd) {
     if (int e = trsm_rec(c, r0, m1)) return e;
     if (int e = trsm_update(c, r0 + m1, m2, r0, m1)) return e;

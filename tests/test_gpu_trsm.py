@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.helpers import from_dev, to_dev
+from tests.helpers import from_dev, to_dev, trsm_leaf_ids
 
 pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
@@ -60,7 +60,7 @@ def test_dtrsm_integer_exact_with_faults(uplo, tr):
     m, n = 300, 300
     T, B, X = integer_system(rng, m, n, uplo, tr)
     fwd = (uplo == "L") != (tr == "T")
-    # (i, j, p): GEMM-update faults (i and p in different 128-row blocks) and diagonal-block
+    # (i, j, p): GEMM-update faults (i and p in different diagonal blocks) and diagonal-block
     # (DMR) faults (same block); p before i in the substitution order; the columns put every
     # fault in its own 127 x 127 unit of whichever update it lands in.
     pairs = [(290, 5, 10), (150, 140, 3), (200, 270, 140), (60, 60, 30), (250, 200, 240)]
@@ -72,8 +72,8 @@ def test_dtrsm_integer_exact_with_faults(uplo, tr):
     assert (rep.detected, rep.corrected, rep.recomputed) == (5, 5, 0)
     # the cross-block faults landed in GEMM updates: ABFT events with global rows; the others
     # were settled by the DMR diagonal-block solves (counted, no event)
-    L = 128  # diagonal-block height of the solve (include/ftblas.h)
-    cross = sorted((f[0], f[1]) for f in faults if f[0] // L != f[2] // L)
+    leaf = trsm_leaf_ids(m)  # diagonal blocks of the solve, substitution order (include/ftblas.h)
+    cross = sorted((f[0], f[1]) for f, (i, j, p) in zip(faults, pairs) if leaf[i] != leaf[p])
     assert len(cross) >= 2 and sorted((e[1], e[2]) for e in rep.events) == cross
     assert all(e[3] == 1 for e in rep.events)
 
@@ -135,7 +135,7 @@ def test_dtrsm_right_side_integer_exact_with_faults(uplo, tr):
     B = np.asfortranarray(X @ (T.T if tr == "T" else T))
     fwd = (uplo == "L") == (tr == "T")  # side R: op(A) upper -> columns ascending
     # (i, j, p): row i, column j, step p preceding j in the substitution order; GEMM-update
-    # faults (j and p in different 128-column blocks) and diagonal-block (DMR) faults
+    # faults (j and p in different diagonal blocks) and diagonal-block (DMR) faults
     pairs = [(5, 290, 10), (140, 150, 3), (250, 200, 140), (60, 60, 30), (200, 250, 240)]
     faults = [((i, j, p, 13.0) if fwd else (i, n - 1 - j, n - 1 - p, -7.0)) for (i, j, p) in pairs]
     dB = to_dev(B)
@@ -143,8 +143,8 @@ def test_dtrsm_right_side_integer_exact_with_faults(uplo, tr):
     rep = F.ftblas_dtrsm("R", uplo, tr, "U", m, n, 1.0, to_dev(T), n, dB, m)
     assert np.array_equal(from_dev(dB, m, n), X)
     assert (rep.detected, rep.corrected, rep.recomputed) == (5, 5, 0)
-    L = 128
-    cross = sorted((f[0], f[1]) for f in faults if f[1] // L != f[2] // L)
+    leaf = trsm_leaf_ids(n)
+    cross = sorted((f[0], f[1]) for f, (i, j, p) in zip(faults, pairs) if leaf[j] != leaf[p])
     assert len(cross) >= 2 and sorted((e[1], e[2]) for e in rep.events) == cross
     d2 = to_dev(B)
     F.ftblas_dtrsm_noft("R", uplo, tr, "U", m, n, 1.0, to_dev(T), n, d2, m)
