@@ -1067,7 +1067,8 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
   P.trans = c.right ? !c.trans : c.trans; P.unit = c.unit;
   P.f = df; P.nf = (int)lf.size(); P.cnt = c.leaf_sc->cnt;
   const int smem = (int)(sizeof(double) * (ftt::LEAF * ftt::LEAF + 2 * ftt::LEAF));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 16 * ftt::LEAF_NCOL - 1) / (16 * ftt::LEAF_NCOL),
+  constexpr int per_cta = ftt::LEAF_THREADS / 32 * ftt::LEAF_NCOL;  // right-hand sides per CTA pass
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + per_cta - 1) / per_cta,
                                                               (int64_t)num_sms()));
   using K = void (*)(ftt::LeafParams);
   // [fwd][dmr][faults]
@@ -1084,7 +1085,7 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
       CUDA_TRY(cudaFuncSetAttribute(kernels[a >> 2][(a >> 1) & 1][a & 1], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     if (dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
   }
-  kernels[c.fwd][c.ft][c.ft && P.nf > 0]<<<grid, 512, smem, c.st>>>(P);
+  kernels[c.fwd][c.ft][c.ft && P.nf > 0]<<<grid, ftt::LEAF_THREADS, smem, c.st>>>(P);
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());
   if (df) CUDA_TRY(cudaFreeAsync(df, c.st));

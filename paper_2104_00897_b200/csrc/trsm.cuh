@@ -120,10 +120,17 @@ __device__ __forceinline__ void leaf_solve(const double *Sc, double (&b)[NCOL * 
   }
 }
 
-constexpr int LEAF_NCOL = 2;  // right-hand sides per warp pass
+#ifndef FTBLAS_LEAF_NCOL
+#define FTBLAS_LEAF_NCOL 2
+#endif
+#ifndef FTBLAS_LEAF_THREADS
+#define FTBLAS_LEAF_THREADS 512
+#endif
+constexpr int LEAF_NCOL = FTBLAS_LEAF_NCOL;        // right-hand sides per warp pass
+constexpr int LEAF_THREADS = FTBLAS_LEAF_THREADS;  // threads per CTA (one CTA per SM: the block fills shared memory)
 
 template <bool FWD, bool DMR, bool FLT>
-__global__ void __launch_bounds__(512) trsm_leaf_kernel(const LeafParams P) {
+__global__ void __launch_bounds__(LEAF_THREADS) trsm_leaf_kernel(const LeafParams P) {
   extern __shared__ double sm[];
   double *Sc = sm, *rd1 = sm + LEAF * LEAF, *rd2 = rd1 + LEAF;
   const int nb = P.nb, tid = threadIdx.x, lane = tid & 31, nslots = (nb + 31) >> 5;

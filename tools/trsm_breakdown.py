@@ -1,10 +1,12 @@
 """Dev: device time of one protected and one unprotected DTRSM (side L, lower, N) by kernel,
-from the torch profiler (CUPTI).  argv[1] = m = n (default 8192)."""
+from the torch profiler (CUPTI).  argv[1] = m = n (default 8192), argv[2] = library (optional)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from torch.profiler import profile, ProfilerActivity
 from paper_2104_00897_b200 import ftblas as F
+if len(sys.argv) > 2:
+    F.LIB_PATH = sys.argv[2]
 
 m = n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 A = torch.rand(m, m, dtype=torch.float64, device="cuda") / m
