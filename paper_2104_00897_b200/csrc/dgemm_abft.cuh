@@ -778,12 +778,24 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     const bool b_sub = P.Bsh && x.ti != 0;
     const bool share = verify && tl.share;
     uint32_t amax_hi = 0u, bmax_hi = 0u;
-    for (int s = warp; s < nk; s += N_ENC_WARPS) {
+    // Encode jobs.  Stages 0..3 of the tile: the two operands of a stage go to two warps
+    // (warps 0, 2 share stages 0 and 2, warps 1, 3 stages 1 and 3; warps 0, 1 take A of stages
+    // 0 / 1 and B of 2 / 3, warps 2, 3 the opposite), so the first stage -- on the critical path
+    // at every tile start -- is encoded in about half the time of one warp doing both
+    // (dev_timeline at 1016^2 x 256: first-stage wait 10.4k -> 6.3k clk).  From stage 4 on,
+    // warp s % 4 encodes both operands of stage s (splitting every stage costs the long
+    // shapes 0.2-0.3%).  The TMA issue stays with warp s % 4 throughout.
+    bool split = verify;  // the unprotected kernel and recompute passes only issue TMA loads
+    for (int s = verify ? (warp & 1) : warp;; s += split ? 2 : N_ENC_WARPS) {
+      if (split && s >= N_ENC_WARPS) { split = false; s = warp + N_ENC_WARPS; }
+      if (s >= nk) break;
+      const bool doA = !split || ((((s >> 1) & 1) == 0) == (warp < 2));
+      const bool doB = !split || !doA;
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
         const long long t0 = P.dev_prof ? clock64() : 0;
         const bool pubs = !(P.Ac || (P.dev_mode & 3));
-        PubA pa = pubs ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
+        PubA pa = pubs && doA ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
         // B_J e words of this stage: relaxed loads before the TMA wait as well
         double pb = 0.0;
         uint32_t pbm = 0xFFFFFFFFu;
@@ -792,11 +804,11 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           pb = lane < 16 && pg < x.k1 ? ld_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
           pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
         };
-        if (pubs && b_sub) fetch_b();
+        if (pubs && doB && b_sub) fetch_b();
         if (!(P.dev_mode & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
-        if (pubs) check_a(s, pa);
+        if (pubs && doA) check_a(s, pa);
         bool bcopy = false;
-        if (pubs && b_sub) {
+        if (pubs && doB && b_sub) {
           bcopy = __all_sync(0xffffffffu, pub_ok(pb) && pub_ok(pbm));
           while ((P.dev_mode & 512) && !bcopy) {  // tests: wait for tile row 0 (copy path)
             __nanosleep(256);
@@ -808,22 +820,26 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
         if (P.Ac) {  // PREPASS: copy the pre-encoded 16 k-slots of e^T A_I / B_J e
-          const int64_t p = x.k0 + s * BK + (lane & 15);
-          const double v = p < x.k1 ? (lane < 16 ? P.Ac[x.ti + p * P.ldac] : P.Br[x.tj + p * P.ldbr]) : 0.0;
-          if (lane < 16) sA[sidx<AKM>(x.cra, lane)] = v;
-          else sB[sidx<BKM>(x.crb, lane & 15)] = v;
+          const int64_t p = x.k0 + s * BK + lane;
+          if (lane < 16) {
+            if (doA) sA[sidx<AKM>(x.cra, lane)] = p < x.k1 ? P.Ac[x.ti + p * P.ldac] : 0.0;
+            if (doB) sB[sidx<BKM>(x.crb, lane)] = p < x.k1 ? P.Br[x.tj + p * P.ldbr] : 0.0;
+          }
         } else if (P.dev_mode & 1) {  // development: pass 1 only
-          amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
-          bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
+          if (doA) amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
+          if (doB) bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
         } else if ((P.dev_mode & 2) && !share) {
           // development: no encode (checksum rows zero)
         } else {
+         if (doA) {
           enc_a(sA, s, pa, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           if (AKM) {
             if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
           } else {
             if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
           }
+         }
+         if (doB) {
           const int64_t sg = x.k0 / BK + s;  // global stage index
           if (bcopy) {  // B_J e of this stage as published by tile row 0
             if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pb;
@@ -876,10 +892,14 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
               if (lane == 0) st_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + sg, hmb);
             }
           }
+         }
         }
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tl.enc[slot]);
+        if (lane == 0) {  // one arrival per operand job (the barrier expects two per stage)
+          mbar_arrive(&tl.enc[slot]);
+          if (doA && doB) mbar_arrive(&tl.enc[slot]);
+        }
         if (P.dev_prof && lane == 0) {
           const long long t2 = clock64();
           unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + warp) * 2;
@@ -887,8 +907,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           dp[1] += (unsigned long long)(t2 - t1);
         }
       }
-      const int s2 = s + N_ENC_WARPS;  // this warp's next stage beyond the first ring
-      if (lane == 0 && s2 >= STAGES && s2 < nk) issue(s2);
+      const int s2 = s + N_ENC_WARPS;  // the next stage of this warp's TMA ring slots
+      if (lane == 0 && (s & 3) == warp && s2 >= STAGES && s2 < nk) issue(s2);
       __syncwarp();
     }
     if (verify && !P.Ac && lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
@@ -1248,7 +1268,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&tl.full[s], 1);
-      mbar_init(&tl.enc[s], 1);
+      mbar_init(&tl.enc[s], 2);  // the A and the B encode job
       mbar_init(&tl.empty[s], N_MMA_WARPS);
     }
     tl.amax_hi = P.Ac ? P.amax_pre[ti] : 0u;
