@@ -674,7 +674,8 @@ struct Ctx {
 // ring slot) and, in the protected pass, waits for stage s's bytes, forms
 // a_sum[p] = sum_{i in I} op(A)_ip and b_sum[p] = sum_{j in J} op(B)_pj for the 16 k-slots,
 // writes them into the free row cr of the staged A tile and of the staged B tile, and arrives
-// on the stage's `enc` barrier.  The DMMA stream then computes C^f = [A; e^T A][B, B e]
+// on the stage's `enc` barrier (one arrival per operand: a tile's stages 0..3 split their A
+// and B encodes between two warps, see the job loop).  The DMMA stream then computes C^f = [A; e^T A][B, B e]
 // tile by tile: acc(cr, j) is the carried column checksum (e^T A_I) B_J and
 // acc(i, cr) the carried row checksum A_I (B_J e) (outer-product maintenance).
 // One encoder per SM sub-partition spreads the encode's issue slots evenly over the four DMMA
