@@ -67,8 +67,6 @@ def lib():
         L.oracle_dgemm_abft_units.argtypes = [c, c, i64, i64, i64, d, P, i64, P, i64, d, P, i64,
                                               i64, i64, i64, i64, ctypes.c_int, P, i64, P, i64,
                                               P, P, i64]
-        L.oracle_round_up_hi32.restype = d
-        L.oracle_round_up_hi32.argtypes = [d]
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_dscal.argtypes = [i64, d, P, i64, P, i64, P]
         L.oracle_daxpy.argtypes = [i64, d, P, i64, P, i64, P, i64, P]
@@ -98,11 +96,6 @@ def gamma(n: int) -> float:
 
 def tau(kt: int, length: int, amax: float, bmax: float) -> float:
     return lib().oracle_tau(kt, length, amax, bmax)
-
-
-def round_up_hi32(x: float) -> float:
-    """Reading R1': x rounded up to the largest double with the same high 32-bit word."""
-    return lib().oracle_round_up_hi32(x)
 
 
 def col_sums(M: np.ndarray) -> np.ndarray:

@@ -24,11 +24,10 @@
  *     (PAPER.md:91); the reading used is the rigorous per-unit bound R1:
  *       tau_col = 2*gamma(kt+bm)*kt*bm*amax*bmax,  tau_row = 2*gamma(kt+bn)*kt*bn*amax*bmax
  *     with gamma(n) = n*u/(1-n*u), u = 2^-53, kt = k accumulated so far, and amax / bmax
- *     the largest |op(A)_ip| / |op(B)_pj| of the unit ROUNDED UP to the largest double
- *     with the same high 32 bits, a non-finite element counting as DBL_MAX (reading R1',
- *     a larger threshold is still rigorous; the rounding lets the kernel track
- *     maxima on 32-bit words; a unit with a non-finite input is flagged by its NaN/Inf
- *     residual whatever the threshold).
+ *     the largest |op(A)_ip| / |op(B)_pj| of the unit read so far (exact maxima; a NaN
+ *     element is ignored by the max, an infinite one makes it infinite).  tau is then
+ *     clamped to the largest finite double (reading R13: non-finite inputs), so a
+ *     residual that is NaN or infinite always flags.
  *   - Multi-flag units (out of the paper's one-error model) are recomputed once
  *     without re-verification (reading R6/R13).
  *   - Injected faults: acc_ij += delta after step_q rank-1 updates, with
@@ -70,18 +69,6 @@ double oracle_gamma(int64_t n) {
 double oracle_tau(int64_t kt, int64_t len, double amax, double bmax) {
   return 2.0 * oracle_gamma(kt + len) * (double)kt * (double)len * amax * bmax;
 }
-
-/* Reading R1': max |x| (non-finite x counting as DBL_MAX), then rounded up to the largest double sharing its
- * high 32-bit word (low word all ones).  An all-zero unit gives 0x00000000FFFFFFFF. */
-static double round_up_hi32(double m) {
-  uint64_t b;
-  memcpy(&b, &m, sizeof b);
-  b |= 0xFFFFFFFFull;
-  double r;
-  memcpy(&r, &b, sizeof r);
-  return r;
-}
-double oracle_round_up_hi32(double m) { return round_up_hi32(m); }
 
 /* op(A)(r, c) for a column-major matrix with leading dimension ld;
  * trans 'N' reads M[r + c*ld], 'T'/'C' reads M[c + r*ld] (real data: C == T). */
@@ -223,14 +210,12 @@ static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t 
       for (int64_t i = 0; i < bm; ++i) {
         double a = op_at(x->A, x->lda, x->tA, i0 + i, p);
         a_sum += a;
-        if (!isfinite(a)) amax = DBL_MAX;
-        else if (fabs(a) > amax) amax = fabs(a);
+        if (fabs(a) > amax) amax = fabs(a);
       }
       for (int64_t j = 0; j < bn; ++j) {
         double b = op_at(x->B, x->ldb, x->tB, p, j0 + j);
         b_sum += b;
-        if (!isfinite(b)) bmax = DBL_MAX;
-        else if (fabs(b) > bmax) bmax = fabs(b);
+        if (fabs(b) > bmax) bmax = fabs(b);
       }
 
       /* Rank-1 update of C (C_s = A(:,s) B(s,:)). */
@@ -258,10 +243,12 @@ static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t 
       r_row[i] = s;
     }
 
-    /* Compare against the maintained checksums; flag where not |d| <= tau (NaN flags; R13). */
-    const double amax_r = round_up_hi32(amax), bmax_r = round_up_hi32(bmax);  /* R1' */
-    const double tau_col = oracle_tau(pe, bm, amax_r, bmax_r);
-    const double tau_row = oracle_tau(pe, bn, amax_r, bmax_r);
+    /* Compare against the maintained checksums; flag where not |d| <= tau (R1), tau clamped
+     * to the largest finite double so that a NaN or infinite residual flags (R13). */
+    double tau_col = oracle_tau(pe, bm, amax, bmax);
+    double tau_row = oracle_tau(pe, bn, amax, bmax);
+    if (!(tau_col <= DBL_MAX)) tau_col = DBL_MAX;
+    if (!(tau_row <= DBL_MAX)) tau_row = DBL_MAX;
     int64_t nfr = 0, nfc = 0, fr = -1, fc = -1;
     for (int64_t i = 0; i < bm; ++i) {
       d_row[i] = r_row[i] - cs_row[i];

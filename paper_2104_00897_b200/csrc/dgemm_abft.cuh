@@ -957,7 +957,8 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
       const double nu = (double)(kt + len) * 0x1p-53;
       // DESIGN.md R1, R17: 2 gamma(kt + len) for the two sums plus 2^-50 = 8u for the fixed-point
       // encode (per element below 2^-50 max|x|, summed over len rows and kt k-slots).
-      const double tau = (2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx;
+      // Clamped to the largest finite double (R13): a NaN or infinite residual always flags.
+      const double tau = fmin((2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx, 0x1.fffffffffffffp1023);
       const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
       const bool flag = valid && !(fabs(d) <= tau) && !(P.dev_mode & 4);
       tl.dres[vt] = d;

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) verify_kernel(const VerifyParams P) {
   const double bmx = __longlong_as_double((long long)(((unsigned long long)P.bmax_hi[J] << 32) | 0xFFFFFFFFull));
   const int len = is_row ? bn : bm;
   const double nu = (double)(P.k + len) * 0x1p-53;
-  const double tau = 2.0 * (nu / (1.0 - nu)) * (double)P.k * (double)len * amx * bmx;  // DESIGN.md R1
+  const double tau = fmin(2.0 * (nu / (1.0 - nu)) * (double)P.k * (double)len * amx * bmx, 0x1.fffffffffffffp1023);  // R1, R13
   const bool flag = valid && !(fabs(d) <= tau);
   dres[tid] = d;
   if (flag) atomicMin(is_row ? &first_row : &first_col, c);

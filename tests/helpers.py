@@ -38,14 +38,12 @@ def bound(case_like, A, B, C0, alpha, beta, ta, tb, k):
 
 
 def unit_tau(A, B, ta, tb, i, j, BM, BN, k):
-    """tau_col, tau_row of the unit containing (i, j) (R1), numpy maxima."""
+    """tau_col, tau_row of the unit containing (i, j) (R1, exact maxima), numpy."""
     oA, oB = op(A, ta), op(B, tb)
     I0, J0 = (i // BM) * BM, (j // BN) * BN
     Ia, Jb = oA[I0:I0 + BM, :], oB[:, J0:J0 + BN]
-    import oracle
-    big = np.finfo(np.float64).max
-    amax = oracle.round_up_hi32(float(np.where(np.isfinite(Ia), np.abs(Ia), big).max(initial=0.0)))
-    bmax = oracle.round_up_hi32(float(np.where(np.isfinite(Jb), np.abs(Jb), big).max(initial=0.0)))
+    amax = float(np.nanmax(np.abs(Ia), initial=0.0))
+    bmax = float(np.nanmax(np.abs(Jb), initial=0.0))
     bm, bn = Ia.shape[0], Jb.shape[1]
     g = lambda nn: nn * U / (1 - nn * U)  # noqa: E731
     return (2 * g(k + bm) * k * bm * amax * bmax, 2 * g(k + bn) * k * bn * amax * bmax)

@@ -258,15 +258,40 @@ def test_no_false_positives_float_inputs():
         assert rep.detected == 0
 
 
-def test_round_up_hi32_definition():
-    """R1': keep the high word, set the low 32 bits: an upper bound within 2^-20 relative."""
-    import struct
-    for x in [1.0, 0.1, 5.3, 1e-300, 7.5e300, 0.0]:
-        r = oracle.round_up_hi32(x)
-        bx, br = (struct.unpack("<Q", struct.pack("<d", v))[0] for v in (x, r))
-        assert br == bx | 0xFFFFFFFF and br >> 32 == bx >> 32
-        assert r >= x and (x == 0.0 or r <= x * (1 + 2.0 ** -20))
-    assert oracle.round_up_hi32(0.0) == struct.unpack("<d", struct.pack("<Q", 0xFFFFFFFF))[0]
+def test_threshold_boundary_exact_maxima():
+    """R1 with exact maxima.  Integer data built so that every partial product, sum and
+    carried checksum is exactly 0 (rows of A sum to 0, columns of B constant): a fault applied
+    after the last update (step = k) gives residuals exactly delta, so a delta just below
+    tau(I, J) is not flagged and one just above is located.  tau uses the unit's own maxima
+    max|op(A)_I:| and max|op(B)_:J| (larger values in another row block do not enter it)."""
+    rng = np.random.default_rng(29)
+    m, n, k = 64, 64, 96
+    A = rng.integers(-3, 4, (m, k)).astype(float)
+    A[:, -1] = -A[:, :-1].sum(axis=1)
+    A[40:, :] *= 1024.0  # row block 1: larger values must not enter unit (0, 0)'s tau
+    A = F(A)
+    B = F(np.tile(rng.integers(-5, 6, (1, n)).astype(float), (k, 1)))
+    g = lambda nn: nn * U / (1 - nn * U)  # noqa: E731
+    amax, bmax = np.abs(A[:32]).max(), np.abs(B[:, :32]).max()
+    tau = 2 * g(k + 32) * k * 32 * amax * bmax  # tau_col == tau_row: 32 x 32 unit
+    for scale, flagged in ((0.999, False), (1.001, True)):
+        _, rep = run(A, B, BM=32, BN=32, BK=4, faults=[(5, 7, k, scale * tau)])
+        assert (rep.detected == 1) == flagged, (scale, rep)
+        if flagged:
+            assert rep.events[0][1:4] == (5, 7, 1)
+            assert rep.events[0][4] == rep.events[0][5] == scale * tau
+
+
+def test_nonfinite_residual_always_flags():
+    """R13: tau is clamped to the largest finite double, so a unit with an infinite input (tau
+    would be infinite) is still flagged by its non-finite residuals and recomputed."""
+    rng = np.random.default_rng(31)
+    m, n, k = 40, 40, 24
+    A, B = F(rng.uniform(-1, 1, (m, k))), F(rng.uniform(-1, 1, (k, n)))
+    A[3, 5] = np.inf
+    C, rep = run(A, B, BM=32, BN=32, BK=4)
+    assert rep.detected >= 1 and rep.corrected + rep.recomputed == rep.detected
+    assert all(e[3] == 2 for e in rep.events if e[1] == 0)
 
 
 def test_threshold_closed_form_and_detection_edge():
@@ -277,7 +302,6 @@ def test_threshold_closed_form_and_detection_edge():
     m, n, k = 48, 40, 100
     A, B = F(rng.uniform(-1, 1, (m, k))), F(rng.uniform(-1, 1, (k, n)))
     amax, bmax = np.abs(A[:32]).max(), np.abs(B[:, :32]).max()
-    amax, bmax = oracle.round_up_hi32(amax), oracle.round_up_hi32(bmax)
     big = 3.0 * oracle.tau(k, 32, amax, bmax)  # > 2 tau: must be located
     _, rep = run(A, B, BM=32, BN=32, BK=4, faults=[(5, 7, 50, big)])
     assert (rep.corrected, rep.recomputed) == (1, 0) and rep.events[0][1:3] == (5, 7)
