@@ -168,6 +168,11 @@ int ftblas_set_correction(int mode);
  *     itself (B_J e split between the two CTAs of a cluster pair);
  *   FTBLAS_ENCODE_PREPASS: two memory-bound passes over A and B before the kernel; the
  *     kernel copies the pre-encoded 16 k-slots into the checksum row of each staged tile.
+ *   FTBLAS_ENCODE_FUSED_WAIT: as FUSED, but a tile whose stage is not published yet waits
+ *     for its publisher instead of encoding the stage itself, so every checksum is encoded
+ *     exactly once (also in single-wave launches).  Relies on the publishing tiles, which
+ *     come first in the launch, being resident before the tiles that wait on them (in-order
+ *     CTA dispatch); meant for testing the copy paths, not for production use.
  * All feed the same in-kernel carry (C^f) and fused epilogue verification.  FUSED and
  * FUSED_LOCAL produce bitwise-identical checksums (same integer encode of the same data);
  * PREPASS agrees within the threshold (its sums differ only in rounding).
@@ -175,6 +180,7 @@ int ftblas_set_correction(int mode);
 #define FTBLAS_ENCODE_FUSED 0
 #define FTBLAS_ENCODE_PREPASS 1
 #define FTBLAS_ENCODE_FUSED_LOCAL 2
+#define FTBLAS_ENCODE_FUSED_WAIT 3
 int ftblas_set_encode(int mode);
 
 /* Verification interval Kc of ftblas_dgemm (§II.A,

@@ -108,18 +108,30 @@ struct Params {
   double *Bsh;
   int64_t ldbsh;
   unsigned int *hmB;
-  unsigned long long *dev_prof;   // development only: per-CTA [warp][wait, work] clock64 sums (null = off)
-  int dev_mode;                   // development only: 1 skip pass 2, 2 skip the encode, 4 never flag,
-                                  // 8 MMA waits for the TMA bytes only, 16 encoders skip the TMA wait,
-                                  // 32 unprotected kernel on the 127 grid, 128 no clusters, 256 tiles
-                                  // wait for the published e^T A_I, 512 tiles wait for the
-                                  // published B_J e (row/column-shared encode copy paths)
+  // Encode mode FUSED_WAIT: a tile whose stage is not published yet waits for the publisher
+  // instead of encoding it itself (every checksum encoded exactly once; tests of the copy paths).
+  int wait_pub;
+  // Development builds only (-DFTBLAS_DEV, libftblas_dev.so; compiled out of libftblas.so):
+  unsigned long long *dev_prof;   // per-CTA [warp][wait, work] clock64 sums (null = off)
+  int dev_mode;                   // 1 skip pass 2, 2 skip the encode, 4 never flag, 8 MMA waits for
+                                  // the TMA bytes only, 16 encoders skip the TMA wait, 32 unprotected
+                                  // kernel on the 127 grid, 128 no clusters
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
   EventDev *events;
   long long ev_cap;
 };
+
+// Development switches exist only in -DFTBLAS_DEV builds; in libftblas.so they are constant
+// zero, so every development branch is compiled out and nothing reads them at run time.
+#ifdef FTBLAS_DEV
+#define FT_DEV_MODE(P) ((P).dev_mode)
+#define FT_DEV_PROF(P) ((P).dev_prof)
+#else
+#define FT_DEV_MODE(P) 0
+#define FT_DEV_PROF(P) ((unsigned long long *)nullptr)
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
@@ -736,11 +748,11 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     f.am = ld_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg);
     return f;
   };
-  // Whole stage published?  (warp-uniform; dev mode 256 waits for it: tests of the copy path)
+  // Whole stage published?  (warp-uniform; encode mode FUSED_WAIT waits for it)
   auto check_a = [&](int s, PubA &f) {
     if (!a_sub) return;
     f.ok = __all_sync(0xffffffffu, pub_ok(f.a0) && pub_ok(f.a1) && pub_ok(f.am));
-    while ((P.dev_mode & 256) && !f.ok) {
+    while (P.wait_pub && !f.ok) {
       __nanosleep(256);
       f = fetch_a(s);
       f.ok = __all_sync(0xffffffffu, pub_ok(f.a0) && pub_ok(f.a1) && pub_ok(f.am));
@@ -794,8 +806,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       const bool doB = !split || !doA;
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
-        const long long t0 = P.dev_prof ? clock64() : 0;
-        const bool pubs = !(P.Ac || (P.dev_mode & 3));
+        const long long t0 = FT_DEV_PROF(P) ? clock64() : 0;
+        const bool pubs = !(P.Ac || (FT_DEV_MODE(P) & 3));
         PubA pa = pubs && doA ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
         // B_J e words of this stage: relaxed loads before the TMA wait as well
         double pb = 0.0;
@@ -806,18 +818,18 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
         };
         if (pubs && doB && b_sub) fetch_b();
-        if (!(P.dev_mode & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
+        if (!(FT_DEV_MODE(P) & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
         if (pubs && doA) check_a(s, pa);
         bool bcopy = false;
         if (pubs && doB && b_sub) {
           bcopy = __all_sync(0xffffffffu, pub_ok(pb) && pub_ok(pbm));
-          while ((P.dev_mode & 512) && !bcopy) {  // tests: wait for tile row 0 (copy path)
+          while (P.wait_pub && !bcopy) {  // FUSED_WAIT: wait for tile row 0
             __nanosleep(256);
             fetch_b();
             bcopy = __all_sync(0xffffffffu, pub_ok(pb) && pub_ok(pbm));
           }
         }
-        const long long t1 = P.dev_prof ? clock64() : 0;
+        const long long t1 = FT_DEV_PROF(P) ? clock64() : 0;
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
         if (P.Ac) {  // PREPASS: copy the pre-encoded 16 k-slots of e^T A_I / B_J e
@@ -826,10 +838,10 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
             if (doA) sA[sidx<AKM>(x.cra, lane)] = p < x.k1 ? P.Ac[x.ti + p * P.ldac] : 0.0;
             if (doB) sB[sidx<BKM>(x.crb, lane)] = p < x.k1 ? P.Br[x.tj + p * P.ldbr] : 0.0;
           }
-        } else if (P.dev_mode & 1) {  // development: pass 1 only
+        } else if (FT_DEV_MODE(P) & 1) {  // development: pass 1 only
           if (doA) amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
           if (doB) bmax_hi = max(bmax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<BKM>(sB, lane, x.crb))));
-        } else if ((P.dev_mode & 2) && !share) {
+        } else if ((FT_DEV_MODE(P) & 2) && !share) {
           // development: no encode (checksum rows zero)
         } else {
          if (doA) {
@@ -901,9 +913,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           mbar_arrive(&tl.enc[slot]);
           if (doA && doB) mbar_arrive(&tl.enc[slot]);
         }
-        if (P.dev_prof && lane == 0) {
+        if (FT_DEV_PROF(P) && lane == 0) {
           const long long t2 = clock64();
-          unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + warp) * 2;
+          unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + warp) * 2;
           dp[0] += (unsigned long long)(t1 - t0);
           dp[1] += (unsigned long long)(t2 - t1);
         }
@@ -960,7 +972,7 @@ __device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *
       // Clamped to the largest finite double (R13): a NaN or infinite residual always flags.
       const double tau = fmin((2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx, 0x1.fffffffffffffp1023);
       const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
-      const bool flag = valid && !(fabs(d) <= tau) && !(P.dev_mode & 4);
+      const bool flag = valid && !(fabs(d) <= tau) && !(FT_DEV_MODE(P) & 4);
       tl.dres[vt] = d;
       if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, cidx);
       const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
@@ -1076,7 +1088,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     // The protected pass waits for the encoded stage (TMA bytes + checksum row/column), the
     // unprotected one for the TMA bytes only.
     // 32-bit shared address of the barrier array to wait on (enc = full + STAGES).
-    const uint32_t ready = smem_u32(tl.full) + ((verify && !(P.dev_mode & 8)) ? STAGES * 8u : 0u);
+    const uint32_t ready = smem_u32(tl.full) + ((verify && !(FT_DEV_MODE(P) & 8)) ? STAGES * 8u : 0u);
 #ifdef FTBLAS_DEV_TIMELINE
     long long tl_a = clock64(), tl_b = tl_a;
     if (attempt == 0 && nk > 0) {
@@ -1134,8 +1146,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     }
     bar_sync(BAR_CTILE, 256);
 #ifdef FTBLAS_DEV_TIMELINE
-    if (!verify && attempt == 0 && vt == 0 && P.dev_prof) {
-      unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + 4) * 2;
+    if (!verify && attempt == 0 && vt == 0 && FT_DEV_PROF(P)) {
+      unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 4) * 2;
       dp[0] = (unsigned long long)(tl_b - tl_a);
       dp[1] = (unsigned long long)(clock64() - tl_b);
       dp[2] = 0ull;
@@ -1150,8 +1162,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
 #endif
     const bool multi = verify_tile<AKM, BKM>(P, tl, ctile, vt, mw);
 #ifdef FTBLAS_DEV_TIMELINE
-    if (attempt == 0 && vt == 0 && P.dev_prof) {
-      unsigned long long *dp = P.dev_prof + ((size_t)blockIdx.x * 12 + 4) * 2;
+    if (attempt == 0 && vt == 0 && FT_DEV_PROF(P)) {
+      unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 4) * 2;
       dp[0] = (unsigned long long)(tl_b - tl_a);
       dp[1] = (unsigned long long)(tl_c - tl_b);
       dp[2] = (unsigned long long)(clock64() - tl_c);
@@ -1197,7 +1209,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // and tile column 0 (e^T A_I) in the first waves, so nearly every other tile finds both
   // checksums published when it runs.  A partial last tile row / column (cheap: its idle warps
   // skip the DMMA stream) goes last, so the final waves are made of short tiles.
-  const int tstr_m = (FT || (P.dev_mode & 32)) ? TM : BM, tstr_n = (FT || (P.dev_mode & 32)) ? TN : BN;
+  const int tstr_m = (FT || (FT_DEV_MODE(P) & 32)) ? TM : BM, tstr_n = (FT || (FT_DEV_MODE(P) & 32)) ? TN : BN;
   const bool prow = P.tiles_m > 1 && (P.m % tstr_m) != 0, pcol = P.tiles_n > 1 && (P.n % tstr_n) != 0;
   auto map_tile = [&](int Lg, int &ti_, int &tj_, int &t_) {
     int L = Lg % P.ntiles;
@@ -1245,7 +1257,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   x.k1 = min64(x.k0 + P.Kc, P.k);
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.
-  const bool g127 = FT || (P.dev_mode & 32);  // dev mode 32: unprotected kernel on the 127 grid
+  const bool g127 = FT || (FT_DEV_MODE(P) & 32);  // dev mode 32: unprotected kernel on the 127 grid
   const int tm = g127 ? TM : BM, tn = g127 ? TN : BN;
   x.ti = ti;
   x.tj = tj;

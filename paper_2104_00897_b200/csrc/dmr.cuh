@@ -396,42 +396,44 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <bool DMR, bool FLT>
-__device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, int lane) {
-  const double *Aj = P.A + j * P.lda;
-  int64_t fstep = -1;
-  double fdel = 0.0;
-  if (DMR && FLT) {
-    int lo = 0, hi = P.nf;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.f[mid].index < j) lo = mid + 1; else hi = mid; }
-    for (; lo < P.nf && P.f[lo].index == j; ++lo)
-      if (P.f[lo].step < P.m && (P.f[lo].step & 31) == lane) { fstep = P.f[lo].step; fdel += P.f[lo].delta; }
-  }
-  double a1 = 0.0, a2 = 0.0;
-  int64_t i = lane;
-  if (!FLT && P.incx == 1 && ((reinterpret_cast<uintptr_t>(Aj) | reinterpret_cast<uintptr_t>(P.x)) & 15) == 0) {
-    // Unit-stride, 16-byte aligned column and x: 8 LDG.128 of A (and of x) in flight per lane,
-    // 512 elements per warp step; the remainder below continues from the first unread element.
-    int64_t b = 0;
-    for (; b + 512 <= P.m; b += 512) {
-      double2 av[8], xv[8];
+// This lane's part of column j's dot product, a1 (plus the duplicate a2 when TWO).  Every
+// computation of the column -- the two DMR copies and the third one that settles a mismatch --
+// goes through this function, so all three use the same partition and order: lanes own
+// elements {b + 64u + 2 lane, +1} of each 512-element block of the unit-stride, 16-byte aligned
+// fast path, then rows i = lane (mod 32) of the remainder.  A fault (FLT) at element fstep is
+// added to a1 before that element's term by the lane that owns it.
+__device__ __forceinline__ int64_t gemv_t_fast_end(const GemvParams &P, const double *Aj) {
+  const bool fast = P.incx == 1 && ((reinterpret_cast<uintptr_t>(Aj) | reinterpret_cast<uintptr_t>(P.x)) & 15) == 0;
+  return fast ? (P.m / 512) * 512 : 0;
+}
+__device__ __forceinline__ int gemv_t_owner(int64_t e, int64_t bfast) { return e < bfast ? (int)((e & 63) >> 1) : (int)(e & 31); }
+
+template <bool TWO, bool FLT>
+__device__ __forceinline__ void dgemv_t_lane(const GemvParams &P, const double *Aj, int lane, int64_t bfast,
+                                             int64_t fstep, double fdel, double &a1, double &a2) {
+  a1 = 0.0;
+  a2 = 0.0;
+  for (int64_t b = 0; b < bfast; b += 512) {
+    double2 av[8], xv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        av[u] = *reinterpret_cast<const double2 *>(Aj + b + 64 * u + 2 * lane);
-        xv[u] = *reinterpret_cast<const double2 *>(P.x + b + 64 * u + 2 * lane);
-      }
+    for (int u = 0; u < 8; ++u) {
+      av[u] = *reinterpret_cast<const double2 *>(Aj + b + 64 * u + 2 * lane);
+      xv[u] = *reinterpret_cast<const double2 *>(P.x + b + 64 * u + 2 * lane);
+    }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        a1 = v_fma(av[u].x, xv[u].x, a1);
-        a1 = v_fma(av[u].y, xv[u].y, a1);
-        if (DMR) {
-          a2 = v_fma(av[u].x, xv[u].x, a2);
-          a2 = v_fma(av[u].y, xv[u].y, a2);
-        }
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = b + 64 * u + 2 * lane;
+      if (FLT && e == fstep) a1 = v_add(a1, fdel);
+      a1 = v_fma(av[u].x, xv[u].x, a1);
+      if (FLT && e + 1 == fstep) a1 = v_add(a1, fdel);
+      a1 = v_fma(av[u].y, xv[u].y, a1);
+      if (TWO) {
+        a2 = v_fma(av[u].x, xv[u].x, a2);
+        a2 = v_fma(av[u].y, xv[u].y, a2);
       }
     }
-    i = b + lane;
   }
+  int64_t i = bfast + lane;
   for (; i + 96 < P.m; i += 128) {
     double av[4], xv[4];
 #pragma unroll
@@ -441,17 +443,33 @@ __device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, i
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (DMR && FLT && (i + 32 * u) == fstep) a1 = v_add(a1, fdel);
+      if (FLT && (i + 32 * u) == fstep) a1 = v_add(a1, fdel);
       a1 = v_fma(av[u], xv[u], a1);
-      if (DMR) a2 = v_fma(av[u], xv[u], a2);
+      if (TWO) a2 = v_fma(av[u], xv[u], a2);
     }
   }
   for (; i < P.m; i += 32) {
     const double av = Aj[i], xv = P.x[vidx(i, P.m, P.incx)];
-    if (DMR && FLT && i == fstep) a1 = v_add(a1, fdel);
+    if (FLT && i == fstep) a1 = v_add(a1, fdel);
     a1 = v_fma(av, xv, a1);
-    if (DMR) a2 = v_fma(av, xv, a2);
+    if (TWO) a2 = v_fma(av, xv, a2);
   }
+}
+
+template <bool DMR, bool FLT>
+__device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, int lane) {
+  const double *Aj = P.A + j * P.lda;
+  const int64_t bfast = gemv_t_fast_end(P, Aj);
+  int64_t fstep = -1;
+  double fdel = 0.0;
+  if (DMR && FLT) {
+    int lo = 0, hi = P.nf;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.f[mid].index < j) lo = mid + 1; else hi = mid; }
+    for (; lo < P.nf && P.f[lo].index == j; ++lo)
+      if (P.f[lo].step < P.m && gemv_t_owner(P.f[lo].step, bfast) == lane) { fstep = P.f[lo].step; fdel += P.f[lo].delta; }
+  }
+  double a1, a2;
+  dgemv_t_lane<DMR, DMR && FLT>(P, Aj, lane, bfast, fstep, fdel, a1, a2);
   double s1 = warp_sum(a1), s2 = DMR ? warp_sum(a2) : 0.0;
   if (DMR && FLT) s1 = v_add(s1, fault_delta(P.f, P.nf, j, P.m));
   double *yj = P.y + vidx(j, P.n, P.incy);
@@ -461,8 +479,8 @@ __device__ __forceinline__ void dgemv_t_column(const GemvParams &P, int64_t j, i
     const double yb2 = P.beta != 0.0 ? v_mul(P.beta, *yj) : 0.0;
     const double r2 = v_fma(P.alpha, s2, yb2);
     if (differ(r1, r2)) {  // warp-uniform: every lane holds the butterfly result
-      double a3 = 0.0;
-      for (int64_t q = lane; q < P.m; q += 32) a3 = v_fma(Aj[q], P.x[vidx(q, P.m, P.incx)], a3);
+      double a3, unused;
+      dgemv_t_lane<false, false>(P, Aj, lane, bfast, -1, 0.0, a3, unused);  // same partition and order
       const double r3 = v_fma(P.alpha, warp_sum(a3), yb2);
       if (lane == 0) r1 = settle(r1, r2, r3, P.cnt);
       else r1 = r3;

@@ -47,6 +47,42 @@ int cuda_fail(cudaError_t e) {
     if (e_ != cudaSuccess) return cuda_fail(e_); \
   } while (0)
 
+// Releases what one call acquired on every return path: the stream-ordered allocations (freed
+// on the call's stream once the library streams listed in `streams` are drained), events and
+// streams.
+struct Cleanup {
+  cudaStream_t st;
+  std::vector<void *> mem;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> events;
+  explicit Cleanup(cudaStream_t s) : st(s) {}
+  Cleanup(const Cleanup &) = delete;
+  Cleanup &operator=(const Cleanup &) = delete;
+  ~Cleanup() {
+    for (cudaStream_t s : streams) cudaStreamSynchronize(s);
+    for (void *p : mem) cudaFreeAsync(p, st);
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    for (cudaStream_t s : streams) cudaStreamDestroy(s);
+  }
+  template <class T>
+  cudaError_t alloc(T **p, size_t bytes) {
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(p), bytes, st);
+    if (e == cudaSuccess) mem.push_back(*p);
+    else *p = nullptr;
+    return e;
+  }
+  cudaError_t stream(cudaStream_t *s) {
+    const cudaError_t e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) streams.push_back(*s);
+    return e;
+  }
+  cudaError_t event(cudaEvent_t *ev) {
+    const cudaError_t e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) events.push_back(*ev);
+    return e;
+  }
+};
+
 bool is_n(char c) { return c == 'N' || c == 'n'; }
 bool is_t(char c) { return c == 'T' || c == 't' || c == 'C' || c == 'c'; }
 
@@ -68,7 +104,7 @@ int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &
   // (C5-like 4.0% -> 3.9%, C4a 9.2% -> 7.8%); a single-wave FUSED launch, which skips the
   // sharing, is also faster plain (1016^2 x 256: first-stage wait 10.2k vs 11.6k clocks), so
   // FUSED launches are plain.
-  if (FT && p.cluster2 && !p.Ac && !p.Ash && !p.Bsh && !(p.dev_mode & 128)) {
+  if (FT && p.cluster2 && !p.Ac && !p.Ash && !p.Bsh && !(FT_DEV_MODE(p) & 128)) {
     p.cluster2 = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((grid.x + 1) & ~1u);
@@ -351,7 +387,9 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.m = m; p.n = n; p.k = k; p.alpha = alpha; p.beta = beta;
   p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
   int dev_mode = 0;
+#ifdef FTBLAS_DEV
   if (const char *dm = std::getenv("FTBLAS_DEV_MODE")) dev_mode = std::atoi(dm);
+#endif
   const bool g127 = ft || (dev_mode & 32);  // dev mode 32: unprotected kernel on the 127 grid
   const int tm = g127 ? ftk::TM : ftk::BM, tn = g127 ? ftk::TN : ftk::BN;  // tile stride in C
   p.tiles_m = (int)((m + tm - 1) / tm);
@@ -368,9 +406,12 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
   p.correct_mode = tl_correct;
   p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL) ? 1 : 0;  // request; launch_one decides
-  // development only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
+#ifdef FTBLAS_DEV
+  // development build only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
-  if (const char *dm = std::getenv("FTBLAS_DEV_MODE")) p.dev_mode = std::atoi(dm);
+  p.dev_mode = dev_mode;
+#endif
+  p.wait_pub = (ft && tl_encode == FTBLAS_ENCODE_FUSED_WAIT) ? 1 : 0;
 
   // Bucket faults by (tile, stage); stable so same-stage faults keep the caller's order.
   std::vector<ftk::FaultDev> fd;
@@ -399,9 +440,10 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // slice maxima and the published sums, filled with all-ones bytes (= not yet published).
   // Launches of a single wave skip it (every tile starts together, so a consumer would almost
   // never find a stage published) unless dev modes 256 / 512 force the copy paths.
-  const bool one_wave = (int64_t)p.ntiles * T <= (int64_t)num_sms() && !(dev_mode & (256 | 512));
-  const bool ashare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_n > 1 && !one_wave;
-  const bool bshare = ft && tl_encode == FTBLAS_ENCODE_FUSED && p.tiles_m > 1 && !one_wave;
+  const bool one_wave = (int64_t)p.ntiles * T <= (int64_t)num_sms() && !p.wait_pub;
+  const bool fused_shared = tl_encode == FTBLAS_ENCODE_FUSED || tl_encode == FTBLAS_ENCODE_FUSED_WAIT;
+  const bool ashare = ft && fused_shared && p.tiles_n > 1 && !one_wave;
+  const bool bshare = ft && fused_shared && p.tiles_m > 1 && !one_wave;
   const size_t nsg = (size_t)p.nk;  // global stages over the whole k
   // Scratch: [counters (64 B) | events | faults | prepass | hmA Ash | hmB Bsh]: the counters
   // zeroed, the publication region filled with 0xFF; counters and the first events are read
@@ -413,8 +455,9 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   const size_t ash_bytes = ashare ? hma_bytes + al256(sizeof(double) * (size_t)p.tiles_m * (size_t)k) : 0;
   const size_t hmb_bytes = bshare ? al256(sizeof(unsigned) * (size_t)p.tiles_n * nsg) : 0;
   const size_t bsh_bytes = bshare ? hmb_bytes + sizeof(double) * (size_t)p.tiles_n * (size_t)k : 0;
+  Cleanup cl(st);
   char *scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes, st));
+  CUDA_TRY(cl.alloc(&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes));
   char *const cnt_ptr = scratch;
   if (ashare) {
     char *sb = scratch + base_bytes + pre_bytes;
@@ -467,14 +510,14 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   auto aligned = [](const double *q, int64_t ld) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0 && ld % 2 == 0; };
   if (!aligned(A, lda)) {
     const int64_t nld = (ar + 1) & ~int64_t(1);
-    CUDA_TRY(cudaMallocAsync((void **)&rA, sizeof(double) * nld * ac, st));
+    CUDA_TRY(cl.alloc(&rA, sizeof(double) * nld * ac));
     CUDA_TRY(cudaMemcpy2DAsync(rA, sizeof(double) * nld, A, sizeof(double) * lda, sizeof(double) * ar, ac,
                                cudaMemcpyDeviceToDevice, st));
     p.A = rA; p.lda = nld;
   }
   if (!aligned(B, ldb)) {
     const int64_t nld = (br + 1) & ~int64_t(1);
-    CUDA_TRY(cudaMallocAsync((void **)&rB, sizeof(double) * nld * bc, st));
+    CUDA_TRY(cl.alloc(&rB, sizeof(double) * nld * bc));
     CUDA_TRY(cudaMemcpy2DAsync(rB, sizeof(double) * nld, B, sizeof(double) * ldb, sizeof(double) * br, bc,
                                cudaMemcpyDeviceToDevice, st));
     p.B = rB; p.ldb = nld;
@@ -495,7 +538,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
     const size_t slice = sizeof(double) * (size_t)m * (size_t)n;
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)(free_b / 2 / slice)));
     double *W = nullptr;
-    CUDA_TRY(cudaMallocAsync((void **)&W, slice * (size_t)G, st));
+    CUDA_TRY(cl.alloc(&W, slice * (size_t)G));
     ftk::Params pw = p;
     pw.C = W; pw.ldc = m; pw.alpha = 1.0; pw.beta = 0.0; pw.wstride = m * n;
     for (int64_t g0 = 0; g0 < T && lrc == 0; g0 += G) {
@@ -509,15 +552,11 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
       ++tl_launches;
       if (cudaGetLastError() != cudaSuccess) lrc = 1;
     }
-    cudaFreeAsync(W, st);
   }
-  if (rA) cudaFreeAsync(rA, st);
-  if (rB) cudaFreeAsync(rB, st);
-  if (lrc) { cudaFreeAsync(scratch, st); return lrc; }
+  if (lrc) return lrc;
 
   if (err && !sink)
     if (int e = finish_report(err, p.counters, p.events, ev_cap, ft ? (int64_t)p.ntiles * T : 0, st)) return e;
-  CUDA_TRY(cudaFreeAsync(scratch, st));
   return 0;
 }
 
@@ -562,8 +601,9 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t total = al(cnt_b) + al(ev_b) + al(hm_b) + al(ac_b) + al(br_b) + al(csc_b) + al(csr_b) + al(rc_b) +
                        al(rr_b) + al(t_b);
+  Cleanup cl(st);
   char *base = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&base, total, st));
+  CUDA_TRY(cl.alloc(&base, total));
   char *q = base;
   auto take = [&](size_t b) { char *r = q; q += al(b); return r; };
   auto *counters = reinterpret_cast<unsigned long long *>(take(cnt_b));
@@ -615,7 +655,6 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   }
   if (err)
     if (int e = finish_report(err, counters, events, ev_cap, nbm * nbn, st)) return e;
-  CUDA_TRY(cudaFreeAsync(base, st));
   return 0;
 }
 
@@ -645,8 +684,9 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   const bool reads_ab = alpha != 0.0 && k > 0;
   if (!reads_ab) {  // C = beta*C: one device round trip, no ABFT
     if (beta == 1.0) return 0;
+    Cleanup cl0(st);
     double *dC = nullptr;
-    CUDA_TRY(cudaMallocAsync((void **)&dC, sizeof(double) * m * n, st));
+    CUDA_TRY(cl0.alloc(&dC, sizeof(double) * m * n));
     if (beta != 0.0)
       CUDA_TRY(cudaMemcpy2DAsync(dC, sizeof(double) * m, C, sizeof(double) * ldc, sizeof(double) * m, n,
                                  cudaMemcpyHostToDevice, st));
@@ -655,7 +695,6 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
     if (r == 0)
       r = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * m, sizeof(double) * m, n,
                             cudaMemcpyDeviceToHost, st) == cudaSuccess ? 0 : 1;
-    cudaFreeAsync(dC, st);
     const cudaError_t se = cudaStreamSynchronize(st);
     return r ? r : (se == cudaSuccess ? 0 : cuda_fail(se));
   }
@@ -723,15 +762,16 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
     return best;
   };
 
+  Cleanup cl(st);
   cudaStream_t sh = nullptr, sd = nullptr;
-  CUDA_TRY(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
-  CUDA_TRY(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  CUDA_TRY(cl.stream(&sh));
+  CUDA_TRY(cl.stream(&sd));
   cudaEvent_t ev_b, ev_in[2], ev_out[2], ev_free[2];
-  CUDA_TRY(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+  CUDA_TRY(cl.event(&ev_b));
   for (int q = 0; q < 2; ++q) {
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_in[q], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_out[q], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_free[q], cudaEventDisableTiming));
+    CUDA_TRY(cl.event(&ev_in[q]));
+    CUDA_TRY(cl.event(&ev_out[q]));
+    CUDA_TRY(cl.event(&ev_free[q]));
   }
   const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
   const size_t cnt_bytes = sizeof(unsigned long long) * ftk::CNT_N;
@@ -742,11 +782,11 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   int r = 0;
   auto fail = [&](cudaError_t e) { if (r == 0 && e != cudaSuccess) r = cuda_fail(e); };
   // Stream-ordered (pooled) staging on the compute stream; the copy streams wait for it.
-  fail(cudaMallocAsync((void **)&rep_base, 256 + ev_bytes, st));
-  fail(cudaMallocAsync((void **)&dB, sizeof(double) * br * bc, st));
+  fail(cl.alloc(&rep_base, 256 + ev_bytes));
+  fail(cl.alloc(&dB, sizeof(double) * br * bc));
   for (int q = 0; q < 2 && q < npan; ++q) {
-    fail(cudaMallocAsync((void **)&dA[q], pa, st));
-    fail(cudaMallocAsync((void **)&dC[q], pc, st));
+    fail(cl.alloc(&dA[q], pa));
+    fail(cl.alloc(&dC[q], pc));
   }
   fail(cudaEventRecord(ev_b, st));
   fail(cudaStreamWaitEvent(sh, ev_b, 0));
@@ -755,7 +795,11 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
                   reinterpret_cast<ftk::EventDev *>(rep_base + 256), ev_cap, 0, 0};
   if (r == 0) fail(cudaMemsetAsync(rep_base, 0, cnt_bytes, st));
   // development only (FTBLAS_DEV_E2E): stream-event timeline of the pipeline, printed at the end
+#ifdef FTBLAS_DEV
   const bool dev_e2e = std::getenv("FTBLAS_DEV_E2E") != nullptr;
+#else
+  const bool dev_e2e = false;
+#endif
   std::vector<std::pair<std::string, cudaEvent_t>> dev_ev;
   auto mark = [&](const std::string &what, cudaStream_t s) {
     if (!dev_e2e) return;
@@ -844,16 +888,6 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   fail(cudaStreamSynchronize(sh));
   fail(cudaStreamSynchronize(st));
   if (r == 0 && err && ft) r = finish_report(err, sink.counters, sink.events, ev_cap, sink.units, st);
-  cudaFreeAsync(rep_base, st);
-  cudaFreeAsync(dB, st);
-  for (int q = 0; q < 2; ++q) {
-    if (dA[q]) cudaFreeAsync(dA[q], st);
-    if (dC[q]) cudaFreeAsync(dC[q], st);
-  }
-  cudaEventDestroy(ev_b);
-  for (int q = 0; q < 2; ++q) { cudaEventDestroy(ev_in[q]); cudaEventDestroy(ev_out[q]); cudaEventDestroy(ev_free[q]); }
-  cudaStreamDestroy(sh);
-  cudaStreamDestroy(sd);
   return r;
 }
 
@@ -879,12 +913,20 @@ int dmr_prepare(bool ft, std::vector<ftblas_fault_t> &faults, int64_t nout, int6
   sc.cnt = reinterpret_cast<unsigned long long *>(sc.base);
   sc.f = fd.empty() ? nullptr : reinterpret_cast<ftd::DmrFault *>(sc.base + 256);
   sc.nf = (int)fd.size();
-  CUDA_TRY(cudaMemsetAsync(sc.cnt, 0, cb, st));
-  if (!fd.empty()) CUDA_TRY(cudaMemcpyAsync(sc.f, fd.data(), fb, cudaMemcpyHostToDevice, st));
+  cudaError_t e = cudaMemsetAsync(sc.cnt, 0, cb, st);
+  if (e == cudaSuccess && !fd.empty()) e = cudaMemcpyAsync(sc.f, fd.data(), fb, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(sc.base, st);
+    sc.base = nullptr;
+    return cuda_fail(e);
+  }
   return 0;
 }
 
 int dmr_finish(DmrScratch &sc, int64_t checked, ftblas_dmr_report_t *rep, cudaStream_t st) {
+  Cleanup cl(st);  // the scratch is released on every path
+  if (sc.base) cl.mem.push_back(sc.base);
+  sc.base = nullptr;
   CUDA_TRY(cudaGetLastError());
   if (rep) {
     unsigned long long c[ftd::D_N];
@@ -895,7 +937,6 @@ int dmr_finish(DmrScratch &sc, int64_t checked, ftblas_dmr_report_t *rep, cudaSt
     rep->corrected = (int64_t)c[ftd::D_CORRECTED];
     rep->uncorrectable = (int64_t)c[ftd::D_UNCORRECTABLE];
   }
-  CUDA_TRY(cudaFreeAsync(sc.base, st));
   return 0;
 }
 
@@ -1051,9 +1092,10 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
       if (e >= r0 && e < r0 + mb && f.step >= r0 && f.step < r0 + mb)
         lf.push_back(ftd::DmrFault{f_rhs(c, f) * ftt::LEAF + (e - r0), f.step - r0, f.delta});
     }
+  Cleanup cl(c.st);
   ftd::DmrFault *df = nullptr;
   if (!lf.empty()) {
-    CUDA_TRY(cudaMallocAsync((void **)&df, sizeof(ftd::DmrFault) * lf.size(), c.st));
+    CUDA_TRY(cl.alloc(&df, sizeof(ftd::DmrFault) * lf.size()));
     CUDA_TRY(cudaMemcpyAsync(df, lf.data(), sizeof(ftd::DmrFault) * lf.size(), cudaMemcpyHostToDevice, c.st));
   }
   ftt::LeafParams P{};
@@ -1088,7 +1130,6 @@ int trsm_leaf(TrsmCtx &c, int64_t r0, int64_t mb) {
   kernels[c.fwd][c.ft][c.ft && P.nf > 0]<<<grid, ftt::LEAF_THREADS, smem, c.st>>>(P);
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());
-  if (df) CUDA_TRY(cudaFreeAsync(df, c.st));
   return 0;
 }
 
@@ -1177,13 +1218,15 @@ int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m,
     if (alpha == 0.0) return 0;
   }
   const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
+  Cleanup cl(st);
   char *rep = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&rep, 256 + sizeof(ftk::EventDev) * (size_t)std::max<int64_t>(ev_cap, 1), st));
+  CUDA_TRY(cl.alloc(&rep, 256 + sizeof(ftk::EventDev) * (size_t)std::max<int64_t>(ev_cap, 1)));
   CUDA_TRY(cudaMemsetAsync(rep, 0, 256, st));
   ReportSink sink{reinterpret_cast<unsigned long long *>(rep), reinterpret_cast<ftk::EventDev *>(rep + 256), ev_cap, 0, 0};
   std::vector<ftblas_fault_t> none;
   DmrScratch lsc;
   if (int e = dmr_prepare(false, none, 1, 0, lsc, st)) return e;  // leaf counters only
+  cl.mem.push_back(lsc.base);
   TrsmCtx c{ft, fwd, trans, unit, right, (int64_t)ftt::LEAF, A, lda, B, ldb, right ? m : n, &faults, &sink, &lsc, st};
   int r = trsm_rec(c, 0, na);
   if (r == 0 && err && ft) {
@@ -1195,8 +1238,6 @@ int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m,
       err->recomputed += (int64_t)lc[ftd::D_UNCORRECTABLE];
     }
   }
-  cudaFreeAsync(rep, st);
-  cudaFreeAsync(lsc.base, st);
   return r;
 }
 
@@ -1321,7 +1362,9 @@ int ftblas_set_interval(int64_t kc) {
 }
 
 int ftblas_set_encode(int mode) {
-  if (mode != FTBLAS_ENCODE_FUSED && mode != FTBLAS_ENCODE_PREPASS && mode != FTBLAS_ENCODE_FUSED_LOCAL) return 4;
+  if (mode != FTBLAS_ENCODE_FUSED && mode != FTBLAS_ENCODE_PREPASS && mode != FTBLAS_ENCODE_FUSED_LOCAL &&
+      mode != FTBLAS_ENCODE_FUSED_WAIT)
+    return 4;
   tl_encode = mode;
   return 0;
 }

@@ -75,15 +75,17 @@ class Report:
 _lib = None
 
 
-def load():
-    """Load libftblas.so (built by paper_2104_00897_b200.build); raise if absent."""
+def load(path: str | None = None):
+    """Load libftblas.so (built by paper_2104_00897_b200.build); raise if absent.  `path`
+    selects another build of the same ABI (development tools: libftblas_dev.so)."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with "
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with "
                           "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     c, i64, d, P, i32 = ctypes.c_char, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
     gemm = [c, c, i64, i64, i64, d, P, i64, P, i64, d, P, i64]
     L.ftblas_dgemm.argtypes = gemm + [ctypes.POINTER(ErrReport)]
@@ -326,7 +328,8 @@ def ftblas_set_correction(mode: int):
 
 
 def ftblas_set_encode(mode: int):
-    """ENCODE_FUSED (0, default), ENCODE_PREPASS (1) or ENCODE_FUSED_LOCAL (2); thread-local."""
+    """ENCODE_FUSED (0, default), ENCODE_PREPASS (1), ENCODE_FUSED_LOCAL (2) or ENCODE_FUSED_WAIT (3);
+    thread-local."""
     _check("ftblas_set_encode", load().ftblas_set_encode(mode))
 
 
@@ -357,5 +360,6 @@ def ftblas_finalize():
 ENCODE_FUSED = 0
 ENCODE_PREPASS = 1
 ENCODE_FUSED_LOCAL = 2
+ENCODE_FUSED_WAIT = 3
 CORRECT_RECOMPUTE = 0
 CORRECT_SUBTRACT = 1

@@ -3,7 +3,6 @@ and the comparison of GPU and oracle reports.  No method arithmetic lives here."
 from __future__ import annotations
 
 import contextlib
-import os
 
 import numpy as np
 
@@ -71,22 +70,15 @@ def assert_reports_match(gpu, orc, A=None, B=None, ta="N", tb="N", k=None):
 def encode_mode(F, name):
     """Encode mode of ftblas_dgemm for the duration: "fused" (e^T A_I shared along tile rows,
     B_J e along tile columns, as scheduled), "fused_copy" (the same, every tile waiting for the
-    published copies: dev modes 256 | 512 | 128), "fused_local" (every CTA encodes itself) or
+    published copies: ENCODE_FUSED_WAIT), "fused_local" (every CTA encodes itself) or
     "prepass"."""
-    mode = {"fused": F.ENCODE_FUSED, "fused_copy": F.ENCODE_FUSED, "fused_local": F.ENCODE_FUSED_LOCAL,
+    mode = {"fused": F.ENCODE_FUSED, "fused_copy": F.ENCODE_FUSED_WAIT, "fused_local": F.ENCODE_FUSED_LOCAL,
             "prepass": F.ENCODE_PREPASS}[name]
-    old = os.environ.get("FTBLAS_DEV_MODE")
-    if name == "fused_copy":
-        os.environ["FTBLAS_DEV_MODE"] = str(256 | 512 | 128)
     F.ftblas_set_encode(mode)
     try:
         yield
     finally:
         F.ftblas_set_encode(F.ENCODE_FUSED)
-        if old is None:
-            os.environ.pop("FTBLAS_DEV_MODE", None)
-        else:
-            os.environ["FTBLAS_DEV_MODE"] = old
 
 
 def trsm_leaf_ids(length, leaf=128, tm=127):

@@ -95,13 +95,21 @@ def test_paper_overhead_model_closed_form():
         predict_unfused_overhead(10, 10, 20, 1.0, 1.0)
 
 
+def test_release_library_reads_no_environment():
+    """The release library has no development switches: no FTBLAS_DEV_* environment names are
+    referenced by libftblas.so (they exist only in the -DFTBLAS_DEV build)."""
+    data = open(F.LIB_PATH, "rb").read()
+    for name in (b"FTBLAS_DEV_MODE", b"FTBLAS_DEV_PROF", b"FTBLAS_DEV_E2E"):
+        assert name not in data, name
+
+
 def test_option_setters_validate_without_a_gpu():
-    """Thread-local options: encode modes FUSED / PREPASS / FUSED_LOCAL accepted, others -> 4;
-    the interval must be a non-negative multiple of the step quantum."""
+    """Thread-local options: encode modes FUSED / PREPASS / FUSED_LOCAL / FUSED_WAIT accepted,
+    others -> 4; the interval must be a non-negative multiple of the step quantum."""
     L = F.load()
-    for mode in (F.ENCODE_FUSED, F.ENCODE_PREPASS, F.ENCODE_FUSED_LOCAL):
+    for mode in (F.ENCODE_FUSED, F.ENCODE_PREPASS, F.ENCODE_FUSED_LOCAL, F.ENCODE_FUSED_WAIT):
         assert L.ftblas_set_encode(mode) == 0
-    assert L.ftblas_set_encode(3) == 4 and L.ftblas_set_encode(-1) == 4
+    assert L.ftblas_set_encode(4) == 4 and L.ftblas_set_encode(-1) == 4
     assert L.ftblas_set_encode(F.ENCODE_FUSED) == 0
     assert L.ftblas_set_interval(32) == 0 and L.ftblas_set_interval(0) == 0
     assert L.ftblas_set_interval(20) == 4 and L.ftblas_set_interval(-16) == 4

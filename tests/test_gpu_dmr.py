@@ -117,3 +117,26 @@ def test_argument_errors():
     F.ftblas_inject_arm([(10, 0, 0, 1.0)])
     with pytest.raises(FtblasError):  # fault index outside the 4 outputs
         F.ftblas_dscal(4, 1.0, dev(np.ones(4)), 1)
+
+
+@pytest.mark.parametrize("m", [512, 2048 + 37, 5000])
+def test_dgemv_t_fast_path_faults_settle_bitwise(m):
+    """DGEMV 'T' on the unit-stride 16-byte aligned fast path (m >= 512): a fault in the
+    original computation is settled by a third computation with the SAME lane partition and
+    order, so every faulted column is counted corrected (never uncorrectable) and the stored y
+    is bitwise the fault-free result of the unprotected twin.  Faults land in the vectorised
+    blocks (both elements of a lane's pair) and in the remainder."""
+    rng = np.random.default_rng(m)
+    n = 96
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    x, y = rng.standard_normal(m), rng.standard_normal(n)
+    steps = [0, 1, 63, 64, 511, m - 1, (m // 512) * 512 + 5 if m % 512 > 5 else 2]
+    faults = [(j, 0, steps[j % len(steps)], float(rng.choice([-1, 1]) * 10 ** rng.uniform(-3, 3)))
+              for j in range(0, n, 3)]
+    dA, dx = dev(A.reshape(-1, order="F")), dev(x)
+    dy, dy0 = dev(y), dev(y)
+    F.ftblas_inject_arm(faults)
+    rep = F.ftblas_dgemv("T", m, n, 0.75, dA, m, dx, 1, -0.5, dy, 1)
+    F.ftblas_dgemv_noft("T", m, n, 0.75, dA, m, dx, 1, -0.5, dy0, 1)
+    assert rep.detected == len(faults) and rep.corrected == len(faults) and rep.uncorrectable == 0
+    assert np.array_equal(host(dy), host(dy0))

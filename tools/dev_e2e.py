@@ -3,7 +3,8 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 os.environ["FTBLAS_DEV_E2E"] = "1"
-from paper_2104_00897_b200 import ftblas as F
+from paper_2104_00897_b200 import build as _build, ftblas as F
+F.load(_build.build(dev=True))  # development switches: libftblas_dev.so (-DFTBLAS_DEV)
 M, N, K = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (32768, 32768, 32768)))
 h = torch.empty(1 << 27, dtype=torch.float64, pin_memory=True); d = torch.empty_like(h, device="cuda")
 for name, fn in (("H2D", lambda: d.copy_(h, non_blocking=True)), ("D2H", lambda: h.copy_(d, non_blocking=True))):

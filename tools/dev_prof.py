@@ -8,7 +8,8 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 ntiles = ((N + 126) // 127) ** 2
 prof = torch.zeros(ntiles * 12 * 2, dtype=torch.int64, device="cuda")
 os.environ["FTBLAS_DEV_PROF"] = str(prof.data_ptr())
-from paper_2104_00897_b200 import ftblas as F
+from paper_2104_00897_b200 import build as _build, ftblas as F
+F.load(_build.build(dev=True))  # development switches: libftblas_dev.so (-DFTBLAS_DEV)
 g = torch.Generator(device="cuda").manual_seed(0)
 A = torch.rand(N * N, dtype=torch.float64, device="cuda", generator=g)
 B = torch.rand(N * N, dtype=torch.float64, device="cuda", generator=g)

@@ -8,7 +8,8 @@ lib, M, N, K = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
 ntiles = ((M + 126) // 127) * ((N + 126) // 127) + 1
 prof = torch.zeros(ntiles * 12 * 2, dtype=torch.int64, device="cuda")
 os.environ["FTBLAS_DEV_PROF"] = str(prof.data_ptr())
-from paper_2104_00897_b200 import ftblas as F
+from paper_2104_00897_b200 import build as _build, ftblas as F
+F.load(_build.build(dev=True))  # development switches: libftblas_dev.so (-DFTBLAS_DEV)
 F.LIB_PATH = lib
 g = torch.Generator(device="cuda").manual_seed(0)
 A = torch.rand(M * K, dtype=torch.float64, device="cuda", generator=g)

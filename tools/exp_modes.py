@@ -6,7 +6,8 @@ code = r'''
 import sys, os, json
 sys.path.insert(0, %r)
 import torch
-from paper_2104_00897_b200 import ftblas as F
+from paper_2104_00897_b200 import build as _build, ftblas as F
+F.load(_build.build(dev=True))  # development switches: libftblas_dev.so (-DFTBLAS_DEV)
 N = int(os.environ.get("N", "8192"))
 M, K = int(os.environ.get("M", N)), int(os.environ.get("K", N))
 g = torch.Generator(device="cuda").manual_seed(0)
