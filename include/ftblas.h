@@ -75,8 +75,10 @@ typedef struct {
   int32_t unit_k;        /* out: Kc, k-length of a verification interval (ftblas_set_interval) */
   int32_t step_quantum;  /* out: BK; an injected fault's step is applied at floor(step/BK)*BK */
   ftblas_event_t *events;  /* in: caller-owned HOST array (may be NULL), filled with the
-                              first min(n_events, events_capacity) events sorted by
-                              (interval, i, j) */
+                              first min(n_events, events_capacity) of ALL the call's events
+                              sorted by (interval, i, j) (deterministic: the library keeps
+                              one event slot per unit, so nothing is dropped before the
+                              sort; FT-DTRSM keeps max(events_capacity, 1024) slots) */
   int64_t events_capacity; /* in */
 } ftblas_err_report_t;
 

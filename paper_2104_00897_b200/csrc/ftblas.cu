@@ -429,7 +429,9 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
     return a.tile != b.tile ? a.tile < b.tile : a.stage < b.stage;
   });
 
-  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
+  // The device event ring holds one event per unit, so it never overflows: the report's events
+  // are the first events_capacity of ALL events in sorted order (deterministic).
+  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, (int64_t)p.ntiles * T) : 0;
   static_assert(sizeof(unsigned long long) * ftk::CNT_N <= 64, "counters fit their 64-byte slot");
   const size_t ev_bytes = sizeof(ftk::EventDev) * (size_t)ev_cap;
   const size_t f_bytes = sizeof(ftk::FaultDev) * fd.size();
@@ -590,7 +592,7 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   const int64_t nbm = (m + ftu::UB - 1) / ftu::UB, nbn = (n + ftu::UB - 1) / ftu::UB;
   const int64_t ldm = (nbm + 1) & ~int64_t(1), ldn = (nbn + 1) & ~int64_t(1), ldr = (m + 1) & ~int64_t(1);
   const bool direct = alpha == 1.0 && beta == 0.0;  // verify C itself, else a scratch product T
-  const int64_t ev_cap = std::max<int64_t>(err ? err->events_capacity : 0, 1024);
+  const int64_t ev_cap = std::max<int64_t>(err ? err->events_capacity : 0, nbm * nbn);  // one per unit
   // scratch: counters, events, maxima, Ac, Br, CSc, CSr, Rc, Rr (+ T)
   const size_t cnt_b = sizeof(unsigned long long) * ftk::CNT_N, ev_b = sizeof(ftk::EventDev) * ev_cap;
   const size_t hm_b = sizeof(unsigned) * (ldm + ldn);
@@ -701,6 +703,7 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
   for (const auto &f : faults)
     if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step > k) return 3;
   const int64_t Kc = (ft && tl_interval > 0 && tl_interval < k) ? tl_interval : k;
+  const int64_t T_units = (k + Kc - 1) / Kc;
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
 
   // Panels: about m/8 rows, a multiple of 2 x 127 (units intact, even leading dimensions),
@@ -773,7 +776,10 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
     CUDA_TRY(cl.event(&ev_out[q]));
     CUDA_TRY(cl.event(&ev_free[q]));
   }
-  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0, 1024) : 0;
+  // one event slot per unit of the whole problem (never overflows; deterministic report)
+  const int64_t ev_cap = ft ? std::max<int64_t>(err ? err->events_capacity : 0,
+                                                ((m + ftk::TM - 1) / ftk::TM) * ((n + ftk::TN - 1) / ftk::TN) * T_units)
+                            : 0;
   const size_t cnt_bytes = sizeof(unsigned long long) * ftk::CNT_N;
   const size_t ev_bytes = sizeof(ftk::EventDev) * (size_t)std::max<int64_t>(ev_cap, 1);
   const size_t pa = sizeof(double) * (size_t)P * (size_t)k, pc = sizeof(double) * (size_t)P * (size_t)n;

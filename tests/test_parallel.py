@@ -14,15 +14,22 @@ from paper_2104_00897_b200.parallel import RowPanelPartitioner, allreduce_counte
 
 
 def test_partition_rows_cover_and_align():
-    for m in [1, 127, 128, 300, 1000, 32768]:
-        for P in [1, 2, 3, 4, 8]:
-            part = RowPanelPartitioner(m, P, 128)
-            spans = [part.rows(r) for r in range(P)]
-            assert spans[0][0] == 0 and spans[-1][1] == m
-            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
-                assert a1 == b0
-            for (r0, r1) in spans:
-                assert r0 % 128 == 0
+    for unit in (127, 128):
+        for m in [1, 127, 128, 300, 1000, 32768]:
+            for P in [1, 2, 3, 4, 8]:
+                part = RowPanelPartitioner(m, P, unit)
+                spans = [part.rows(r) for r in range(P)]
+                assert spans[0][0] == 0 and spans[-1][1] == m
+                for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                    assert a1 == b0
+                for (r0, r1) in spans:
+                    assert r0 % unit == 0
+                # units split as evenly as whole units allow (at most one unit apart)
+                nu = [-(-(r1 - r0) // unit) for (r0, r1) in spans]
+                assert max(nu) - min(nu) <= 1
+    # C5 on the library's 127-row units: 259 unit rows over 8 ranks -> 32 or 33 each
+    part = RowPanelPartitioner(32768, 8, 127)
+    assert sorted({(r1 - r0 + 126) // 127 for (r0, r1) in (part.rows(r) for r in range(8))}) == [32, 33]
     part = RowPanelPartitioner(32768, 8, 128)
     assert [part.rows(r) for r in range(8)] == [(4096 * r, 4096 * (r + 1)) for r in range(8)]
     faults = [(5000, 3, 7, 1.0), (100, 4, 0, 2.0), (32767, 0, 9, 3.0)]
