@@ -141,6 +141,15 @@ int ftblas_dgemm_noft_host(char transA, char transB, int64_t m, int64_t n, int64
 int ftblas_inject_arm(const ftblas_fault_t *faults, int64_t n);
 int ftblas_inject_disarm(void);
 
+/* Test hook for the checksum lanes themselves (reading R6): perturb a CARRIED checksum of the
+ * verification unit that contains C(i, j) instead of a data accumulator -- lanes[e] == 1: the
+ * column checksum ((e^T A_I) B_J)_j, lanes[e] == 2: the row checksum (A_I (B_J e))_i -- by
+ * delta after `step` rank-1 updates (quantised like data faults).  Such a fault flags one
+ * direction only, so its unit is recomputed.  Consumed by the next ftblas_dgemm call on this
+ * thread (together with ftblas_inject_arm's list); any other entry point that finds them armed
+ * disarms them and returns 3, as does a lane other than 1 or 2. */
+int ftblas_inject_arm_checksum(const ftblas_fault_t *faults, const int32_t *lanes, int64_t n);
+
 /* Seeded fault generator: SplitMix64 (Steele, Lea, Flood 2014) seeded with `seed`; per
  * fault draw u0..u4 in [0,1) from the top 53 bits and set i = floor(u0*m),
  * j = floor(u1*n), step = floor(u2*k) (each clamped to the last index),

@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
 
 class _Fault(ctypes.Structure):
     _fields_ = [("i", ctypes.c_int64), ("j", ctypes.c_int64), ("step", ctypes.c_int64),
-                ("delta", ctypes.c_double)]
+                ("delta", ctypes.c_double), ("lane", ctypes.c_int64)]
 
 
 class _Event(ctypes.Structure):
@@ -159,7 +159,8 @@ def dgemm_abft(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *, BM, BN, 
                faults=(), units=None, subtract=False, events_cap=None):
     """Online ABFT DGEMM oracle.
 
-    ``faults``: iterable of (i, j, step, delta).  ``units``: optional list of (ti, tj)
+    ``faults``: iterable of (i, j, step, delta) or (i, j, step, delta, lane): lane 0 the data
+    accumulator, 1 the column checksum of column j, 2 the row checksum of row i (reading R6).  ``units``: optional list of (ti, tj)
     tile indices (sampled oracle); C entries outside those units are returned unchanged.
     Returns (C_out_flat, Report).
     """
@@ -167,8 +168,8 @@ def dgemm_abft(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, *, BM, BN, 
     Cout = _flat(C).copy()
     faults = list(faults)
     fa = (_Fault * max(len(faults), 1))()
-    for e, (i, j, s, dlt) in enumerate(faults):
-        fa[e] = _Fault(int(i), int(j), int(s), float(dlt))
+    for e, f in enumerate(faults):
+        fa[e] = _Fault(int(f[0]), int(f[1]), int(f[2]), float(f[3]), int(f[4]) if len(f) > 4 else 0)
     if units is not None:
         ua = np.ascontiguousarray(np.asarray(units, dtype=np.int64).reshape(-1))
         uptr, nu = _ptr(ua), len(ua) // 2
@@ -200,7 +201,7 @@ def _faults(faults):
     faults = list(faults)
     fa = (_Fault * max(len(faults), 1))()
     for e, (i, j, s, dlt) in enumerate(faults):
-        fa[e] = _Fault(int(i), int(j), int(s), float(dlt))
+        fa[e] = _Fault(int(i), int(j), int(s), float(dlt), 0)
     return ctypes.cast(fa, ctypes.c_void_p), len(faults), fa
 
 

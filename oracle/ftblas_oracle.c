@@ -46,7 +46,10 @@
 #include <omp.h>
 #endif
 
-typedef struct { int64_t i, j, step; double delta; } or_fault_t;
+/* lane 0: the data accumulator C_ij; 1: the carried column checksum ((e^T A_I) B_J)_j of the
+ * unit containing (i, j); 2: its carried row checksum (A_I (B_J e))_i (reading R6: a fault in a
+ * checksum lane). */
+typedef struct { int64_t i, j, step; double delta; int64_t lane; } or_fault_t;
 typedef struct {
   int64_t i, j;
   int32_t kind;      /* 1 = corrected at (i,j); 2 = recomputed unit with origin (i,j) */
@@ -173,11 +176,14 @@ static double dot_upto(const unit_ctx_t *x, int64_t i, int64_t j, int64_t pe) {
   return s;
 }
 
-static void apply_faults_at(double *acc, int64_t bm, int64_t i0, int64_t j0, const or_fault_t *f,
-                            int64_t nf, int64_t BK, int64_t step_q_wanted) {
+static void apply_faults_at(double *acc, double *cs_col, double *cs_row, int64_t bm, int64_t i0, int64_t j0,
+                            const or_fault_t *f, int64_t nf, int64_t BK, int64_t step_q_wanted) {
   for (int64_t e = 0; e < nf; ++e) {
     int64_t step_q = (f[e].step / BK) * BK; /* reading R8: quantised to BK */
-    if (step_q == step_q_wanted) acc[(f[e].i - i0) + (f[e].j - j0) * bm] += f[e].delta;
+    if (step_q != step_q_wanted) continue;
+    if (f[e].lane == 1) cs_col[f[e].j - j0] += f[e].delta;
+    else if (f[e].lane == 2) cs_row[f[e].i - i0] += f[e].delta;
+    else acc[(f[e].i - i0) + (f[e].j - j0) * bm] += f[e].delta;
   }
 }
 
@@ -201,7 +207,7 @@ static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t 
     const int64_t ps = t * Kc, pe = (ps + Kc < k) ? ps + Kc : k;
     for (int64_t p = ps; p < pe; ++p) {
       /* Injection point: faults whose quantised step equals p land before update p. */
-      apply_faults_at(acc, bm, i0, j0, f, nf, x->BK, p);
+      apply_faults_at(acc, cs_col, cs_row, bm, i0, j0, f, nf, x->BK, p);
 
       /* Encode: a_sum = sum_{i in I} opA(i,p)  (e^T A column p),
        *                       b_sum = sum_{j in J} opB(p,j)  (B e row p);
@@ -229,7 +235,7 @@ static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t 
       for (int64_t j = 0; j < bn; ++j) cs_col[j] += a_sum * op_at(x->B, x->ldb, x->tB, p, j0 + j);
       for (int64_t i = 0; i < bm; ++i) cs_row[i] += op_at(x->A, x->lda, x->tA, i0 + i, p) * b_sum;
     }
-    if (t == T - 1) apply_faults_at(acc, bm, i0, j0, f, nf, x->BK, k); /* step_q == k */
+    if (t == T - 1) apply_faults_at(acc, cs_col, cs_row, bm, i0, j0, f, nf, x->BK, k); /* step_q == k */
 
     /* Reference checksums from the computed C: r_col = e^T C_IJ, r_row = C_IJ e. */
     for (int64_t j = 0; j < bn; ++j) {

@@ -51,7 +51,7 @@ static_assert(BM * LDC_S <= STAGES * STAGE_ELEMS, "C tile must fit in the stage 
 
 struct FaultDev {        // one armed fault, sorted by (tile, stage)
   int32_t tile, stage;   // tile = ti + tj*tiles_m; stage = floor(step / BK)
-  int32_t li, lj;        // tile-local row / column
+  int32_t li, lj;        // tile-local row / column (-1: the checksum row / column)
   double delta;
 };
 
@@ -1060,7 +1060,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       while (s == next_stage) {
         const FaultDev f = P.faults[fnext];
         const TileGeom gf = load_geom(tl.geo);
-        const int si = f.li + gf.oa, sj = f.lj + gf.ob;  // staged row / column
+        // staged row / column; -1 = the unit's checksum row / column (checksum-lane faults)
+        const int si = f.li < 0 ? gf.cra : f.li + gf.oa, sj = f.lj < 0 ? gf.crb : f.lj + gf.ob;
         const int lr = si & 63, lc = sj & 31;
         const int fmt = AKM ? (lr >> 3) : 2 * (lr >> 4) + (lr & 1);
         const int rr = lr & 7;  // K-major: row in the 8-row tile = 4*(g&1) + (g>>1)

@@ -28,6 +28,12 @@ namespace {
 thread_local cudaStream_t tl_stream = nullptr;
 thread_local std::vector<ftblas_fault_t> tl_armed;
 thread_local bool tl_have_armed = false;
+// Checksum-lane faults (ftblas_inject_arm_checksum): lane 1 = column checksum, 2 = row checksum.
+struct CsFault {
+  ftblas_fault_t f;
+  int32_t lane;
+};
+thread_local std::vector<CsFault> tl_armed_cs;
 thread_local int tl_correct = FTBLAS_CORRECT_RECOMPUTE;
 thread_local int tl_encode = FTBLAS_ENCODE_FUSED;
 thread_local int64_t tl_interval = 0;  // Kc; 0 = k (one interval)
@@ -207,6 +213,14 @@ void zero_report(ftblas_err_report_t *err, int64_t k) {
   fill_geometry(err, k);
 }
 
+std::vector<CsFault> take_armed_cs() {
+  std::vector<CsFault> cs;
+  cs.swap(tl_armed_cs);
+  return cs;
+}
+// Entry points other than ftblas_dgemm: armed checksum-lane faults are a bad fault list.
+bool reject_armed_cs() { return !take_armed_cs().empty(); }
+
 std::vector<ftblas_fault_t> take_armed() {
   std::vector<ftblas_fault_t> faults;
   if (tl_have_armed) { faults.swap(tl_armed); tl_have_armed = false; }
@@ -364,7 +378,8 @@ struct ReportSink {
 // The core entry: device pointers, protected (FT) or not, explicit fault list.
 int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char tb, int64_t m, int64_t n,
                int64_t k, double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
-               double *C, int64_t ldc, ftblas_err_report_t *err, ReportSink *sink = nullptr) {
+               double *C, int64_t ldc, ftblas_err_report_t *err, ReportSink *sink = nullptr,
+               const std::vector<CsFault> &csf = {}) {
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
   if (rc) return rc;
   zero_report(err, k);
@@ -382,6 +397,10 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   }
   for (const auto &f : faults)
     if (f.i < 0 || f.i >= m || f.j < 0 || f.j >= n || f.step < 0 || f.step > k) return 3;
+  for (const auto &c : csf)
+    if (!ft || c.f.i < 0 || c.f.i >= m || c.f.j < 0 || c.f.j >= n || c.f.step < 0 || c.f.step > k ||
+        (c.lane != 1 && c.lane != 2))
+      return 3;
 
   ftk::Params p{};
   p.m = m; p.n = n; p.k = k; p.alpha = alpha; p.beta = beta;
@@ -415,16 +434,21 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
 
   // Bucket faults by (tile, stage); stable so same-stage faults keep the caller's order.
   std::vector<ftk::FaultDev> fd;
-  fd.reserve(faults.size());
-  for (const auto &f : faults) {
+  fd.reserve(faults.size() + csf.size());
+  // lane 0: the data accumulator (i, j); 1: the column checksum of column j of (i, j)'s unit
+  // (tile-local row -1 = the checksum row); 2: the row checksum of row i (column -1).
+  auto bucket = [&](const ftblas_fault_t &f, int lane) {
     const int64_t ti = f.i / tm, tj = f.j / tn;
     // step quantised to BK (R8); interval t = step_q / Kc (step_q == k: after the last update
     // of the last interval), stage local to the interval.
     const int64_t step_q = (f.step / ftk::BK) * ftk::BK;
     const int64_t t = std::min<int64_t>(step_q / Kc, T - 1);
     fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m + t * p.ntiles), (int32_t)((step_q - t * Kc) / ftk::BK),
-                               (int32_t)(f.i - ti * tm), (int32_t)(f.j - tj * tn), f.delta});
-  }
+                               lane == 1 ? -1 : (int32_t)(f.i - ti * tm), lane == 2 ? -1 : (int32_t)(f.j - tj * tn),
+                               f.delta});
+  };
+  for (const auto &f : faults) bucket(f, 0);
+  for (const auto &c : csf) bucket(c.f, c.lane);
   std::stable_sort(fd.begin(), fd.end(), [](const ftk::FaultDev &a, const ftk::FaultDev &b) {
     return a.tile != b.tile ? a.tile < b.tile : a.stage < b.stage;
   });
@@ -566,7 +590,8 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
                int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
                ftblas_err_report_t *err) {
   const std::vector<ftblas_fault_t> faults = take_armed();
-  return dgemm_core(ft, faults, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err);
+  const std::vector<CsFault> csf = take_armed_cs();
+  return dgemm_core(ft, faults, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err, nullptr, csf);
 }
 
 // The unfused ABFT baseline (kernels in unfused.cuh): encode passes,
@@ -574,6 +599,7 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
 int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A, int64_t lda,
                  const double *B, int64_t ldb, double beta, double *C, int64_t ldc, ftblas_err_report_t *err) {
   const std::vector<ftblas_fault_t> faults = take_armed();
+  if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
   if (rc) return rc;
   if (err) {
@@ -677,6 +703,7 @@ int dgemm_host_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, 
                     const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                     double *C, int64_t ldc, ftblas_err_report_t *err) {
   std::vector<ftblas_fault_t> faults = take_armed();
+  if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
   if (rc) return rc;
   zero_report(err, k);
@@ -967,6 +994,7 @@ int l1_grid(int64_t n, bool dmr) {
 
 int dscal_impl(bool ft, int64_t n, double alpha, double *x, int64_t incx, ftblas_dmr_report_t *rep) {
   std::vector<ftblas_fault_t> faults = take_armed();
+  if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   if (n < 0) return -1;
   if (n > 0 && x == nullptr) return -3;
   if (incx == 0) return -4;
@@ -991,6 +1019,7 @@ int dscal_impl(bool ft, int64_t n, double alpha, double *x, int64_t incx, ftblas
 int daxpy_impl(bool ft, int64_t n, double alpha, const double *x, int64_t incx, double *y, int64_t incy,
                ftblas_dmr_report_t *rep) {
   std::vector<ftblas_fault_t> faults = take_armed();
+  if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   if (n < 0) return -1;
   if (n > 0 && x == nullptr) return -3;
   if (incx == 0) return -4;
@@ -1017,6 +1046,7 @@ int daxpy_impl(bool ft, int64_t n, double alpha, const double *x, int64_t incx, 
 int dgemv_impl(bool ft, char trans, int64_t m, int64_t n, double alpha, const double *A, int64_t lda,
                const double *x, int64_t incx, double beta, double *y, int64_t incy, ftblas_dmr_report_t *rep) {
   std::vector<ftblas_fault_t> faults = take_armed();
+  if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   if (!is_n(trans) && !is_t(trans)) return -1;
   if (m < 0) return -2;
   if (n < 0) return -3;
@@ -1188,6 +1218,7 @@ int trsm_rec(TrsmCtx &c, int64_t r0, int64_t m) {
 int dtrsm_impl(bool ft, char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
                const double *A, int64_t lda, double *B, int64_t ldb, ftblas_err_report_t *err) {
   std::vector<ftblas_fault_t> faults = take_armed();
+  if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   const bool right = side == 'R' || side == 'r';
   if (!right && side != 'L' && side != 'l') return -1;
   const bool lower = uplo == 'L' || uplo == 'l';
@@ -1331,6 +1362,16 @@ int ftblas_inject_arm(const ftblas_fault_t *faults, int64_t n) {
 int ftblas_inject_disarm(void) {
   tl_armed.clear();
   tl_have_armed = false;
+  tl_armed_cs.clear();
+  return 0;
+}
+int ftblas_inject_arm_checksum(const ftblas_fault_t *faults, const int32_t *lanes, int64_t n) {
+  if (n < 0 || (n > 0 && (faults == nullptr || lanes == nullptr))) return 3;
+  tl_armed_cs.clear();
+  for (int64_t e = 0; e < n; ++e) {
+    if (lanes[e] != 1 && lanes[e] != 2) { tl_armed_cs.clear(); return 3; }
+    tl_armed_cs.push_back(CsFault{faults[e], lanes[e]});
+  }
   return 0;
 }
 

@@ -95,6 +95,7 @@ def load(path: str | None = None):
     L.ftblas_dgemm_noft_host.argtypes = gemm
     L.ftblas_inject_arm.argtypes = [ctypes.POINTER(Fault), i64]
     L.ftblas_inject_disarm.argtypes = []
+    L.ftblas_inject_arm_checksum.argtypes = [ctypes.POINTER(Fault), ctypes.POINTER(ctypes.c_int32), i64]
     L.ftblas_inject_seeded.argtypes = [ctypes.c_uint64, i64, i64, i64, i64, d, d,
                                        ctypes.POINTER(Fault)]
     L.ftblas_set_stream.argtypes = [P]
@@ -120,7 +121,7 @@ def load(path: str | None = None):
     L.ftblas_status_string.argtypes = [i32]
     L.ftblas_finalize.argtypes = []
     for fn in ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
-               "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
+               "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded", "ftblas_inject_arm_checksum",
                "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode",
                "ftblas_set_interval", "ftblas_get_geometry", "ftblas_finalize"):
         getattr(L, fn).restype = ctypes.c_int
@@ -129,7 +130,7 @@ def load(path: str | None = None):
 
 
 EXPORTED = ("ftblas_dgemm", "ftblas_dgemm_unfused", "ftblas_dgemm_noft", "ftblas_dgemm_host", "ftblas_dgemm_noft_host",
-            "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded",
+            "ftblas_inject_arm", "ftblas_inject_disarm", "ftblas_inject_seeded", "ftblas_inject_arm_checksum",
             "ftblas_set_stream", "ftblas_set_correction", "ftblas_set_encode", "ftblas_set_interval",
             "ftblas_get_geometry", "ftblas_take_launch_count", "ftblas_status_string", "ftblas_finalize",
             "ftblas_dscal", "ftblas_dscal_noft", "ftblas_daxpy", "ftblas_daxpy_noft", "ftblas_dgemv",
@@ -304,6 +305,18 @@ def ftblas_inject_arm(faults):
     for e, (i, j, s, d) in enumerate(faults):
         arr[e] = Fault(int(i), int(j), int(s), float(d))
     _check("ftblas_inject_arm", load().ftblas_inject_arm(arr, len(faults)))
+
+
+def ftblas_inject_arm_checksum(faults):
+    """Checksum-lane faults (test hook, reading R6): (i, j, step, delta, lane) with lane 1 = the
+    column checksum of column j, 2 = the row checksum of row i, of the unit containing (i, j)."""
+    faults = list(faults)
+    arr = (Fault * max(len(faults), 1))()
+    lanes = (ctypes.c_int32 * max(len(faults), 1))()
+    for e, (i, j, s, d, lane) in enumerate(faults):
+        arr[e] = Fault(int(i), int(j), int(s), float(d))
+        lanes[e] = int(lane)
+    _check("ftblas_inject_arm_checksum", load().ftblas_inject_arm_checksum(arr, lanes, len(faults)))
 
 
 def ftblas_inject_disarm():

@@ -405,3 +405,21 @@ def test_gemm_elements_matches_full():
     assert np.array_equal(el, full[ii, jj])
     S = oracle.abs_product_elements("T", "T", k, A, k, B, n, ii, jj)
     assert np.allclose(S, (np.abs(A.T) @ np.abs(B.T))[ii, jj], rtol=1e-13)
+
+
+def test_checksum_lane_fault_flags_one_direction_and_recomputes():
+    """Reading R6: a fault in a CARRIED checksum (lane 1: the column checksum of column j, lane 2:
+    the row checksum of row i) flags that one column (row) and no row (column): out of the
+    one-error pattern, so the unit is recomputed; on integer data the residual is exactly -delta
+    and C equals the exact product."""
+    rng = np.random.default_rng(37)
+    m, n, k = 70, 50, 40
+    A, B = int_mats(rng, m, n, k)
+    exact = A.astype(np.int64) @ B.astype(np.int64)
+    for lane, (i, j) in ((1, (5, 9)), (2, (40, 33))):
+        C, rep = run(A, B, BM=32, BN=32, BK=8, faults=[(i, j, 16, 3.0, lane)])
+        assert (rep.detected, rep.corrected, rep.recomputed) == (1, 0, 1)
+        (t, ei, ej, kind, rr, rc), = rep.events
+        assert kind == 2 and (ei, ej) == ((i // 32) * 32, (j // 32) * 32)
+        assert (rr, rc) == ((0.0, -3.0) if lane == 1 else (-3.0, 0.0))
+        assert np.array_equal(C, exact)
