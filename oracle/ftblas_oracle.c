@@ -176,6 +176,23 @@ static double dot_upto(const unit_ctx_t *x, int64_t i, int64_t j, int64_t pe) {
   return s;
 }
 
+/* The unit's carried checksums recomputed from scratch over p in [0, pe), fault-free: the same
+ * encode and outer-product maintenance as the main loop.  Used when a unit
+ * is recomputed (reading R6): its whole C^f block -- data and checksums -- is formed afresh, so a
+ * fault that sat in a checksum lane does not outlive the recompute. */
+static void carry_fresh(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t j0, int64_t bn, int64_t pe,
+                        double *cs_col, double *cs_row) {
+  for (int64_t j = 0; j < bn; ++j) cs_col[j] = 0.0;
+  for (int64_t i = 0; i < bm; ++i) cs_row[i] = 0.0;
+  for (int64_t p = 0; p < pe; ++p) {
+    double a_sum = 0.0, b_sum = 0.0;
+    for (int64_t i = 0; i < bm; ++i) a_sum += op_at(x->A, x->lda, x->tA, i0 + i, p);
+    for (int64_t j = 0; j < bn; ++j) b_sum += op_at(x->B, x->ldb, x->tB, p, j0 + j);
+    for (int64_t j = 0; j < bn; ++j) cs_col[j] += a_sum * op_at(x->B, x->ldb, x->tB, p, j0 + j);
+    for (int64_t i = 0; i < bm; ++i) cs_row[i] += op_at(x->A, x->lda, x->tA, i0 + i, p) * b_sum;
+  }
+}
+
 static void apply_faults_at(double *acc, double *cs_col, double *cs_row, int64_t bm, int64_t i0, int64_t j0,
                             const or_fault_t *f, int64_t nf, int64_t BK, int64_t step_q_wanted) {
   for (int64_t e = 0; e < nf; ++e) {
@@ -279,9 +296,12 @@ static int64_t verify_unit(const unit_ctx_t *x, int64_t i0, int64_t bm, int64_t 
       cnt->corrected += 1;
       e.kind = 1; e.i = i0 + fr; e.j = j0 + fc;
     } else {
-      /* Out of the one-error model (R6): recompute the whole unit once, no re-verify. */
+      /* Out of the one-error model (R6): recompute the whole unit once, no re-verify of this
+       * interval; its carried checksums are formed afresh too, so later intervals verify the
+       * recomputed block. */
       for (int64_t j = 0; j < bn; ++j)
         for (int64_t i = 0; i < bm; ++i) acc[i + j * bm] = dot_upto(x, i0 + i, j0 + j, pe);
+      if (t < T - 1) carry_fresh(x, i0, bm, j0, bn, pe, cs_col, cs_row);
       cnt->recomputed += 1;
       e.kind = 2; e.i = i0; e.j = j0;
     }

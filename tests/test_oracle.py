@@ -423,3 +423,20 @@ def test_checksum_lane_fault_flags_one_direction_and_recomputes():
         assert kind == 2 and (ei, ej) == ((i // 32) * 32, (j // 32) * 32)
         assert (rr, rc) == ((0.0, -3.0) if lane == 1 else (-3.0, 0.0))
         assert np.array_equal(C, exact)
+
+
+def test_recomputed_unit_gets_fresh_checksums_for_later_intervals():
+    """Reading R6 with intervals: a unit recomputed at the end of interval t is re-formed as a
+    whole C^f block (data AND carried checksums), so a checksum-lane fault of interval 0 is
+    reported once (interval 0, recomputed) and interval 1 of the same unit verifies clean;
+    a data fault in interval 1 of that unit is then corrected as usual."""
+    rng = np.random.default_rng(43)
+    m, n, k = 40, 40, 64
+    A, B = int_mats(rng, m, n, k)
+    exact = A.astype(np.int64) @ B.astype(np.int64)
+    C, rep = run(A, B, BM=32, BN=32, BK=8, Kc=32, faults=[(3, 4, 8, 5.0, 1)])
+    assert [(e[0], e[3]) for e in rep.events] == [(0, 2)] and rep.units_checked == 4 * 2
+    assert np.array_equal(C, exact)
+    C, rep = run(A, B, BM=32, BN=32, BK=8, Kc=32, faults=[(3, 4, 8, 5.0, 1), (6, 7, 40, 2.0)])
+    assert [(e[0], e[1], e[2], e[3]) for e in rep.events] == [(0, 0, 0, 2), (1, 6, 7, 1)]
+    assert np.array_equal(C, exact)
