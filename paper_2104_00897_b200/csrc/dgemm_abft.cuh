@@ -73,12 +73,11 @@ struct Params {
   double *C;
   int64_t ldc;
   int tiles_m, tiles_n, nk;
-  // Verification intervals: the k-loop is split
-  // into T intervals of Kc rank-1 updates; CTA L works on interval t = L / ntiles over
-  // k in [t*Kc, min((t+1)*Kc, k)) and, when T > 1, writes its verified raw increment to the
-  // workspace slice C + t*wstride (alpha = 1, beta = 0; a reduction kernel finishes C).
-  int64_t Kc, wstride;
-  int T, ntiles, t_base;
+  // Verification intervals: every CTA verifies
+  // its tile online after every Kc rank-1 updates (T intervals, the last one ragged), from the
+  // live accumulators; Kc is a multiple of BK.
+  int64_t Kc;
+  int T, ntiles;
   // Launched as 2-CTA clusters (fused encode): consecutive CTAs 2c, 2c+1 hold tiles of one
   // tile column, so they stage the same B_J: each encodes half of its 16 k-slots and the pair
   // swaps halves through distributed shared memory.  `total` = real CTAs of this launch.
@@ -166,6 +165,15 @@ __device__ __forceinline__ bool pub_ok(double v) { return __double_as_longlong(v
 __device__ __forceinline__ bool pub_ok(unsigned v) { return v != 0xFFFFFFFFu; }
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// Volatile 32-bit shared-memory word q of the array at shared address base.
+__device__ __forceinline__ int ld_sv(uint32_t base, int q) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(base + 4u * q) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_sv(uint32_t base, int q, int v) {
+  asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(base + 4u * q), "r"(v) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -619,14 +627,15 @@ __device__ __forceinline__ void enc_operand(const double *s, int lane, int cr, d
 // Tile geometry kept in shared memory: the MMA warps re-read it after the k-loop, so none of
 // it has to stay live in registers across the DMMA stream.
 struct TileGeom {
-  int ti, tj, i0, j0, bm_eff, bn_eff, oa, ob, cra, crb, t;
-  int64_t k0, k1;  // this CTA's k range [k0, k1) (one verification interval)
+  int ti, tj, i0, j0, bm_eff, bn_eff, oa, ob, cra, crb;
+  int64_t k0, k1;  // the k range [k0, k1) = [0, k)
 };
 __device__ __forceinline__ TileGeom load_geom(const TileGeom &g) {
   const volatile TileGeom &v = g;
-  return TileGeom{v.ti, v.tj, v.i0, v.j0, v.bm_eff, v.bn_eff, v.oa, v.ob, v.cra, v.crb, v.t, v.k0, v.k1};
+  return TileGeom{v.ti, v.tj, v.i0, v.j0, v.bm_eff, v.bn_eff, v.oa, v.ob, v.cra, v.crb, v.k0, v.k1};
 }
 
+constexpr int MAX_FIX = 32;  // distinct corrected cells per tile recomputed in the epilogue (R4)
 struct SmemTail {
   TileGeom geo;
   // Cluster-pair B encode: the partner's 8 k-slot sums of B_J e per stage and its half maximum;
@@ -637,17 +646,24 @@ struct SmemTail {
   uint64_t mfull[STAGES], mfree[STAGES];
   int share;  // this CTA encodes half of B and swaps it with its cluster partner
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
-  double dres[256];                // residuals: 0..127 columns, 128..255 rows
+  // Online verification (check_unit): the staging strip (128 rows x 16 columns), the reference
+  // sums, the carried checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
+  double strip[128 * 16], colsum[128], rowsum[128], cs_col[128], cs_row[128];
+  double dres[256];
   double red[NTHREADS / 32];
-  unsigned int amax_hi, bmax_hi;   // max finite |op(A)|, |op(B)| high words (R1')
-  int first_row, first_col;
-  int retry;
+  unsigned int amax_hi, bmax_hi;   // PREPASS: the blocks' whole-k maxima (R1' high words)
+  unsigned int int_am[8], int_bm[8];  // per-interval (slot t & 7) stage maxima from the encoders
+  unsigned int cum_am, cum_bm;     // maxima of the intervals already verified
+  int first_row[2], first_col[2];  // first flagged row / column, by check parity
+  int nfix, fix[MAX_FIX];          // corrected cells (staged row | col << 8) to recompute (R4)
+  int wstate[N_MMA_WARPS][8];      // per MMA warp: segment state of the k-loop (mma_role)
+  int retry;                       // -1: done; else the interval whose check asked for a recompute
 };
 constexpr size_t SMEM_BYTES = 1024 + sizeof(double) * STAGES * STAGE_ELEMS + sizeof(SmemTail);
 
 // Named barriers (id 0 is __syncthreads).  Both roles execute the same sequence of the
 // CTA-wide ones; the 256-thread ones are private to the MMA warpgroups.
-enum { BAR_RING_FREE = 1, BAR_CTILE = 2, BAR_FLAGS_R = 3, BAR_FLAGS_C = 4, BAR_DECIDE = 5, BAR_RED = 6 };
+enum { BAR_RING_FREE = 1, BAR_CTILE = 2, BAR_FLAGS_R = 3, BAR_FLAGS_C = 4, BAR_DECIDE = 5, BAR_RED = 6, BAR_PART = 7 };
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -672,7 +688,7 @@ __device__ __forceinline__ int mma_warp(int w) { return CS_HIGH ? w : w - N_CS_W
 struct Ctx {
   double *ring;
   SmemTail *tl;
-  int tid, lane, warp, tile, ti, tj, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi, t;
+  int tid, lane, warp, tile, ti, tj, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi;
   int64_t k0, k1;
   // Protected tiles: TMA boxes start at the even coordinate xs = x0 - (x0 & 1) (the contiguous
   // dimension of a TMA box must start 16-byte aligned), so tile-local data row i sits in
@@ -782,15 +798,16 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       if (lane == 0) st_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg, hm);
     }
   };
+  const int KcS = max(1, (int)(P.Kc / BK));
+  int t_done = -1;  // intervals <= t_done are not verified again (retry after a recompute decision)
   for (int attempt = 0;; ++attempt) {
-    const bool verify = FT && attempt == 0;
+    const bool verify = FT && t_done < P.T - 1;
     if (lane == 0)
       for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
     // B_J e published by tile row 0 is copied per stage like e^T A_I.  Publication only
     // happens in launches without clusters, so a cluster pair (share) never copies.
     const bool b_sub = P.Bsh && x.ti != 0;
     const bool share = verify && tl.share;
-    uint32_t amax_hi = 0u, bmax_hi = 0u;
     // Encode jobs.  Stages 0..3 of the tile: the two operands of a stage go to two warps
     // (warps 0, 2 share stages 0 and 2, warps 1, 3 stages 1 and 3; warps 0, 1 take A of stages
     // 0 / 1 and B of 2 / 3, warps 2, 3 the opposite), so the first stage -- on the critical path
@@ -806,6 +823,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       const bool doB = !split || !doA;
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
+        uint32_t amax_hi = 0u, bmax_hi = 0u;  // this stage's slice maxima (R1' high words)
         const long long t0 = FT_DEV_PROF(P) ? clock64() : 0;
         const bool pubs = !(P.Ac || (FT_DEV_MODE(P) & 3));
         PubA pa = pubs && doA ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
@@ -907,6 +925,11 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           }
          }
         }
+        if (!P.Ac && lane == 0) {  // the interval's maxima, read by the MMA warps at its check
+          const int tint = min(s / KcS, P.T - 1) & 7;
+          if (doA) atomicMax(&tl.int_am[tint], amax_hi);
+          if (doB) atomicMax(&tl.int_bm[tint], bmax_hi);
+        }
         fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
         __syncwarp();
         if (lane == 0) {  // one arrival per operand job (the barrier expects two per stage)
@@ -924,103 +947,184 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       if (lane == 0 && (s & 3) == warp && s2 >= STAGES && s2 < nk) issue(s2);
       __syncwarp();
     }
-    if (verify && !P.Ac && lane == 0) { atomicMax(&tl.amax_hi, amax_hi); atomicMax(&tl.bmax_hi, bmax_hi); }
     stage_base += nk;
-    bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone; maxima visible
+    bar_sync(BAR_RING_FREE, NTHREADS);  // ring consumed by everyone
     if (!verify) return;
-    bar_sync(BAR_DECIDE, NTHREADS);     // MMA warps decided: clean / corrected / recompute
-    if (!tl.retry) return;
+    bar_sync(BAR_DECIDE, NTHREADS);     // MMA warps decided: done, or recompute from k = 0
+    const int r = tl.retry;
+    if (r < 0) return;
+    t_done = r;
   }
 }
 
-// ---- verification: reference checksums r from the computed C_IJ (staged in
-// ctile) against the carried checksums in row / column cr of C^f; flag, classify, correct in
-// place (R1, R4, R6), record the event.  Returns true when the
-// unit must be recomputed.  Called by the 256 MMA threads (vt = 0..255).
+// ---- online verification (§II.A, 258 §V.A) from the LIVE accumulators.
+// The MMA tile is the unit's C^f block: staged row cra holds the carried column checksums
+// (e^T A_I) B_J, staged column crb the carried row checksums A_I (B_J e).  At the
+// end of verification interval t (after kt = min((t+1) Kc, k) rank-1 updates) the 256 MMA
+// threads form the reference checksums e^T C and C e of the partial product held in their
+// registers: per thread over its 8 rows / 8 columns of the m8n8k4 accumulator fragments, then
+// warp shuffles over the lanes sharing a column (xor 4, 8, 16) or a row (xor 1, 2), then a small
+// shared-memory exchange across the 2 x 4 warp grid.  Residuals d = r - cs against tau (DESIGN
+// R1, R1', R17, clamped: R13), flags counted with bar.red.popc; exactly one flagged row and one
+// flagged column -> the element at their intersection is corrected in its owner's register
+// (recompute over [0, kt) or subtract; R4); any other pattern -> the unit is
+// recomputed (R6).  Returns true for the latter.
 template <bool AKM, bool BKM>
-__device__ __noinline__ bool verify_tile(const Params &P, SmemTail &tl, double *ctile, int vt, int mw) {
-  const TileGeom x = load_geom(tl.geo);
-  const int lane = vt & 31;
-      // ctile is indexed by staged rows / columns: data row i at i + oa, data column j at j + ob.
-      // The sums run over the data only (a partial tile's checksum row / column sits right after
-      // its data).
-      const int cidx = vt & 127;
-      const bool is_row = vt >= 128;
-      double r = 0.0, cs = 0.0;
-      if (cidx < DM) {
-        if (is_row) {
-          const double *rowp = ctile + (cidx + x.oa);
-  #pragma unroll 9
-          for (int j = 0; j < x.bn_eff; ++j) r += rowp[(j + x.ob) * LDC_S];
-          cs = rowp[x.crb * LDC_S];  // A_I (B_J e)
-        } else {
-          const double *colp = ctile + (cidx + x.ob) * LDC_S;
-  #pragma unroll 9
-          for (int i = 0; i < x.bm_eff; ++i) r += colp[i + x.oa];
-          cs = colp[x.cra];  // (e^T A_I) B_J
-        }
-      }
-      const double d = r - cs;
-      // R1': maxima rounded up to the largest double with the same high word.
-      const double amx = __longlong_as_double((long long)(((unsigned long long)tl.amax_hi << 32) | 0xFFFFFFFFull));
-      const double bmx = __longlong_as_double((long long)(((unsigned long long)tl.bmax_hi << 32) | 0xFFFFFFFFull));
-      const int64_t kt = x.k1 - x.k0;  // rank-1 updates in this interval
-      const int len = is_row ? x.bn_eff : x.bm_eff;
-      const double nu = (double)(kt + len) * 0x1p-53;
-      // DESIGN.md R1, R17: 2 gamma(kt + len) for the two sums plus 2^-50 = 8u for the fixed-point
-      // encode (per element below 2^-50 max|x|, summed over len rows and kt k-slots).
-      // Clamped to the largest finite double (R13): a NaN or infinite residual always flags.
-      const double tau = fmin((2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx, 0x1.fffffffffffffp1023);
-      const bool valid = is_row ? (cidx < x.bm_eff) : (cidx < x.bn_eff);
-      const bool flag = valid && !(fabs(d) <= tau) && !(FT_DEV_MODE(P) & 4);
-      tl.dres[vt] = d;
-      if (flag) atomicMin(is_row ? &tl.first_row : &tl.first_col, cidx);
-      const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
-      const int nfc = bar_popc(BAR_FLAGS_C, 256, flag && !is_row);
-      const bool multi = !(nfr == 0 && nfc == 0) && !(nfr == 1 && nfc == 1);
-      const int fr = tl.first_row, fc = tl.first_col;
-      if (nfr == 1 && nfc == 1) {
-        // Single error at the intersection (i0+fr, j0+fc): correct in place.
-        if (P.correct_mode == 1) {
-          if (vt == 0) ctile[(fc + x.ob) * LDC_S + fr + x.oa] -= tl.dres[fc];  // subtract d_col
-        } else {
-          // Recompute C_ij with a fresh k-long dot product (R4).
-          const int64_t gi = x.i0 + fr, gj = x.j0 + fc;
-          double part = 0.0;
-          for (int64_t p = x.k0 + vt; p < x.k1; p += 256) {
-            const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
-            const double bv = BKM ? P.B[p + gj * P.ldb] : P.B[gj + p * P.ldb];
-            part = fma(av, bv, part);
-          }
-  #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-          if (lane == 0) tl.red[mw] = part;
-          bar_sync(BAR_RED, 256);
-          if (vt == 0) {
-            double v = 0.0;
-  #pragma unroll
-            for (int q = 0; q < N_MMA_WARPS; ++q) v += tl.red[q];
-            ctile[(fc + x.ob) * LDC_S + fr + x.oa] = v;
-          }
-        }
-      }
-      if (vt == 0 && (nfr | nfc)) {
-        atomicAdd(&P.counters[CNT_DETECTED], 1ull);
-        atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
-        const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
-        if ((long long)slot < P.ev_cap)
-          P.events[slot] = multi ? EventDev{(long long)(x.i0 + P.ev_row_off), (long long)(x.j0 + P.ev_col_off), 2, x.t, nfr ? tl.dres[128 + fr] : 0.0,
-                                            nfc ? tl.dres[fc] : 0.0}
-                                 : EventDev{(long long)(x.i0 + fr + P.ev_row_off), (long long)(x.j0 + fc + P.ev_col_off), 1, x.t, tl.dres[128 + fr],
-                                            tl.dres[fc]};
-      }
-      if (vt == 0) tl.retry = multi ? 1 : 0;
-      if (multi) fence_proxy_async();  // generic writes to the ring (C tile) before TMA reuses it
-      bar_sync(BAR_DECIDE, NTHREADS);
-  return multi;
+__device__ __forceinline__ int acc_owner_index(int si, int sj, int wm, int wn, int lane) {
+  // Register index (a*4 + b)*2 + e of staged element (si, sj) in this thread, or -1.
+  const int lr = si & 63, lc = sj & 31;
+  const int fmt = AKM ? (lr >> 3) : 2 * (lr >> 4) + (lr & 1);
+  const int rr = lr & 7;  // K-major: row in the 8-row tile = 4*(g&1) + (g>>1)
+  const int fg = AKM ? (((rr & 3) << 1) | (rr >> 2)) : ((lr & 15) >> 1);
+  const int fnt = BKM ? (lc >> 3) : 2 * (lc >> 4) + (lc & 1);
+  const int cr = lc & 7;  // K-major: column in the 8-column tile, same mapping
+  const int cc = BKM ? (((cr & 3) << 1) | (cr >> 2)) : ((lc & 15) >> 1);  // n-index
+  const bool owner = (si >> 6) == wm && (sj >> 5) == wn && lane == fg * 4 + (cc >> 1);
+  return owner ? (fmt * 4 + fnt) * 2 + (cc & 1) : -1;
 }
 
-// ---------------- warpgroups 1-2: MMA warps (+ epilogue)
+// The accumulators stay in registers: they are staged through a 16 KB shared-memory strip, one
+// (b, e) accumulator slot of every thread per round (a 128-row x 16-column strip of the tile),
+// and reduced from there: thread i < 128 keeps the running row sum of row i, threads 128..255
+// sum the strip's columns (8 threads x 16 rows per column, then xor-shuffles).  Staging only
+// reads the accumulators, so the DMMA k-loop keeps its register allocation.
+struct CheckOut {
+  int multi;    // 1: recompute the unit (R6)
+  int si, sj;   // single error: the located staged cell (si = -1: none)
+  double dcol;  // the located magnitude d_col to subtract from it
+};
+template <bool AKM, bool BKM>
+__device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, const double (&acc)[8][4][2], int t,
+                                               int64_t kt, int mw, int wm, int wn, int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+  const int vt = mw * 32 + lane;  // 0..255
+  const int cra = tl.geo.cra, crb = tl.geo.crb;
+  double rsum = 0.0;  // vt < 128: row vt over the data columns (checksum column crb excluded)
+  // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round
+  // rd = 2 b + e.  The rounds run as a rolled loop (one copy of the reduction code); only the
+  // staging selects its accumulator slot by a switch on the round.
+  const int q = wn * 4 + tq;
+  double *const st = tl.strip + q * 128 + wm * 64;
+#pragma unroll 1
+  for (int rd = 0; rd < 8; ++rd) {
+    switch (rd) {
+#define FT_STAGE_ROUND(B, E)                                                           \
+  case 2 * B + E:                                                                      \
+    _Pragma("unroll") for (int a = 0; a < 8; ++a) st[tile_row<AKM>(a, g)] = acc[a][B][E]; \
+    break;
+      FT_STAGE_ROUND(0, 0) FT_STAGE_ROUND(0, 1) FT_STAGE_ROUND(1, 0) FT_STAGE_ROUND(1, 1)
+      FT_STAGE_ROUND(2, 0) FT_STAGE_ROUND(2, 1) FT_STAGE_ROUND(3, 0) FT_STAGE_ROUND(3, 1)
+#undef FT_STAGE_ROUND
+    }
+    bar_sync(BAR_PART, 256);
+    const int b = rd >> 1, e = rd & 1;
+    if (vt < 128) {
+      const int r = vt;
+      for (int qq = 0; qq < 16; ++qq) {
+        const int col = (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
+        const double v = tl.strip[qq * 128 + r];
+        if (col != crb) rsum += v;
+        else tl.cs_row[r] = v;  // carried A_I (B_J e)
+      }
+    } else {
+      const int qq = (vt - 128) >> 3, part = vt & 7;  // column qq, rows 16 part .. 16 part + 15
+      double c = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = 16 * part + i;
+        const double v = tl.strip[qq * 128 + r];
+        if (r != cra) c += v;
+      }
+#pragma unroll
+      for (int o = 1; o <= 4; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      const int col = (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
+      if (part == 0) {
+        tl.colsum[col] = c;
+        tl.cs_col[col] = tl.strip[qq * 128 + cra];  // carried (e^T A_I) B_J
+      }
+    }
+    bar_sync(BAR_PART, 256);  // the strip is rewritten by the next round
+  }
+  if (vt < 128) tl.rowsum[vt] = rsum;
+  bar_sync(BAR_PART, 256);
+  const TileGeom x = load_geom(tl.geo);
+  // Cumulative maxima of op(A)_I and op(B)_J over the updates so far (R1'): the running value
+  // plus the encoders' maxima of interval t's stages (slot t & 7; PREPASS: whole-k presets).
+  const uint32_t amax_hi = max(tl.cum_am, tl.int_am[t & 7]), bmax_hi = max(tl.cum_bm, tl.int_bm[t & 7]);
+  // one thread per data column (vt < 128) / data row (vt >= 128): residual, tau, flag
+  const int par = t & 1;
+  const int cidx = vt & 127;
+  const bool is_row = vt >= 128;
+  double d = 0.0;
+  bool valid = false;
+  if (cidx < DM) {
+    if (is_row) {
+      const int sr = cidx + x.oa;
+      valid = cidx < x.bm_eff;
+      d = tl.rowsum[sr] - tl.cs_row[sr];
+    } else {
+      const int sc = cidx + x.ob;
+      valid = cidx < x.bn_eff;
+      d = tl.colsum[sc] - tl.cs_col[sc];
+    }
+  }
+  // R1': maxima rounded up to the largest double with the same high word.
+  const double amx = __longlong_as_double((long long)(((unsigned long long)amax_hi << 32) | 0xFFFFFFFFull));
+  const double bmx = __longlong_as_double((long long)(((unsigned long long)bmax_hi << 32) | 0xFFFFFFFFull));
+  const int len = is_row ? x.bn_eff : x.bm_eff;
+  const double nu = (double)(kt + len) * 0x1p-53;
+  // DESIGN.md R1, R17: 2 gamma(kt + len) for the two sums plus 2^-50 = 8u for the fixed-point
+  // encode (per element below 2^-50 max|x|, summed over len rows and kt k-slots); clamped to the
+  // largest finite double (R13): a NaN or infinite residual always flags.
+  const double tau = fmin((2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx, 0x1.fffffffffffffp1023);
+  const bool flag = valid && !(fabs(d) <= tau) && !(FT_DEV_MODE(P) & 4);
+  tl.dres[vt] = d;
+  if (flag) atomicMin(is_row ? &tl.first_row[par] : &tl.first_col[par], cidx);
+  const int nfr = bar_popc(BAR_FLAGS_R, 256, flag && is_row);
+  const int nfc = bar_popc(BAR_FLAGS_C, 256, flag && !is_row);
+  if (vt == 0) {  // everyone has read the maxima and the other parity's slots: roll them over
+    tl.first_row[par ^ 1] = 0x7fffffff;
+    tl.first_col[par ^ 1] = 0x7fffffff;
+    tl.cum_am = amax_hi;
+    tl.cum_bm = bmax_hi;
+    tl.int_am[t & 7] = tl.int_bm[t & 7] = 0u;  // the slot of interval t + 8
+  }
+  CheckOut out{0, -1, 0, 0.0};
+  if (nfr == 0 && nfc == 0) return out;
+  const bool multi = !(nfr == 1 && nfc == 1);
+  const int fr = tl.first_row[par], fc = tl.first_col[par];
+  if (!multi) {
+    // Single error at the intersection (i0+fr, j0+fc): the caller subtracts the located
+    // magnitude d_col in its owner's register now, so the next intervals verify
+    // the corrected partial product; in recompute mode (R4) the element is replaced by a fresh
+    // k-long dot product in the epilogue (fix list), which equals the oracle's recomputed
+    // partial plus its later updates.
+    const int si = fr + x.oa, sj = fc + x.ob;
+    out.si = si;
+    out.sj = sj;
+    out.dcol = tl.dres[fc];
+    if (vt == 0 && P.correct_mode != 1) {
+      const int cell = si | (sj << 8);
+      int q = 0;
+      while (q < tl.nfix && tl.fix[q] != cell) ++q;
+      if (q == tl.nfix && q < MAX_FIX) tl.fix[tl.nfix++] = cell;
+    }
+  }
+  if (vt == 0) {
+    atomicAdd(&P.counters[CNT_DETECTED], 1ull);
+    atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
+    const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
+    if ((long long)slot < P.ev_cap)
+      P.events[slot] = multi ? EventDev{(long long)(x.i0 + P.ev_row_off), (long long)(x.j0 + P.ev_col_off), 2, t,
+                                        nfr ? tl.dres[128 + fr] : 0.0, nfc ? tl.dres[fc] : 0.0}
+                             : EventDev{(long long)(x.i0 + fr + P.ev_row_off), (long long)(x.j0 + fc + P.ev_col_off), 1, t,
+                                        tl.dres[128 + fr], tl.dres[fc]};
+  }
+  out.multi = multi ? 1 : 0;
+  return out;
+}
+
+// ---------------- warpgroups 1-2: MMA warps (+ online verification and epilogue)
 template <bool AKM, bool BKM, bool FT>
 __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   SmemTail &tl = *x.tl;
@@ -1046,71 +1150,55 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   const bool active = FT ? (wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1))
                          : (!SKIP || (wm * 64 < x.bm_eff && wn * 32 < x.bn_eff));
   double acc[8][4][2];
-  int stage_base = 0;
+  // Segment state that changes only between segments lives in this warp's shared-memory slots
+  // (lane-uniform), not in registers across the DMMA loop: next fault stage, next interval end,
+  // next fault index, the interval of a recompute decision in this attempt.
+  // (32-bit shared addresses through volatile ld/st.shared: no generic pointer held in registers)
+  const uint32_t ws = smem_u32(&tl.wstate[mw][0]);
+  enum { W_NEXT_STAGE = 0, W_NEXT_CHECK, W_FNEXT, W_FAILED, W_BASE };
+  if (lane == 0) st_sv(ws, W_BASE, 0);
   for (int attempt = 0;; ++attempt) {
-    const bool verify = FT && attempt == 0;
-    const bool inject = attempt == 0 && x.f_lo < x.f_hi;
-    int fnext = x.f_lo;
-    int next_stage = inject ? P.faults[fnext].stage : 0x7fffffff;
+    // Interval of the last recompute decision (tl.retry, -1 in the first attempt): intervals
+    // <= t_done are neither re-injected nor re-verified (the unit restarts from k = 0).
+    const int t_done = tl.retry;
+    const bool verify = FT && t_done < P.T - 1;
+    if (lane == 0) {
+      st_sv(ws, W_FNEXT, x.f_lo);
+      st_sv(ws, W_NEXT_STAGE, x.f_lo < x.f_hi ? P.faults[x.f_lo].stage : 0x7fffffff);
+      // Stage index at which the next verification interval ends (Kc = KcS stages); the last
+      // interval is checked at the virtual stage nk + 1.
+      st_sv(ws, W_NEXT_CHECK, !verify ? 0x7fffffff
+                         : (t_done + 1 < P.T - 1 ? (t_done + 2) * max(1, (int)(P.Kc / BK)) : nk + 1));
+      st_sv(ws, W_FAILED, -1);
+    }
+    __syncwarp();
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    auto apply_faults = [&](int s) {
-      while (s == next_stage) {
-        const FaultDev f = P.faults[fnext];
-        const TileGeom gf = load_geom(tl.geo);
-        // staged row / column; -1 = the unit's checksum row / column (checksum-lane faults)
-        const int si = f.li < 0 ? gf.cra : f.li + gf.oa, sj = f.lj < 0 ? gf.crb : f.lj + gf.ob;
-        const int lr = si & 63, lc = sj & 31;
-        const int fmt = AKM ? (lr >> 3) : 2 * (lr >> 4) + (lr & 1);
-        const int rr = lr & 7;  // K-major: row in the 8-row tile = 4*(g&1) + (g>>1)
-        const int fg = AKM ? (((rr & 3) << 1) | (rr >> 2)) : ((lr & 15) >> 1);
-        const int fnt = BKM ? (lc >> 3) : 2 * (lc >> 4) + (lc & 1);
-        const int cr = lc & 7;  // K-major: column in the 8-column tile, same mapping
-        const int cc = BKM ? (((cr & 3) << 1) | (cr >> 2)) : ((lc & 15) >> 1);  // n-index
-        // Register index of the owning accumulator, -1 for every other thread.  Select-based
-        // (no dynamic register indexing) so the accumulators stay in registers.
-        const bool owner = (si >> 6) == wm && (sj >> 5) == wn && lane == fg * 4 + (cc >> 1);
-        const int fidx = owner ? (fmt * 4 + fnt) * 2 + (cc & 1) : -1;
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const double v = acc[a][b][e];
-              acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v + f.delta : v;
-            }
-        ++fnext;
-        next_stage = fnext < x.f_hi ? P.faults[fnext].stage : 0x7fffffff;
-      }
-    };
     // The protected pass waits for the encoded stage (TMA bytes + checksum row/column), the
     // unprotected one for the TMA bytes only.
     // 32-bit shared address of the barrier array to wait on (enc = full + STAGES).
     const uint32_t ready = smem_u32(tl.full) + ((verify && !(FT_DEV_MODE(P) & 8)) ? STAGES * 8u : 0u);
-#ifdef FTBLAS_DEV_TIMELINE
-    long long tl_a = clock64(), tl_b = tl_a;
-    if (attempt == 0 && nk > 0) {
-      mbar_wait_u32(ready + 8u * (stage_base % STAGES), (stage_base / STAGES) & 1);
-      tl_b = clock64();
-    }
-#endif
-    // The k-loop runs in segments between fault stages, so that the DMMA loop body carries no
-    // injection code (which would make the register allocator shuffle accumulators).
-    for (int s = 0; s < nk;) {
-      const int s_end = __shfl_sync(0xffffffffu, next_stage < nk ? next_stage : nk, 0);
+    // The k-loop runs in segments between fault stages and interval ends, so that the DMMA loop
+    // body carries neither injection nor verification code (which would make the register
+    // allocator shuffle accumulators).
+    // Stage counters run on the global stage index gs (ring slot gs % STAGES, parity
+    // (gs / STAGES) & 1); this attempt's first stage is kept in the warp's shared slot W_BASE.
+    for (int s = 0;;) {
+      const int base = ld_sv(ws, W_BASE);
+      int gs = base + s;
+      const int gs_end = base + __shfl_sync(0xffffffffu, min(min(ld_sv(ws, W_NEXT_STAGE), ld_sv(ws, W_NEXT_CHECK)), nk), 0);
       if (SKIP && !active) {  // nothing of this warp's quarter is used: release the stages only
-        for (; s < s_end; ++s) {
-          const int gs = stage_base + s, slot = gs % STAGES;
+        for (; gs < gs_end; ++gs) {
+          const int slot = gs % STAGES;
           mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
           __syncwarp();
           if (lane == 0) mbar_arrive(&tl.empty[slot]);
         }
       }
-      for (; s < s_end; ++s) {
-        const int gs = stage_base + s, slot = gs % STAGES;
+      for (; gs < gs_end; ++gs) {
+        const int slot = gs % STAGES;
         mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
         const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
 #pragma unroll
@@ -1128,58 +1216,145 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&tl.empty[slot]);
       }
-      if (s < nk) apply_faults(s);  // s == next_stage: faults due before stage s's updates
-    }
-    if (inject) apply_faults(nk);  // faults with step_q == k
-    stage_base += nk;
-    bar_sync(BAR_RING_FREE, NTHREADS);  // every stage consumed: the ring is free for the C tile
-
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const int row = wm * 64 + tile_row<AKM>(a, g);
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = wn * 32 + tile_row<BKM>(b, 2 * t + e);
-          ctile[col * LDC_S + row] = acc[a][b][e];
+      s = gs - ld_sv(ws, W_BASE);
+      // At the end of a segment: an interval ends at stage s (its check comes before the faults
+      // due at stage s, which belong to the next interval); the last interval is checked at the
+      // virtual stage nk + 1, after the faults with step_q == k.  One call site each, so the
+      // register allocation of the DMMA loop is not disturbed.
+      // A correction located by the check is applied like a fault: -d_col at the located cell
+      // (one select block for both, so the register allocation of the DMMA loop is undisturbed).
+      int pend_si = -1, pend_sj = 0;
+      double pend_d = 0.0;
+      if (FT && s == ld_sv(ws, W_NEXT_CHECK)) {
+        const int kcs = max(1, (int)(P.Kc / BK));
+        const int tcur = s > nk ? P.T - 1 : s / kcs - 1;
+        const CheckOut co = check_unit<AKM, BKM>(P, tl, acc, tcur, min64((int64_t)s * BK, P.k), mw, wm, wn, lane);
+        pend_si = co.si;
+        pend_sj = co.sj;
+        pend_d = -co.dcol;
+        __syncwarp();
+        if (lane == 0) {
+          if (co.multi) {  // recompute: the rest of this attempt is neither injected nor verified
+            st_sv(ws, W_FAILED, tcur);
+            st_sv(ws, W_NEXT_CHECK, 0x7fffffff);
+            st_sv(ws, W_FNEXT, x.f_hi);
+            st_sv(ws, W_NEXT_STAGE, 0x7fffffff);
+          } else {
+            st_sv(ws, W_NEXT_CHECK, tcur + 1 < P.T - 1 ? (tcur + 2) * kcs : (tcur + 1 == P.T - 1 ? nk + 1 : 0x7fffffff));
+          }
         }
+        __syncwarp();
+      }
+      // Then the faults due before stage s's updates (s == nk: after the last update).
+      for (;;) {
+        int si = -1, sj = 0;
+        double dv = 0.0;
+        if (pend_si >= 0) {
+          si = pend_si;
+          sj = pend_sj;
+          dv = pend_d;
+          pend_si = -1;
+        } else if (s == ld_sv(ws, W_NEXT_STAGE)) {
+          const int fnext = ld_sv(ws, W_FNEXT);
+          const FaultDev f = P.faults[fnext];
+          // a fault belongs to interval min(stage / KcS, T - 1); a retry skips the decided ones
+          if (min(f.stage / max(1, (int)(P.Kc / BK)), P.T - 1) > tl.retry) {
+            const TileGeom gf = load_geom(tl.geo);
+            // staged row / column; -1 = the unit's checksum row / column (checksum-lane faults)
+            si = f.li < 0 ? gf.cra : f.li + gf.oa;
+            sj = f.lj < 0 ? gf.crb : f.lj + gf.ob;
+            dv = f.delta;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            st_sv(ws, W_FNEXT, fnext + 1);
+            st_sv(ws, W_NEXT_STAGE, fnext + 1 < x.f_hi ? P.faults[fnext + 1].stage : 0x7fffffff);
+          }
+          __syncwarp();
+        } else {
+          break;
+        }
+        // Register index of the owning accumulator, -1 for every other thread.  Select-based
+        // (no dynamic register indexing) so the accumulators stay in registers.
+        const int fidx = si >= 0 ? acc_owner_index<AKM, BKM>(si, sj, wm, wn, lane) : -1;
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const double v = acc[a][b][e];
+              acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v + dv : v;
+            }
+      }
+      if (s == nk && ld_sv(ws, W_NEXT_CHECK) == nk + 1) {  // go round once more for the last interval's check
+        ++s;
+        continue;
+      }
+      if (s >= nk) break;
     }
-    bar_sync(BAR_CTILE, 256);
-#ifdef FTBLAS_DEV_TIMELINE
-    if (!verify && attempt == 0 && vt == 0 && FT_DEV_PROF(P)) {
-      unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 4) * 2;
-      dp[0] = (unsigned long long)(tl_b - tl_a);
-      dp[1] = (unsigned long long)(clock64() - tl_b);
-      dp[2] = 0ull;
-    }
-#endif
+    __syncwarp();
+    if (lane == 0) st_sv(ws, W_BASE, ld_sv(ws, W_BASE) + nk);  // the next attempt's first stage
+    __syncwarp();
+    bar_sync(BAR_RING_FREE, NTHREADS);  // every stage consumed: the ring is free for the C tile
     if (!verify) break;
-
-    // ---- verification, out of line so that its register needs do not shape
-    // the allocation of the DMMA k-loop above (the accumulators are dead here: staged in smem).
-#ifdef FTBLAS_DEV_TIMELINE
-    const long long tl_c = clock64();
-#endif
-    const bool multi = verify_tile<AKM, BKM>(P, tl, ctile, vt, mw);
-#ifdef FTBLAS_DEV_TIMELINE
-    if (attempt == 0 && vt == 0 && FT_DEV_PROF(P)) {
-      unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 4) * 2;
-      dp[0] = (unsigned long long)(tl_b - tl_a);
-      dp[1] = (unsigned long long)(tl_c - tl_b);
-      dp[2] = (unsigned long long)(clock64() - tl_c);
+    const int failed = ld_sv(ws, W_FAILED);  // the same in every MMA warp (a CTA-wide decision)
+    if (vt == 0) {
+      tl.retry = failed;
+      if (failed >= 0) tl.nfix = 0;  // the recompute re-forms every element
+      tl.cum_am = tl.amax_hi;  // the next attempt's maxima: from scratch (PREPASS preset)
+      tl.cum_bm = tl.bmax_hi;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tl.int_am[q] = tl.int_bm[q] = 0u;
     }
-#endif
-    if (!multi) break;
-    // Out of the one-error model: recompute the whole tile once (no re-verification).
+    bar_sync(BAR_DECIDE, NTHREADS);  // encoders learn whether (and from where) to run again
+    if (failed < 0) break;  // else out of the one-error model: recompute the unit (R6)
   }
 
-  // ---- store: C = alpha*acc + beta*C0 (two roundings each, no contraction).
+  // ---- store: C = alpha*acc + beta*C0 (two roundings each, no contraction), staged through
+  // shared memory for coalesced column stores.
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int row = wm * 64 + tile_row<AKM>(a, g);
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + tile_row<BKM>(b, 2 * t + e);
+        ctile[col * LDC_S + row] = acc[a][b][e];
+      }
+  }
+  bar_sync(BAR_CTILE, 256);
   const TileGeom ge = load_geom(tl.geo);
+  if (FT) {
+    // Recompute mode (R4): each corrected element becomes a fresh dot product over all k.
+    const int nfix = tl.nfix;
+    for (int q = 0; q < nfix; ++q) {
+      const int si = tl.fix[q] & 255, sj = tl.fix[q] >> 8;
+      const int64_t gi = ge.i0 + si - ge.oa, gj = ge.j0 + sj - ge.ob;
+      double part = 0.0;
+      for (int64_t p = vt; p < P.k; p += 256) {
+        const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
+        const double bv = BKM ? P.B[p + gj * P.ldb] : P.B[gj + p * P.ldb];
+        part = fma(av, bv, part);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) tl.red[mw] = part;
+      bar_sync(BAR_RED, 256);
+      if (vt == 0) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < N_MMA_WARPS; ++w) v += tl.red[w];
+        ctile[sj * LDC_S + si] = v;
+      }
+      bar_sync(BAR_CTILE, 256);
+    }
+  }
   const int i = vt & 127;
   const double alpha = P.alpha, beta = P.beta;
   if (i < ge.bm_eff) {
-    double *crow = P.C + (int64_t)(ge.t - P.t_base) * P.wstride + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
+    double *crow = P.C + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
 #pragma unroll 4
     for (int j = vt >> 7; j < ge.bn_eff; j += 2) {
       const double v = __dmul_rn(alpha, ctile[(j + ge.ob) * LDC_S + i + ge.oa]);
@@ -1192,7 +1367,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
 template <bool AKM, bool BKM, bool FT>
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_abft_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const Params P) {
+                      const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Ctx x;
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (an integer round trip
@@ -1212,9 +1387,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // skip the DMMA stream) goes last, so the final waves are made of short tiles.
   const int tstr_m = (FT || (FT_DEV_MODE(P) & 32)) ? TM : BM, tstr_n = (FT || (FT_DEV_MODE(P) & 32)) ? TN : BN;
   const bool prow = P.tiles_m > 1 && (P.m % tstr_m) != 0, pcol = P.tiles_n > 1 && (P.n % tstr_n) != 0;
-  auto map_tile = [&](int Lg, int &ti_, int &tj_, int &t_) {
-    int L = Lg % P.ntiles;
-    t_ = P.t_base + Lg / P.ntiles;
+  auto map_tile = [&](int Lg, int &ti_, int &tj_) {
+    int L = Lg;
     int r0 = 0, c0 = 0;
     if (FT && P.Ash && P.Bsh) {
       if (L < P.tiles_n) { ti_ = 0; tj_ = L; return; }
@@ -1242,20 +1416,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   };
   const int Lg = (int)blockIdx.x;
   const bool ghost = P.cluster2 && Lg >= P.total;  // pads an odd grid to whole clusters
-  int ti, tj, tt;
-  map_tile(ghost ? Lg - 1 : Lg, ti, tj, tt);
+  int ti, tj;
+  map_tile(ghost ? Lg - 1 : Lg, ti, tj);
   // Cluster pair (2c, 2c+1): share the B_J encode when both are real tiles of the same tile
   // column and interval (a band with an odd row count pairs across columns: no sharing).
   bool share = false;
   if (FT && P.cluster2 && !P.Ac && !ghost && (Lg ^ 1) < P.total) {
-    int pti, ptj, ptt;
-    map_tile(Lg ^ 1, pti, ptj, ptt);
-    share = ptj == tj && ptt == tt;
+    int pti, ptj;
+    map_tile(Lg ^ 1, pti, ptj);
+    share = ptj == tj;
   }
-  x.t = tt;  // verification interval
-  x.tile = ti + tj * P.tiles_m + x.t * P.ntiles;  // fault bucket key: (tile, interval)
-  x.k0 = (int64_t)x.t * P.Kc;
-  x.k1 = min64(x.k0 + P.Kc, P.k);
+  x.tile = ti + tj * P.tiles_m;  // fault bucket key
+  x.k0 = 0;
+  x.k1 = P.k;
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.
   const bool g127 = FT || (FT_DEV_MODE(P) & 32);  // dev mode 32: unprotected kernel on the 127 grid
@@ -1277,7 +1450,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   x.nk = (int)((x.k1 - x.k0 + BK - 1) / BK);
 
   if (x.tid == 0) {
-    tl.geo = TileGeom{x.ti, x.tj, x.i0, x.j0, x.bm_eff, x.bn_eff, x.oa, x.ob, x.cra, x.crb, x.t, x.k0, x.k1};
+    tl.geo = TileGeom{x.ti, x.tj, x.i0, x.j0, x.bm_eff, x.bn_eff, x.oa, x.ob, x.cra, x.crb, x.k0, x.k1};
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
 #pragma unroll
@@ -1288,9 +1461,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tl.amax_hi = P.Ac ? P.amax_pre[ti] : 0u;
     tl.bmax_hi = P.Ac ? P.bmax_pre[tj] : 0u;
-    tl.first_row = 0x7fffffff;
-    tl.first_col = 0x7fffffff;
-    tl.retry = 0;
+    tl.first_row[0] = tl.first_row[1] = 0x7fffffff;
+    tl.first_col[0] = tl.first_col[1] = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tl.int_am[q] = tl.int_bm[q] = 0u;
+    tl.cum_am = tl.amax_hi;
+    tl.cum_bm = tl.bmax_hi;
+    tl.nfix = 0;
+    tl.retry = -1;
     tl.share = share ? 1 : 0;
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -1323,23 +1501,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   // A sharing pair stays resident until the partner has made its last remote access.
   if (share) cluster_sync_all();
-}
-
-// Intervals (NEXT-1): C = alpha * sum_{t < G} W_t + (first ? beta * C0 : C), the increments
-// summed in interval order (deterministic), two roundings for the alpha/beta combination.
-__global__ void interval_reduce_kernel(int64_t m, int64_t n, int G, const double *__restrict__ W, int64_t ldw,
-                                       int64_t wstride, double alpha, double beta, double *__restrict__ C,
-                                       int64_t ldc, bool first) {
-  const int64_t total = m * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e % m, j = e / m;
-    double acc = W[i + j * ldw];
-    for (int t = 1; t < G; ++t) acc = __dadd_rn(acc, W[t * wstride + i + j * ldw]);
-    double *c = C + i + j * ldc;
-    const double v = __dmul_rn(alpha, acc);
-    if (first) *c = beta != 0.0 ? __dadd_rn(v, __dmul_rn(beta, *c)) : v;
-    else *c = __dadd_rn(*c, v);
-  }
 }
 
 // C = beta*C (beta == 0: C = 0 without reading C).

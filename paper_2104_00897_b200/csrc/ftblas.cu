@@ -420,8 +420,6 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.Kc = Kc;
   p.T = (int)T;
   p.ntiles = p.tiles_m * p.tiles_n;
-  p.t_base = 0;
-  p.wstride = 0;
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
   p.correct_mode = tl_correct;
   p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL) ? 1 : 0;  // request; launch_one decides
@@ -439,11 +437,10 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // (tile-local row -1 = the checksum row); 2: the row checksum of row i (column -1).
   auto bucket = [&](const ftblas_fault_t &f, int lane) {
     const int64_t ti = f.i / tm, tj = f.j / tn;
-    // step quantised to BK (R8); interval t = step_q / Kc (step_q == k: after the last update
-    // of the last interval), stage local to the interval.
+    // step quantised to BK (R8), applied before stage step_q / BK; it belongs to interval
+    // min(step_q / Kc, T - 1) (step_q == k: after the last update of the last interval).
     const int64_t step_q = (f.step / ftk::BK) * ftk::BK;
-    const int64_t t = std::min<int64_t>(step_q / Kc, T - 1);
-    fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m + t * p.ntiles), (int32_t)((step_q - t * Kc) / ftk::BK),
+    fd.push_back(ftk::FaultDev{(int32_t)(ti + tj * p.tiles_m), (int32_t)(step_q / ftk::BK),
                                lane == 1 ? -1 : (int32_t)(f.i - ti * tm), lane == 2 ? -1 : (int32_t)(f.j - tj * tn),
                                f.delta});
   };
@@ -466,7 +463,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // slice maxima and the published sums, filled with all-ones bytes (= not yet published).
   // Launches of a single wave skip it (every tile starts together, so a consumer would almost
   // never find a stage published) unless dev modes 256 / 512 force the copy paths.
-  const bool one_wave = (int64_t)p.ntiles * T <= (int64_t)num_sms() && !p.wait_pub;
+  const bool one_wave = (int64_t)p.ntiles <= (int64_t)num_sms() && !p.wait_pub;
   const bool fused_shared = tl_encode == FTBLAS_ENCODE_FUSED || tl_encode == FTBLAS_ENCODE_FUSED_WAIT;
   const bool ashare = ft && fused_shared && p.tiles_n > 1 && !one_wave;
   const bool bshare = ft && fused_shared && p.tiles_m > 1 && !one_wave;
@@ -551,34 +548,9 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   CUtensorMap tmA, tmB;
   if (int e = make_tmap(&tmA, p.A, p.lda, akm, m, k)) return e;
   if (int e = make_tmap(&tmB, p.B, p.ldb, bkm, n, k)) return e;
-  int lrc = 0;
-  if (T == 1) {
-    const dim3 grid((unsigned)p.ntiles);  // 1-D: grouped raster in the kernel
-    lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
-  } else {
-    // Every interval's verified increment goes to a workspace slice (all intervals of a group
-    // run in one launch, so the k-split also fills the machine on skinny shapes); a
-    // deterministic reduction then forms C = alpha * sum_t inc_t + beta * C0.
-    size_t free_b = 0, total_b = 0;
-    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-    const size_t slice = sizeof(double) * (size_t)m * (size_t)n;
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)(free_b / 2 / slice)));
-    double *W = nullptr;
-    CUDA_TRY(cl.alloc(&W, slice * (size_t)G));
-    ftk::Params pw = p;
-    pw.C = W; pw.ldc = m; pw.alpha = 1.0; pw.beta = 0.0; pw.wstride = m * n;
-    for (int64_t g0 = 0; g0 < T && lrc == 0; g0 += G) {
-      const int64_t gn = std::min<int64_t>(G, T - g0);
-      pw.t_base = (int)g0;
-      const dim3 grid((unsigned)(p.ntiles * gn));
-      lrc = dispatch<true>(akm, bkm, tmA, tmB, pw, grid, st);
-      if (lrc) break;
-      const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, 148 * 16);
-      ftk::interval_reduce_kernel<<<blocks, 256, 0, st>>>(m, n, (int)gn, W, m, m * n, alpha, beta, C, ldc, g0 == 0);
-      ++tl_launches;
-      if (cudaGetLastError() != cudaSuccess) lrc = 1;
-    }
-  }
+  // One launch: every CTA verifies its tile online after every Kc updates (T checks).
+  const dim3 grid((unsigned)p.ntiles);  // 1-D: grouped raster in the kernel
+  const int lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
   if (lrc) return lrc;
 
   if (err && !sink)

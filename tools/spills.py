@@ -17,4 +17,4 @@ for l in txt.splitlines():
     if cur and re.search(r'\b(STL|LDL)', l):
         per.setdefault(cur, Counter())[curline] += 1
 for k, c in per.items():
-    print(k[-40:], sum(c.values()), sorted(c.items(), key=lambda x: -x[1])[:10])
+    print(k[17:60], sum(c.values()), sorted(c.items(), key=lambda x: -x[1])[:10])
