@@ -72,6 +72,8 @@ def parse():
     p.add_argument("--interval", type=int, default=0,
                    help="verification interval Kc (multiple of 16; 0 = k): ftblas_set_interval")
     p.add_argument("--cpu-sample-units", type=int, default=0)
+    p.add_argument("--no-sweep", action="store_true",
+                   help="skip the verification-interval sweep (fused vs unfused at Kc, overhead model)")
     return p.parse_args()
 
 
@@ -535,6 +537,60 @@ def main():
             del Ct
         ms_cublas = max_over_ranks([min(cb)])[0]
 
+    # 3b. verification every Kc updates (NEXT-1 fused online check vs the NEXT-2 unfused scheme)
+    #     and the paper's overhead model of unfused ABFT:
+    #     T_ovhd / T_gemm = (6 + 2K/Kc) P_mm / (n P_mv), with P_mm the unprotected DGEMM rate
+    #     and P_mv the DGEMV rate measured here on the same operands.
+    sweep = None
+    if not args.no_sweep and world == 1 and args.interval == 0:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        xv = torch.ones(k, dtype=torch.float64, device=dev)
+        yv = torch.zeros(mloc, dtype=torch.float64, device=dev)
+
+        def gemv():  # y = op(A) x over the resident op(A) (the unprotected DGEMV, NEXT-4 twin)
+            if ta == "N":
+                F.ftblas_dgemv_noft("N", mloc, k, 1.0, A, mloc, xv, 1, 0.0, yv, 1)
+            else:
+                F.ftblas_dgemv_noft("T", k, mloc, 1.0, A, k, xv, 1, 0.0, yv, 1)
+        gemv()
+        torch.cuda.synchronize()
+        gemv_ms = []
+        for _ in range(3):
+            e0.record(stream)
+            gemv()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            gemv_ms.append(e0.elapsed_time(e1))
+        p_mv = 2.0 * mloc * k / (min(gemv_ms) * 1e-3) / 1e12
+        p_mm = flops_total / (t_pno * 1e-3) / 1e12
+        rows = []
+        for kc in [k, 8192, 2048, 512]:
+            if kc > k or kc % 16:
+                continue
+            F.ftblas_set_interval(0 if kc == k else kc)
+            try:
+                tt = {}
+                for kind in ("ft", "unfused"):
+                    ts_ = []
+                    for _ in range(max(1, ncmp // 2)):
+                        e0.record(stream)
+                        r_ = step(kind)
+                        e1.record(stream)
+                        torch.cuda.synchronize()
+                        ts_.append(e0.elapsed_time(e1))
+                    tt[kind] = (min(ts_), r_)
+            finally:
+                F.ftblas_set_interval(0)
+            T_ = -(-k // kc)
+            rows.append({"Kc": kc, "intervals": T_,
+                         "fused_overhead_pct": 100.0 * (tt["ft"][0] - t_pno) / t_pno,
+                         "unfused_overhead_pct": 100.0 * (tt["unfused"][0] - t_pno) / t_pno,
+                         "model_unfused_pct": 100.0 * (6 + 2 * T_) * p_mm / (n * p_mv),
+                         "fused_events": tt["ft"][1].n_events, "unfused_events": tt["unfused"][1].n_events,
+                         "fused_units": tt["ft"][1].units_checked, "unfused_units": tt["unfused"][1].units_checked})
+        sweep = {"p_mm_tflops": p_mm, "p_mv_tflops": p_mv, "p_mm_over_p_mv": p_mm / p_mv, "n": n,
+                 "model": "(6 + 2K/Kc) P_mm / (n P_mv) (PAPER.md:261-265)", "rows": rows}
+
     # 4. the dominant kernel alone (roofline): events bracketing only the protected launch
     kern = []
     for _ in range(max(2, min(args.steps, 3))):
@@ -618,7 +674,8 @@ def main():
                  "prepass_encode": pre, "unfused_baseline": unf,
                  "ms_per_step_all": {"protected": per_ft, "pairs_protected": pairs["ft"],
                                      "pairs_unprotected": pairs["noft"]},
-                 "cublas_dgemm_tflops": flops_total / (ms_cublas * 1e-3) / 1e12 if ms_cublas else None},
+                 "cublas_dgemm_tflops": flops_total / (ms_cublas * 1e-3) / 1e12 if ms_cublas else None,
+                 "interval_sweep": sweep},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": "dgemm_abft_kernel (FT)", "kernel_ms": kern_ms,

@@ -29,6 +29,7 @@
 // tile once (R6).  Store C = alpha*acc + beta*C0 (C0 not read when beta == 0).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -185,7 +186,41 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifdef FTBLAS_DEV
+// Development builds: every mbarrier wait has a watchdog that reports (once) a wait that has
+// not completed after ~2^27 polls -- locates a hang instead of timing out silently.
+__device__ __forceinline__ bool mbar_try_u32(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Host-mapped report slot of the watchdog (set through FTBLAS_DEV_WATCH to a pinned host
+// address; a hung kernel never flushes printf, so the host polls this buffer instead).
+__device__ unsigned long long *g_dev_watch = nullptr;
+__device__ __noinline__ void mbar_watchdog(uint32_t bar, uint32_t parity, int where) {
+  long long n = 0;
+  while (!mbar_try_u32(bar, parity))
+    if (++n == (1ll << 24) && g_dev_watch) {
+      volatile unsigned long long *w = g_dev_watch;
+      const unsigned long long q = atomicAdd(g_dev_watch, 1ull);
+      if (q < 255) {
+        w[1 + q] = ((unsigned long long)blockIdx.x << 40) | ((unsigned long long)threadIdx.x << 28) |
+                   ((unsigned long long)where << 12) | ((unsigned long long)(bar & 0x7FF) << 1) | parity;
+        __threadfence_system();
+      }
+    }
+}
+#define FT_WATCH(bar, parity, where) mbar_watchdog((bar), (parity), (where))
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef FTBLAS_DEV
+  FT_WATCH(static_cast<uint32_t>(__cvta_generic_to_shared(bar)), parity, __LINE__);
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -197,6 +232,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+#ifdef FTBLAS_DEV
+  FT_WATCH(bar, parity, __LINE__);
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -807,7 +846,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     // B_J e published by tile row 0 is copied per stage like e^T A_I.  Publication only
     // happens in launches without clusters, so a cluster pair (share) never copies.
     const bool b_sub = P.Bsh && x.ti != 0;
-    const bool share = verify && tl.share;
+    // Only the first attempt exchanges half encodes with the cluster partner: a recompute pass
+    // (this tile alone) encodes its B_J e itself, bitwise the same checksum.
+    const bool share = verify && tl.share && attempt == 0;
     // Encode jobs.  Stages 0..3 of the tile: the two operands of a stage go to two warps
     // (warps 0, 2 share stages 0 and 2, warps 1, 3 stages 1 and 3; warps 0, 1 take A of stages
     // 0 / 1 and B of 2 / 3, warps 2, 3 the opposite), so the first stage -- on the critical path

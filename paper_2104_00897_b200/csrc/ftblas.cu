@@ -348,15 +348,15 @@ int finish_report(ftblas_err_report_t *err, const unsigned long long *d_counters
 
 // Block sums over bs-long x-blocks (encode passes, reference sums): unfused.cuh.
 int launch_block_sum(const double *X, bool xc, int64_t ld, int64_t nx, int64_t np, double *S, int64_t lds,
-                     unsigned *hm, int bs, cudaStream_t st) {
+                     unsigned *hm, int bs, cudaStream_t st, const int *enable = nullptr) {
   const int64_t nb = (nx + bs - 1) / bs;
   if (nb == 0 || np == 0) return 0;
   if (xc) {
     const dim3 g((unsigned)nb, (unsigned)((np + 31) / 32));
-    ftu::block_sum_kernel<true><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm, bs);
+    ftu::block_sum_kernel<true><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm, bs, enable);
   } else {
     const dim3 g((unsigned)nb, (unsigned)((np + 255) / 256));
-    ftu::block_sum_kernel<false><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm, bs);
+    ftu::block_sum_kernel<false><<<g, 256, 0, st>>>(X, ld, nx, np, S, lds, hm, bs, enable);
   }
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());
@@ -424,6 +424,10 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.correct_mode = tl_correct;
   p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL) ? 1 : 0;  // request; launch_one decides
 #ifdef FTBLAS_DEV
+  if (const char *dw = std::getenv("FTBLAS_DEV_WATCH")) {  // hang watchdog slot (tools/hang_probe.py)
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(std::strtoull(dw, nullptr, 0));
+    CUDA_TRY(cudaMemcpyToSymbol(ftk::g_dev_watch, &w, sizeof w));
+  }
   // development build only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
   p.dev_mode = dev_mode;
@@ -566,18 +570,23 @@ int dgemm_impl(bool ft, char ta, char tb, int64_t m, int64_t n, int64_t k, doubl
   return dgemm_core(ft, faults, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, err, nullptr, csf);
 }
 
-// The unfused ABFT baseline (kernels in unfused.cuh): encode passes,
-// the unprotected GEMM, two checksum GEMMs, reference-sum passes over the product, verify.
+// The unfused ABFT baseline (kernels in unfused.cuh; PAPER.md:257-261
+// §V.A): encode passes, then for every interval of Kc updates: the unprotected GEMM on the
+// k-slice (accumulating into C), the two skinny GEMMs carrying the checksums, the reference
+// row sums C e, the row check, the column sums e^T C only on a mismatch, verify / locate /
+// correct the flagged units.
 int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A, int64_t lda,
                  const double *B, int64_t ldb, double beta, double *C, int64_t ldc, ftblas_err_report_t *err) {
   const std::vector<ftblas_fault_t> faults = take_armed();
   if (reject_armed_cs()) return 3;  // checksum-lane faults: ftblas_dgemm only
   const int rc = check_args(ta, tb, m, n, k, alpha, A, lda, B, ldb, C, ldc);
   if (rc) return rc;
+  const int64_t Kc = (tl_interval > 0 && tl_interval < k) ? tl_interval : std::max<int64_t>(k, 1);
+  const int64_t T = (k + Kc - 1) / Kc;
   if (err) {
     err->units_checked = err->detected = err->corrected = err->recomputed = err->n_events = 0;
     err->unit_rows = err->unit_cols = ftu::UB;
-    err->unit_k = (int32_t)std::min<int64_t>(k, INT32_MAX);
+    err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
     err->step_quantum = ftk::BK;
   }
   if (m == 0 || n == 0) return 0;
@@ -590,17 +599,18 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   const int64_t nbm = (m + ftu::UB - 1) / ftu::UB, nbn = (n + ftu::UB - 1) / ftu::UB;
   const int64_t ldm = (nbm + 1) & ~int64_t(1), ldn = (nbn + 1) & ~int64_t(1), ldr = (m + 1) & ~int64_t(1);
   const bool direct = alpha == 1.0 && beta == 0.0;  // verify C itself, else a scratch product T
-  const int64_t ev_cap = std::max<int64_t>(err ? err->events_capacity : 0, nbm * nbn);  // one per unit
-  // scratch: counters, events, maxima, Ac, Br, CSc, CSr, Rc, Rr (+ T)
+  const int64_t ev_cap = std::max<int64_t>(err ? err->events_capacity : 0, nbm * nbn * T);  // one per unit
+  // scratch: counters, events, maxima, Ac, Br, CSc, CSr, Rc, Rr, unit flags (+ T)
   const size_t cnt_b = sizeof(unsigned long long) * ftk::CNT_N, ev_b = sizeof(ftk::EventDev) * ev_cap;
   const size_t hm_b = sizeof(unsigned) * (ldm + ldn);
   const size_t ac_b = sizeof(double) * ldm * k, br_b = sizeof(double) * ldn * k;
   const size_t csc_b = sizeof(double) * ldm * n, csr_b = sizeof(double) * ldr * ldn;
   const size_t rc_b = sizeof(double) * ldm * n, rr_b = sizeof(double) * ldn * m;
+  const size_t fl_b = sizeof(int) * (nbm * nbn + 1);
   const size_t t_b = direct ? 0 : sizeof(double) * ldr * n;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t total = al(cnt_b) + al(ev_b) + al(hm_b) + al(ac_b) + al(br_b) + al(csc_b) + al(csr_b) + al(rc_b) +
-                       al(rr_b) + al(t_b);
+                       al(rr_b) + al(fl_b) + al(t_b);
   Cleanup cl(st);
   char *base = nullptr;
   CUDA_TRY(cl.alloc(&base, total));
@@ -615,7 +625,8 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   auto *CSr = reinterpret_cast<double *>(take(csr_b));
   auto *Rc = reinterpret_cast<double *>(take(rc_b));
   auto *Rr = reinterpret_cast<double *>(take(rr_b));
-  double *T = direct ? C : reinterpret_cast<double *>(take(t_b));
+  auto *flags = reinterpret_cast<int *>(take(fl_b));  // [unit flags | any]
+  double *Tm = direct ? C : reinterpret_cast<double *>(take(t_b));
   const int64_t ldt = direct ? ldc : ldr;
   CUDA_TRY(cudaMemsetAsync(counters, 0, cnt_b, st));
   CUDA_TRY(cudaMemsetAsync(hmax, 0, hm_b, st));
@@ -624,37 +635,62 @@ int unfused_impl(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha
   if (ldn != nbn) CUDA_TRY(cudaMemsetAsync(Br, 0, br_b, st));
 
   auto block_sum = [&](const double *X, bool xc, int64_t ld, int64_t nx, int64_t np, double *S, int64_t lds,
-                       unsigned *hm) -> int { return launch_block_sum(X, xc, ld, nx, np, S, lds, hm, ftu::UB, st); };
+                       unsigned *hm, const int *enable = nullptr) -> int {
+    return launch_block_sum(X, xc, ld, nx, np, S, lds, hm, ftu::UB, st, enable);
+  };
   // 1. encode: e^T A_I for every row block I (x = i), B_J e for every column block J (x = j).
   if (int e = block_sum(A, is_n(ta), lda, m, k, Ac, ldm, hmax)) return e;
   if (int e = block_sum(B, is_t(tb), ldb, n, k, Br, ldn, hmax + ldm)) return e;
-  // 2. the product, unprotected kernel (armed faults land here).
-  if (int e = dgemm_core(false, faults, ta, tb, m, n, k, 1.0, A, lda, B, ldb, 0.0, T, ldt, nullptr)) return e;
-  // 3. carried checksums: (e^T A_I) B (nbm x n) and A (B_J e) (m x nbn), two skinny GEMMs.
-  if (int e = dgemm_core(false, {}, 'N', tb, ldm, n, k, 1.0, Ac, ldm, B, ldb, 0.0, CSc, ldm, nullptr)) return e;
-  if (int e = dgemm_core(false, {}, ta, 'T', m, ldn, k, 1.0, A, lda, Br, ldn, 0.0, CSr, ldr, nullptr)) return e;
-  // 4. reference checksums of the product: e^T T_I (x = i) and T_J e (x = j).
-  if (int e = block_sum(T, true, ldt, m, n, Rc, ldm, nullptr)) return e;
-  if (int e = block_sum(T, false, ldt, n, m, Rr, ldn, nullptr)) return e;
-  // 5. verify / locate / correct, one CTA per 128 x 128 unit.
-  ftu::VerifyParams vp{};
-  vp.m = m; vp.n = n; vp.k = k; vp.ta = is_n(ta) ? 'N' : 'T'; vp.tb = is_n(tb) ? 'N' : 'T';
-  vp.A = A; vp.lda = lda; vp.B = B; vp.ldb = ldb; vp.T = T; vp.ldt = ldt;
-  vp.Rc = Rc; vp.CSc = CSc; vp.ldm = ldm; vp.Rr = Rr; vp.ldn = ldn; vp.CSr = CSr; vp.ldr = ldr;
-  vp.amax_hi = hmax; vp.bmax_hi = hmax + ldm; vp.nbm = (int)nbm; vp.nbn = (int)nbn;
-  vp.correct_mode = tl_correct; vp.counters = counters; vp.events = events; vp.ev_cap = ev_cap;
-  ftu::verify_kernel<<<(unsigned)(nbm * nbn), 256, 0, st>>>(vp);
-  ++tl_launches;
-  CUDA_TRY(cudaGetLastError());
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t k0 = t * Kc, k1 = std::min(k0 + Kc, k), kl = k1 - k0;
+    const double bt = t ? 1.0 : 0.0;  // accumulate the intervals into C (and the checksums)
+    const double *At = is_n(ta) ? A + k0 * lda : A + k0;
+    const double *Bt = is_n(tb) ? B + k0 : B + k0 * ldb;
+    // 2. the product on the k-slice, unprotected kernel (this interval's faults land here, their
+    //    steps local to the slice).
+    std::vector<ftblas_fault_t> ft_t;
+    for (const auto &f : faults) {
+      const int64_t sq = (f.step / ftk::BK) * ftk::BK;
+      if (std::min<int64_t>(sq / Kc, T - 1) == t) ft_t.push_back(ftblas_fault_t{f.i, f.j, f.step - k0, f.delta});
+    }
+    if (int e = dgemm_core(false, ft_t, ta, tb, m, n, kl, 1.0, At, lda, Bt, ldb, bt, Tm, ldt, nullptr)) return e;
+    // 3. carried checksums: (e^T A_I) B (nbm x n) and A (B_J e) (m x nbn), two skinny GEMMs.
+    if (int e = dgemm_core(false, {}, 'N', tb, ldm, n, kl, 1.0, Ac + k0 * ldm, ldm, Bt, ldb, bt, CSc, ldm, nullptr)) return e;
+    if (int e = dgemm_core(false, {}, ta, 'T', m, ldn, kl, 1.0, At, lda, Br + k0 * ldn, ldn, bt, CSr, ldr, nullptr)) return e;
+    // 4. reference row checksums C_J e first; the row check marks mismatching units.
+    CUDA_TRY(cudaMemsetAsync(flags, 0, fl_b, st));
+    if (int e = block_sum(Tm, false, ldt, n, m, Rr, ldn, nullptr)) return e;
+    {
+      const int blocks = (int)std::min<int64_t>((m * nbn + 255) / 256, 148 * 8);
+      ftu::row_check_kernel<<<blocks, 256, 0, st>>>(m, n, k1, Rr, ldn, CSr, ldr, hmax, hmax + ldm, (int)nbm, (int)nbn,
+                                                    flags, flags + nbm * nbn);
+      ++tl_launches;
+      CUDA_TRY(cudaGetLastError());
+    }
+    // 5. e^T C_I only on a mismatch (the pass returns at once otherwise), then verify / locate /
+    //    correct the marked units.
+    if (int e = block_sum(Tm, true, ldt, m, n, Rc, ldm, nullptr, flags + nbm * nbn)) return e;
+    ftu::VerifyParams vp{};
+    vp.m = m; vp.n = n; vp.k = k1; vp.interval = (int)t; vp.unit_flag = flags;
+    vp.ta = is_n(ta) ? 'N' : 'T'; vp.tb = is_n(tb) ? 'N' : 'T';
+    vp.A = A; vp.lda = lda; vp.B = B; vp.ldb = ldb; vp.T = Tm; vp.ldt = ldt;
+    vp.Rc = Rc; vp.CSc = CSc; vp.ldm = ldm; vp.Rr = Rr; vp.ldn = ldn; vp.CSr = CSr; vp.ldr = ldr;
+    vp.amax_hi = hmax; vp.bmax_hi = hmax + ldm; vp.nbm = (int)nbm; vp.nbn = (int)nbn;
+    vp.Ac = t + 1 < T ? Ac : nullptr; vp.Br = Br; vp.CSc_w = CSc; vp.CSr_w = CSr;
+    vp.correct_mode = tl_correct; vp.counters = counters; vp.events = events; vp.ev_cap = ev_cap;
+    ftu::verify_kernel<<<(unsigned)(nbm * nbn), 256, 0, st>>>(vp);
+    ++tl_launches;
+    CUDA_TRY(cudaGetLastError());
+  }
   // 6. C = alpha*T + beta*C0 when the product was verified in scratch.
   if (!direct) {
     const int blocks = (int)std::min<int64_t>((m * n + 255) / 256, 148 * 16);
-    ftu::axpby_kernel<<<blocks, 256, 0, st>>>(m, n, alpha, T, ldt, beta, C, ldc);
+    ftu::axpby_kernel<<<blocks, 256, 0, st>>>(m, n, alpha, Tm, ldt, beta, C, ldc);
     ++tl_launches;
     CUDA_TRY(cudaGetLastError());
   }
   if (err)
-    if (int e = finish_report(err, counters, events, ev_cap, nbm * nbn, st)) return e;
+    if (int e = finish_report(err, counters, events, ev_cap, nbm * nbn * T, st)) return e;
   return 0;
 }
 

@@ -10,9 +10,16 @@
 // with the same verification unit semantics as the fused path but on 128 x 128 units (no
 // C^f tile: the checksums live outside C).
 //
+// With a verification interval Kc < k ("for each rank-Kc update") the product
+// and the carried checksums are formed Kc updates at a time and C is verified after each:
+// the reference row sums C e first (one memory pass), the column sums e^T C only when a row
+// mismatched (the paper's "C^r first, C^c only on mismatch"), then locate / correct.
+//
 //   block_sum_kernel   S[xb + p*lds] = sum_{x in block xb} X(x, p)   (+ running max |hi|)
 //                      used for e^T A_I (x = i), B_J e (x = j), e^T C_IJ and C_IJ e
-//   verify_kernel      one CTA per unit: residuals, threshold, classify, correct in place
+//   row_check_kernel   one thread per (row i, column block J): C_J e against A (B_J e); marks
+//                      the unit and raises the "mismatch" flag that enables the e^T C pass
+//   verify_kernel      one CTA per flagged unit: residuals, threshold, classify, correct in place
 //   axpby_kernel       C = alpha*T + beta*C0 when the verified product lives in scratch
 #pragma once
 #include <cstdint>
@@ -29,7 +36,9 @@ constexpr int UB = 128;  // unit rows / columns of the unfused path
 template <bool XC>
 __global__ void __launch_bounds__(256) block_sum_kernel(const double *__restrict__ X, int64_t ld, int64_t nx,
                                                         int64_t np, double *__restrict__ S, int64_t lds,
-                                                        unsigned int *__restrict__ hmax, int bs) {
+                                                        unsigned int *__restrict__ hmax, int bs,
+                                                        const int *__restrict__ enable) {
+  if (enable && *enable == 0) return;  // a pass that runs only on mismatch (e^T C)
   const int64_t xb = blockIdx.x, x0 = xb * bs;  // block size bs <= 128
   const int xn = (int)min((int64_t)bs, nx - x0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -89,7 +98,9 @@ __global__ void __launch_bounds__(256) block_sum_kernel(const double *__restrict
 }
 
 struct VerifyParams {
-  int64_t m, n, k;
+  int64_t m, n, k;   // k: updates accumulated so far (the end of the interval being verified)
+  int interval;      // verification interval index t
+  const int *unit_flag;  // row-check marks (null: verify every unit)
   char ta, tb;
   const double *A;
   int64_t lda;
@@ -104,6 +115,10 @@ struct VerifyParams {
   const double *CSr;       // A (B_J e) as CSr[i + J*ldr]
   int64_t ldr;
   const unsigned int *amax_hi, *bmax_hi;
+  // the encoded block sums (e^T A_I as Ac[I + p*ldm], B_J e as Br[J + p*ldn]) and the carried
+  // checksums to re-form for a recomputed unit (null when there is no later interval)
+  const double *Ac, *Br;
+  double *CSc_w, *CSr_w;
   int nbm, nbn;
   int correct_mode;
   unsigned long long *counters;  // [detected, corrected, recomputed, events] (ftk::CNT_*)
@@ -132,6 +147,7 @@ __global__ void __launch_bounds__(256) verify_kernel(const VerifyParams P) {
   __shared__ double red[8];
   __shared__ int first_row, first_col;
   const int unit = blockIdx.x, I = unit % P.nbm, J = unit / P.nbm;
+  if (P.unit_flag && P.unit_flag[unit] == 0) return;  // its rows matched: clean
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t i0 = (int64_t)I * UB, j0 = (int64_t)J * UB;
   const int bm = (int)min((int64_t)UB, P.m - i0), bn = (int)min((int64_t)UB, P.n - j0);
@@ -183,12 +199,26 @@ __global__ void __launch_bounds__(256) verify_kernel(const VerifyParams P) {
       }
     }
   } else {
-    // Out of the one-error model: recompute the unit once, no re-verification (R6).
+    // Out of the one-error model: recompute the unit once, no re-verification (R6); with
+    // later intervals to come its carried checksums are re-formed too (R6').
     for (int e = tid; e < bm * bn; e += 256) {
       const int64_t gi = i0 + e % bm, gj = j0 + e / bm;
       double v = 0.0;
       for (int64_t p = 0; p < P.k; ++p) v = fma(opA(P, gi, p), opB(P, p, gj), v);
       P.T[gi + gj * P.ldt] = v;
+    }
+    if (P.Ac) {
+      for (int c = tid; c < bn + bm; c += 256) {
+        double v = 0.0;
+        if (c < bn) {  // (e^T A_I) B_J, column j0 + c
+          for (int64_t p = 0; p < P.k; ++p) v = fma(P.Ac[I + p * P.ldm], opB(P, p, j0 + c), v);
+          P.CSc_w[I + (j0 + c) * P.ldm] = v;
+        } else {       // A_I (B_J e), row i0 + c - bn
+          const int64_t gi = i0 + c - bn;
+          for (int64_t p = 0; p < P.k; ++p) v = fma(opA(P, gi, p), P.Br[J + p * P.ldn], v);
+          P.CSr_w[gi + J * P.ldr] = v;
+        }
+      }
     }
   }
   if (tid == 0) {
@@ -197,8 +227,32 @@ __global__ void __launch_bounds__(256) verify_kernel(const VerifyParams P) {
     const unsigned long long slot = atomicAdd(&P.counters[3], 1ull);
     EventU *ev = reinterpret_cast<EventU *>(P.events);
     if ((long long)slot < P.ev_cap)
-      ev[slot] = multi ? EventU{(long long)i0, (long long)j0, 2, 0, nfr ? dres[128 + fr] : 0.0, nfc ? dres[fc] : 0.0}
-                       : EventU{(long long)(i0 + fr), (long long)(j0 + fc), 1, 0, dres[128 + fr], dres[fc]};
+      ev[slot] = multi ? EventU{(long long)i0, (long long)j0, 2, P.interval, nfr ? dres[128 + fr] : 0.0, nfc ? dres[fc] : 0.0}
+                       : EventU{(long long)(i0 + fr), (long long)(j0 + fc), 1, P.interval, dres[128 + fr], dres[fc]};
+  }
+}
+
+// The reference row checksums first: one thread per (row i, column block J)
+// compares (C_J e)_i with (A (B_J e))_i against the row threshold of unit (i / 128, J); a
+// mismatch marks the unit and enables the e^T C pass and the verify kernel.
+__global__ void row_check_kernel(int64_t m, int64_t n, int64_t kt, const double *__restrict__ Rr, int64_t ldn,
+                                 const double *__restrict__ CSr, int64_t ldr, const unsigned int *__restrict__ amax_hi,
+                                 const unsigned int *__restrict__ bmax_hi, int nbm, int nbn, int *__restrict__ unit_flag,
+                                 int *__restrict__ any) {
+  const int64_t total = m * nbn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m;
+    const int J = (int)(e / m), I = (int)(i / UB);
+    const int bn = (int)min((int64_t)UB, n - (int64_t)J * UB);
+    const double d = Rr[J + i * ldn] - CSr[i + J * ldr];
+    const double amx = __longlong_as_double((long long)(((unsigned long long)amax_hi[I] << 32) | 0xFFFFFFFFull));
+    const double bmx = __longlong_as_double((long long)(((unsigned long long)bmax_hi[J] << 32) | 0xFFFFFFFFull));
+    const double nu = (double)(kt + bn) * 0x1p-53;
+    const double tau = fmin(2.0 * (nu / (1.0 - nu)) * (double)kt * (double)bn * amx * bmx, 0x1.fffffffffffffp1023);
+    if (!(fabs(d) <= tau)) {
+      unit_flag[I + (int64_t)J * nbm] = 1;
+      *any = 1;
+    }
   }
 }
 

@@ -36,23 +36,25 @@ def stored(X, t):
 
 
 def run_unfused(A, B, C0, *, ta="N", tb="N", alpha=1.0, beta=0.0, faults=(), subtract=False,
-                check_values=True):
+                check_values=True, Kc=0):
     m, k = op(A, ta).shape
     n = op(B, tb).shape[1]
     lda, ldb = max(A.shape[0], 1), max(B.shape[0], 1)
     dA, dB, dC = to_dev(A), to_dev(B), to_dev(C0)
     F.ftblas_set_correction(F.CORRECT_SUBTRACT if subtract else F.CORRECT_RECOMPUTE)
+    F.ftblas_set_interval(Kc)
     try:
         if faults:
             F.ftblas_inject_arm(faults)
         rep = F.ftblas_dgemm_unfused(ta, tb, m, n, k, alpha, dA, lda, dB, ldb, beta, dC, max(m, 1))
     finally:
         F.ftblas_set_correction(F.CORRECT_RECOMPUTE)
+        F.ftblas_set_interval(0)
     assert (rep.unit_rows, rep.unit_cols) == (128, 128)
     Cg = from_dev(dC, m, n)
     Co, orep = oracle.dgemm_abft(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C0, max(m, 1),
                                  BM=128, BN=128, BK=rep.step_quantum, faults=list(faults),
-                                 subtract=subtract)
+                                 subtract=subtract, Kc=Kc or None)
     Co = Co.reshape((n, m)).T
     if check_values:
         tol = bound(None, A, B, C0, alpha, beta, ta, tb, k)
@@ -125,3 +127,22 @@ def test_unfused_nan_input_recomputed():
     assert rep.recomputed == orep.recomputed >= 1
     assert events_key(rep.events) == events_key(orep.events)
     assert np.isnan(Cg[10]).all() and not np.isnan(np.delete(Cg, 10, axis=0)).any()
+
+
+@pytest.mark.parametrize("trans", ["NN", "TT"])
+@pytest.mark.parametrize("Kc", [16, 48, 64])
+def test_unfused_intervals_match_oracle(trans, Kc):
+    """The unfused baseline verifying every Kc updates: per interval the slice
+    GEMM, the skinny checksum GEMMs, C e first and e^T C only on a mismatch; counters and the
+    sorted (interval, i, j, kind) events equal the oracle's with the same Kc, including a unit
+    recomputed in interval 0 that verifies clean (and then corrects a new fault) later (R6')."""
+    rng = np.random.default_rng(310 + Kc)
+    m, n, k = 260, 200, 150
+    A, B, C0 = rand(rng, m, k), rand(rng, k, n), rand(rng, m, n)
+    faults = [(3, 4, 0, 5.0), (3, 4, k, -7.0), (130, 70, Kc, 2.5), (131, 71, Kc + 1, 9.0),
+              (10, 150, 2 * Kc, -1e3), (250, 199, k - 1, 0.125), (140, 60, 140, 3.0)]
+    _, _, rep, orep = run_unfused(stored(A, trans[0]), stored(B, trans[1]), C0, ta=trans[0],
+                                  tb=trans[1], faults=faults, Kc=Kc, alpha=1.25, beta=-0.5)
+    assert rep.unit_k == Kc and rep.units_checked == orep.units_checked == 3 * 2 * -(-k // Kc)
+    assert_reports_match(rep, orep, stored(A, trans[0]), stored(B, trans[1]), trans[0], trans[1], k)
+    assert rep.recomputed >= 1 and rep.corrected >= 3
