@@ -73,6 +73,8 @@ def lib():
         L.oracle_dgemv.argtypes = [c, i64, i64, d, P, i64, P, i64, d, P, i64, P, i64, P]
         L.oracle_dtrsm.argtypes = [c, c, c, i64, i64, d, P, i64, P, i64, i64, P]
         L.oracle_dtrsm_right.argtypes = [c, c, c, i64, i64, d, P, i64, P, i64, i64, P]
+        L.oracle_dtrsm_bookkeeping.restype = ctypes.c_int
+        L.oracle_dtrsm_bookkeeping.argtypes = [c, c, c, i64, i64, i64, i64, P, i64, P, P, i64]
         _lib = L
     return _lib
 
@@ -244,14 +246,39 @@ def dgemv(trans, m, n, alpha, A, lda, x, incx, beta, y, incy, faults=()):
 
 def dtrsm(uplo, transa, diag, m, n, alpha, A, lda, B, ldb, faults=(), side="L"):
     """DTRSM oracle (NEXT-3): solve op(A) X = alpha B (side L, op(A) m x m) or X op(A) = alpha B
-    (side R, op(A) n x n); returns (X flat, (detected, corrected))."""
+    (side R, op(A) n x n); returns (X flat, Report) -- X the fault-free solution (the faults are
+    corrected by the protection), the Report the FT bookkeeping of the blocked solve
+    (dtrsm_bookkeeping: DMR detections of the diagonal blocks, ABFT units / events of the GEMM
+    updates)."""
     A = _flat(A)
     Bo = _flat(B).copy()
     cnt = np.zeros(4, dtype=np.int64)
     fn = lib().oracle_dtrsm if side in ("L", "l") else lib().oracle_dtrsm_right
     fn(uplo.encode(), transa.encode(), diag.encode(), m, n, alpha, _ptr(A), lda, _ptr(Bo), ldb,
        len(list(faults)), _ptr(cnt))
-    return Bo, (int(cnt[1]), int(cnt[2]))
+    return Bo, dtrsm_bookkeeping(side, uplo, transa, m, n, faults)
+
+
+def dtrsm_bookkeeping(side, uplo, transa, m, n, faults, leaf=128, tm=127):
+    """FT-DTRSM bookkeeping of the blocked solve (reading R21): which faults the DMR diagonal
+    solves settle and which land in the ABFT-protected GEMM updates.  Returns a Report
+    (units_checked, detected, corrected, recomputed, n_events, events) with events
+    (0, i, j, kind, 0.0, 0.0) sorted by (i, j)."""
+    faults = list(faults)
+    fa = (_Fault * max(len(faults), 1))()
+    for e, (i, j, s_, dlt) in enumerate(faults):
+        fa[e] = _Fault(int(i), int(j), int(s_), float(dlt), 0)
+    cap = max(1, 2 * len(faults))
+    ev = (_Event * cap)()
+    cnt = np.zeros(5, dtype=np.int64)
+    rc = lib().oracle_dtrsm_bookkeeping(side.encode(), uplo.encode(), transa.encode(), m, n, leaf, tm,
+                                        ctypes.cast(fa, ctypes.c_void_p), len(faults), _ptr(cnt),
+                                        ctypes.cast(ev, ctypes.c_void_p), cap)
+    if rc != 0:
+        raise ValueError("oracle_dtrsm_bookkeeping rejected arguments")
+    events = [(ev[e].interval, ev[e].i, ev[e].j, ev[e].kind, ev[e].residual_row, ev[e].residual_col)
+              for e in range(int(min(cnt[4], cap)))]
+    return Report(*[int(x) for x in cnt], events)
 
 
 def num_threads() -> int:

@@ -482,8 +482,8 @@ void oracle_dgemv(char trans, int64_t m, int64_t n, double alpha, const double *
  * x_i = (alpha b_i - sum_p op(A)_ip x_p) computed as an fma chain over p in substitution order,
  * then multiplied by the reciprocal 1/op(A)_ii (the paper's packed reciprocal diagonal; unit
  * diagonal: no multiply).  Faults are corrected by the protection (ABFT on the updates, DMR on
- * the diagonal solves), so X is the fault-free solution and every fault counts as detected and
- * corrected (reading R21: faults far apart, one per verification unit).
+ * the diagonal solves), so X is the fault-free solution; which protection reports what is
+ * oracle_dtrsm_bookkeeping's (reading R21).
  * ------------------------------------------------------------------------- */
 void oracle_dtrsm(char uplo, char transa, char diag, int64_t m, int64_t n, double alpha, const double *A,
                   int64_t lda, double *B, int64_t ldb, int64_t nfaults, int64_t *counters) {
@@ -506,14 +506,16 @@ void oracle_dtrsm(char uplo, char transa, char diag, int64_t m, int64_t n, doubl
       }
     }
   }
-  counters[0] = 0; counters[1] = nfaults; counters[2] = nfaults; counters[3] = 0;
+  (void)nfaults; /* the FT bookkeeping is oracle_dtrsm_bookkeeping's */
+  counters[0] = counters[1] = counters[2] = counters[3] = 0;
 }
 
 /* DTRSM side 'R' (B = alpha B op(A)^-1): X op(A) = alpha B, op(A) n x n, in place,
  * row by row: each row x of X solves x op(A) = alpha b by substitution over the columns of
  * op(A) -- forward (j ascending) when op(A) is upper, backward when lower: x_j = b_j * (1 /
  * op(A)_jj), then b_q -= op(A)_jq x_j for the columns q still to solve (fma, substitution
- * order).  Faults are corrected by the protection, as on the left (reading R21). */
+ * order).  Faults are corrected by the protection, as on the left (reading R21; bookkeeping:
+ * oracle_dtrsm_bookkeeping). */
 void oracle_dtrsm_right(char uplo, char transa, char diag, int64_t m, int64_t n, double alpha, const double *A,
                         int64_t lda, double *B, int64_t ldb, int64_t nfaults, int64_t *counters) {
   int lower = (uplo == 'L' || uplo == 'l'), tr = is_trans(transa), unit = (diag == 'U' || diag == 'u');
@@ -533,7 +535,120 @@ void oracle_dtrsm_right(char uplo, char transa, char diag, int64_t m, int64_t n,
       }
     }
   }
-  counters[0] = 0; counters[1] = nfaults; counters[2] = nfaults; counters[3] = 0;
+  (void)nfaults; /* the FT bookkeeping is oracle_dtrsm_bookkeeping's */
+  counters[0] = counters[1] = counters[2] = counters[3] = 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * FT-DTRSM bookkeeping (§III.C.3, 476; reading
+ * R21): which protection sees each injected fault, and what it reports.  The blocked solve
+ * is the recursion include/ftblas.h documents, written out with its two parameters: the
+ * diagonal-block size `leaf` and the GEMM unit size `tm` (blocks of len > leaf positions
+ * split off u = 2 tm j positions, j = floor((len + 2 tm) / (4 tm)) reduced until u < len, or
+ * u = tm - 1 when j = 0; the part solved first comes first in substitution order).
+ *   - A fault (i, j, step p) whose element e (side L: row i; side R: column j) and step p fall
+ *     in one diagonal block is seen by that block's DMR solve: one detection and correction per
+ *     (block, right-hand side) holding faults, no event (DMR).
+ *   - Otherwise it lands in the unique coupling GEMM update whose rows hold e and whose k
+ *     range holds p: an ABFT unit (tm x tm, in the update's own coordinates) with one distinct
+ *     faulty cell is corrected (event at the global (i, j)); with more cells it is recomputed
+ *     (event at the unit's global origin), as in oracle_dgemm_abft (R6).
+ *   - units_checked counts the units of every update.
+ * counters[5] = {units_checked, detected, corrected, recomputed, n_events}; events sorted by
+ * (interval = 0, i, j).  Faults: (i, j, step) triples, n_rhs = m for side R, n for side L. */
+typedef struct {
+  int right, fwd;
+  int64_t leaf, tm, nrhs;
+  const or_fault_t *f;
+  int64_t nf;
+  int64_t cnt[5];
+  or_event_t *ev;
+  int64_t ev_cap;
+} bk_ctx_t;
+
+static int64_t bk_elem(const bk_ctx_t *c, const or_fault_t *f) { return c->right ? f->j : f->i; }
+static int64_t bk_rhs(const bk_ctx_t *c, const or_fault_t *f) { return c->right ? f->i : f->j; }
+
+static void bk_event(bk_ctx_t *c, int64_t i, int64_t j, int kind) {
+  if (c->cnt[4] < c->ev_cap) {
+    or_event_t e = {i, j, kind, 0, 0.0, 0.0};
+    c->ev[c->cnt[4]] = e;
+  }
+  c->cnt[4] += 1;
+}
+
+static void bk_leaf(bk_ctx_t *c, int64_t r0, int64_t len) {
+  /* one detection per right-hand side with a fault inside this diagonal block */
+  for (int64_t rhs = 0; rhs < c->nrhs; ++rhs) {
+    int hit = 0;
+    for (int64_t e = 0; e < c->nf && !hit; ++e) {
+      const int64_t el = bk_elem(c, &c->f[e]);
+      hit = bk_rhs(c, &c->f[e]) == rhs && el >= r0 && el < r0 + len && c->f[e].step >= r0 && c->f[e].step < r0 + len;
+    }
+    if (hit) { c->cnt[1] += 1; c->cnt[2] += 1; }
+  }
+}
+
+static void bk_gemm(bk_ctx_t *c, int64_t R0, int64_t mr, int64_t K0, int64_t mk) {
+  /* update rows (side L) / columns (side R) [R0, R0+mr), k range [K0, K0+mk) */
+  const int64_t rows = c->right ? c->nrhs : mr, cols = c->right ? mr : c->nrhs;
+  const int64_t tmr = (rows + c->tm - 1) / c->tm, tnc = (cols + c->tm - 1) / c->tm;
+  c->cnt[0] += tmr * tnc;
+  for (int64_t u = 0; u < tmr * tnc; ++u) {
+    const int64_t ti = u % tmr, tj = u / tmr;
+    int64_t ncell = 0, ci = -1, cj = -1;
+    for (int64_t e = 0; e < c->nf; ++e) {
+      const or_fault_t *f = &c->f[e];
+      const int64_t el = bk_elem(c, f);
+      if (!(el >= R0 && el < R0 + mr && f->step >= K0 && f->step < K0 + mk)) continue;
+      const int64_t li = c->right ? f->i : el - R0, lj = c->right ? el - R0 : f->j;  /* update coordinates */
+      if (li / c->tm != ti || lj / c->tm != tj) continue;
+      if (ncell == 0) { ci = f->i; cj = f->j; ncell = 1; }
+      else if (f->i != ci || f->j != cj) ncell = 2;
+    }
+    if (ncell == 0) continue;
+    c->cnt[1] += 1;
+    if (ncell == 1) { c->cnt[2] += 1; bk_event(c, ci, cj, 1); }
+    else {
+      c->cnt[3] += 1;
+      bk_event(c, c->right ? ti * c->tm : R0 + ti * c->tm, c->right ? R0 + tj * c->tm : tj * c->tm, 2);
+    }
+  }
+}
+
+static void bk_rec(bk_ctx_t *c, int64_t r0, int64_t len) {
+  if (len <= c->leaf) { bk_leaf(c, r0, len); return; }
+  int64_t j = (len + 2 * c->tm) / (4 * c->tm);
+  while (j > 0 && 2 * c->tm * j >= len) --j;
+  const int64_t u = j > 0 ? 2 * c->tm * j : c->tm - 1;
+  const int64_t m1 = c->fwd ? len - u : u, m2 = len - m1;
+  if (c->fwd) {
+    bk_rec(c, r0, m1);
+    bk_gemm(c, r0 + m1, m2, r0, m1);
+    bk_rec(c, r0 + m1, m2);
+  } else {
+    bk_rec(c, r0 + m1, m2);
+    bk_gemm(c, r0, m1, r0 + m1, m2);
+    bk_rec(c, r0, m1);
+  }
+}
+
+int oracle_dtrsm_bookkeeping(char side, char uplo, char transa, int64_t m, int64_t n, int64_t leaf, int64_t tm,
+                             const or_fault_t *faults, int64_t nfaults, int64_t *counters, or_event_t *events,
+                             int64_t events_cap) {
+  const int right = (side == 'R' || side == 'r'), lower = (uplo == 'L' || uplo == 'l'), tr = is_trans(transa);
+  bk_ctx_t c;
+  memset(&c, 0, sizeof c);
+  c.right = right;
+  c.fwd = right ? (lower == tr) : (lower != tr); /* substitution order (ascending when fwd) */
+  c.leaf = leaf; c.tm = tm; c.nrhs = right ? m : n;
+  c.f = faults; c.nf = nfaults; c.ev = events; c.ev_cap = events_cap;
+  if (leaf <= 0 || tm <= 1) return -1;
+  if (m > 0 && n > 0) bk_rec(&c, 0, right ? n : m);
+  const int64_t ns = c.cnt[4] < events_cap ? c.cnt[4] : events_cap;
+  if (ns > 1) qsort(events, (size_t)ns, sizeof(or_event_t), cmp_event);
+  for (int q = 0; q < 5; ++q) counters[q] = c.cnt[q];
+  return 0;
 }
 
 int oracle_num_threads(void) {

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.helpers import from_dev, to_dev, trsm_leaf_ids
+from tests.helpers import events_key, from_dev, to_dev
 
 pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
@@ -70,12 +70,12 @@ def test_dtrsm_integer_exact_with_faults(uplo, tr):
     rep = F.ftblas_dtrsm("L", uplo, tr, "U", m, n, 1.0, to_dev(T), m, dB, m)
     assert np.array_equal(from_dev(dB, m, n), X)
     assert (rep.detected, rep.corrected, rep.recomputed) == (5, 5, 0)
-    # the cross-block faults landed in GEMM updates: ABFT events with global rows; the others
-    # were settled by the DMR diagonal-block solves (counted, no event)
-    leaf = trsm_leaf_ids(m)  # diagonal blocks of the solve, substitution order (include/ftblas.h)
-    cross = sorted((f[0], f[1]) for f, (i, j, p) in zip(faults, pairs) if leaf[i] != leaf[p])
-    assert len(cross) >= 2 and sorted((e[1], e[2]) for e in rep.events) == cross
-    assert all(e[3] == 1 for e in rep.events)
+    # the oracle's bookkeeping of the blocked solve (reading R21) decides which faults the GEMM
+    # updates' ABFT reports (events with global rows) and which the DMR diagonal solves settle
+    bk = oracle.dtrsm_bookkeeping("L", uplo, tr, m, n, faults)
+    assert (rep.units_checked, rep.detected, rep.corrected, rep.recomputed) == \
+        (bk.units_checked, bk.detected, bk.corrected, bk.recomputed)
+    assert events_key(rep.events) == events_key(bk.events) and len(bk.events) >= 2
 
 
 def test_dtrsm_noft_twin_bitwise_and_alpha():
@@ -143,9 +143,41 @@ def test_dtrsm_right_side_integer_exact_with_faults(uplo, tr):
     rep = F.ftblas_dtrsm("R", uplo, tr, "U", m, n, 1.0, to_dev(T), n, dB, m)
     assert np.array_equal(from_dev(dB, m, n), X)
     assert (rep.detected, rep.corrected, rep.recomputed) == (5, 5, 0)
-    leaf = trsm_leaf_ids(n)
-    cross = sorted((f[0], f[1]) for f, (i, j, p) in zip(faults, pairs) if leaf[j] != leaf[p])
-    assert len(cross) >= 2 and sorted((e[1], e[2]) for e in rep.events) == cross
+    bk = oracle.dtrsm_bookkeeping("R", uplo, tr, m, n, faults)
+    assert (rep.units_checked, rep.detected, rep.corrected, rep.recomputed) == \
+        (bk.units_checked, bk.detected, bk.corrected, bk.recomputed)
+    assert events_key(rep.events) == events_key(bk.events) and len(bk.events) >= 2
     d2 = to_dev(B)
     F.ftblas_dtrsm_noft("R", uplo, tr, "U", m, n, 1.0, to_dev(T), n, d2, m)
     assert np.array_equal(from_dev(d2, m, n), X)
+
+
+@pytest.mark.parametrize("side", ["L", "R"])
+def test_dtrsm_multi_fault_units_against_bookkeeping(side):
+    """Two cells of one ABFT unit of an update -> recomputed (event at the unit origin), two
+    faults of one right-hand side in one diagonal block -> one DMR detection: GPU counters and
+    events against the oracle's bookkeeping of the blocked solve (reading R21, R6)."""
+    rng = np.random.default_rng(23)
+    na, nr = 700, 190
+    T = rng.integers(-1, 2, (na, na)).astype(float)
+    T = np.asfortranarray(np.tril(T, -1) + np.eye(na))
+    X = rng.integers(-3, 4, (na, nr) if side == "L" else (nr, na)).astype(float)
+    if side == "L":
+        B = np.asfortranarray(T @ X)
+        m, n = na, nr
+        faults = [(600, 5, 20, 7.0), (601, 6, 30, -3.0), (650, 150, 400, 2.0), (60, 9, 30, 5.0),
+                  (20, 9, 5, 1.0), (70, 9, 40, 1.0)]
+    else:  # X T = B, T lower -> columns in descending order: step after the column
+        B = np.asfortranarray(X @ T)
+        m, n = nr, na
+        faults = [(5, 20, 600, 7.0), (6, 30, 601, -3.0), (150, 300, 650, 2.0), (9, 640, 660, 5.0),
+                  (9, 650, 670, 1.0)]
+    dB = to_dev(B)
+    F.ftblas_inject_arm(faults)
+    rep = F.ftblas_dtrsm(side, "L", "N", "U", m, n, 1.0, to_dev(T), na, dB, m)
+    assert np.array_equal(from_dev(dB, m, n), X)
+    bk = oracle.dtrsm_bookkeeping(side, "L", "N", m, n, faults)
+    assert (rep.units_checked, rep.detected, rep.corrected, rep.recomputed) == \
+        (bk.units_checked, bk.detected, bk.corrected, bk.recomputed)
+    assert events_key(rep.events) == events_key(bk.events)
+    assert bk.recomputed >= 1 and bk.detected > bk.n_events  # ABFT units and DMR blocks

@@ -51,7 +51,9 @@ def test_against_scipy_within_bound():
             Xs = sla.solve_triangular(A, -0.75 * B, lower=(uplo == "L"), trans=(1 if tr == "T" else 0))
             Xo = Xo.reshape((n, m)).T
             assert np.max(np.abs(Xo - Xs)) <= 64 * m * U * np.max(np.abs(Xs))
-            assert det == (1, 1)  # faults are corrected by the protection: counted, X fault-free
+            # faults are corrected by the protection (X fault-free); (1, 0, 0) sits in the one
+            # diagonal block: a DMR detection and correction, no ABFT event
+            assert (det.detected, det.corrected, det.n_events) == (1, 1, 0)
 
 
 def test_right_side_closed_forms_integer_and_scipy():
@@ -87,3 +89,32 @@ def test_right_side_closed_forms_integer_and_scipy():
             Xs = sla.solve_triangular(opA.T, 0.5 * Bs.T, lower=not ((uplo == "L") != (tr == "T"))).T
             Xo = Xo.reshape((n, m)).T
             assert np.max(np.abs(Xo - Xs)) <= 64 * n * U * np.max(np.abs(Xs))
+
+
+def test_dtrsm_bookkeeping_hand_derived_split():
+    """FT-DTRSM bookkeeping (reading R21) against the split worked out by hand for 300
+    positions (leaf 128, units 127; include/ftblas.h): forward order solves [0, 46) (leaf),
+    updates rows [46, 300) with k in [0, 46), then splits [46, 300) into the leaf [46, 174),
+    the update rows [174, 300) with k in [46, 174) and the leaf [174, 300).  Units of the
+    first update: 2 x 3, of the second 1 x 3 (n = 300 right-hand sides)."""
+    bk = oracle.dtrsm_bookkeeping
+    r = bk("L", "L", "N", 300, 300, [(200, 5, 10, 1.0)])  # row 200, step 10: first update
+    assert (r.units_checked, r.detected, r.corrected, r.recomputed) == (9, 1, 1, 0)
+    assert [e[:4] for e in r.events] == [(0, 200, 5, 1)]
+    r = bk("L", "L", "N", 300, 300, [(100, 5, 60, 1.0)])  # both in the leaf [46, 174): DMR
+    assert (r.detected, r.corrected, r.n_events) == (1, 1, 0)
+    # two cells of one unit of the second update (rows 174.., k 46..174): recomputed, origin (174, 0)
+    r = bk("L", "L", "N", 300, 300, [(180, 7, 100, 1.0), (185, 8, 50, 2.0), (181, 200, 60, 3.0)])
+    assert (r.detected, r.corrected, r.recomputed) == (2, 1, 1)
+    assert [e[:4] for e in r.events] == [(0, 174, 0, 2), (0, 181, 200, 1)]
+    # two faults in one leaf block, same right-hand side: one DMR detection (per column)
+    r = bk("L", "L", "N", 300, 300, [(100, 5, 60, 1.0), (120, 5, 50, 1.0), (120, 6, 50, 1.0)])
+    assert (r.detected, r.corrected, r.n_events) == (2, 2, 0)
+    # backward order (lower, transposed): leaf [254, 300) first, then rows [0, 254) with k in
+    # [254, 300); row 10, step 280 -> that update, unit (0, 0)
+    r = bk("L", "L", "T", 300, 300, [(10, 3, 280, 1.0)])
+    assert [e[:4] for e in r.events] == [(0, 10, 3, 1)] and r.units_checked == 2 * 3 + 1 * 3
+    # side R, forward (upper, not transposed): the same split over B's 300 columns; row i is the
+    # right-hand side: (i 5, column 200, step 10) -> first update, unit (0, (200 - 46) // 127)
+    r = bk("R", "U", "N", 260, 300, [(5, 200, 10, 1.0)])
+    assert [e[:4] for e in r.events] == [(0, 5, 200, 1)] and r.units_checked == 3 * 2 + 3 * 1
