@@ -79,28 +79,3 @@ def encode_mode(F, name):
         yield
     finally:
         F.ftblas_set_encode(F.ENCODE_FUSED)
-
-
-def trsm_leaf_ids(length, leaf=128, tm=127):
-    """Diagonal-block id of every position (substitution order) of the recursive FT-DTRSM split
-    documented in include/ftblas.h: a block of len > leaf positions solves its first len - u
-    positions, then updates and solves its last u = 2 tm j (j = (len + 2 tm) // (4 tm), reduced
-    until u < len) or tm - 1 when j = 0."""
-    ids = [0] * length
-    nxt = [0]
-
-    def rec(q0, n):
-        if n <= leaf:
-            for q in range(q0, q0 + n):
-                ids[q] = nxt[0]
-            nxt[0] += 1
-            return
-        j = (n + 2 * tm) // (4 * tm)
-        while j > 0 and 2 * tm * j >= n:
-            j -= 1
-        u = 2 * tm * j if j > 0 else tm - 1
-        rec(q0, n - u)
-        rec(q0 + n - u, u)
-
-    rec(0, length)
-    return ids
