@@ -675,6 +675,7 @@ __device__ __forceinline__ TileGeom load_geom(const TileGeom &g) {
 }
 
 constexpr int MAX_FIX = 32;  // distinct corrected cells per tile recomputed in the epilogue (R4)
+constexpr int STRIP_LD = 128;  // column stride of the verification strip (doubles)
 struct SmemTail {
   TileGeom geo;
   // Cluster-pair B encode: the partner's 8 k-slot sums of B_J e per stage and its half maximum;
@@ -687,7 +688,7 @@ struct SmemTail {
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
   // Online verification (check_unit): the staging strip (128 rows x 16 columns), the reference
   // sums, the carried checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
-  double strip[128 * 16], colsum[128], rowsum[128], cs_col[128], cs_row[128];
+  double strip[16 * STRIP_LD], colsum[128], rowsum[128], rowpart[2][128], cs_col[128], cs_row[128];
   double dres[256];
   double red[NTHREADS / 32];
   unsigned int amax_hi, bmax_hi;   // PREPASS: the blocks' whole-k maxima (R1' high words)
@@ -1024,70 +1025,38 @@ __device__ __forceinline__ int acc_owner_index(int si, int sj, int wm, int wn, i
   return owner ? (fmt * 4 + fnt) * 2 + (cc & 1) : -1;
 }
 
-// The accumulators stay in registers: they are staged through a 16 KB shared-memory strip, one
-// (b, e) accumulator slot of every thread per round (a 128-row x 16-column strip of the tile),
-// and reduced from there: thread i < 128 keeps the running row sum of row i, threads 128..255
-// sum the strip's columns (8 threads x 16 rows per column, then xor-shuffles).  Staging only
-// reads the accumulators, so the DMMA k-loop keeps its register allocation.
+// Record a corrected cell (staged row si, column sj) for the epilogue's fresh dot product.
+__device__ __forceinline__ void add_fix(SmemTail &tl, int si, int sj) {
+  const int cell = si | (sj << 8);
+  int q = 0;
+  while (q < tl.nfix && tl.fix[q] != cell) ++q;
+  if (q == tl.nfix && q < MAX_FIX) tl.fix[tl.nfix++] = cell;
+}
+
 struct CheckOut {
   int multi;    // 1: recompute the unit (R6)
   int si, sj;   // single error: the located staged cell (si = -1: none)
   double dcol;  // the located magnitude d_col to subtract from it
 };
+
+// Sum over 4 rows of one staged column held by a lane (rows lane + 32 q), the checksum row
+// excluded, then over the warp: the column's reference sum e^T C_IJ in every lane.
+__device__ __forceinline__ double col_sum_warp(const double *col, int lane, int cra) {
+  double v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = (lane + 32 * q == cra) ? 0.0 : col[lane + 32 * q];
+  double c = (v[0] + v[1]) + (v[2] + v[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  return c;
+}
+
+// Residuals, threshold, flags, classification and report of one unit at the end of
+// interval t, from the reference sums (tl.colsum, tl.rowsum) and the carried checksums
+// (tl.cs_col, tl.cs_row) already in shared memory.  All 256 MMA threads.
 template <bool AKM, bool BKM>
-__device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, const double (&acc)[8][4][2], int t,
-                                               int64_t kt, int mw, int wm, int wn, int lane) {
-  const int g = lane >> 2, tq = lane & 3;
+__device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, int t, int64_t kt, int mw, int lane) {
   const int vt = mw * 32 + lane;  // 0..255
-  const int cra = tl.geo.cra, crb = tl.geo.crb;
-  double rsum = 0.0;  // vt < 128: row vt over the data columns (checksum column crb excluded)
-  // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round
-  // rd = 2 b + e.  The rounds run as a rolled loop (one copy of the reduction code); only the
-  // staging selects its accumulator slot by a switch on the round.
-  const int q = wn * 4 + tq;
-  double *const st = tl.strip + q * 128 + wm * 64;
-#pragma unroll 1
-  for (int rd = 0; rd < 8; ++rd) {
-    switch (rd) {
-#define FT_STAGE_ROUND(B, E)                                                           \
-  case 2 * B + E:                                                                      \
-    _Pragma("unroll") for (int a = 0; a < 8; ++a) st[tile_row<AKM>(a, g)] = acc[a][B][E]; \
-    break;
-      FT_STAGE_ROUND(0, 0) FT_STAGE_ROUND(0, 1) FT_STAGE_ROUND(1, 0) FT_STAGE_ROUND(1, 1)
-      FT_STAGE_ROUND(2, 0) FT_STAGE_ROUND(2, 1) FT_STAGE_ROUND(3, 0) FT_STAGE_ROUND(3, 1)
-#undef FT_STAGE_ROUND
-    }
-    bar_sync(BAR_PART, 256);
-    const int b = rd >> 1, e = rd & 1;
-    if (vt < 128) {
-      const int r = vt;
-      for (int qq = 0; qq < 16; ++qq) {
-        const int col = (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
-        const double v = tl.strip[qq * 128 + r];
-        if (col != crb) rsum += v;
-        else tl.cs_row[r] = v;  // carried A_I (B_J e)
-      }
-    } else {
-      const int qq = (vt - 128) >> 3, part = vt & 7;  // column qq, rows 16 part .. 16 part + 15
-      double c = 0.0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int r = 16 * part + i;
-        const double v = tl.strip[qq * 128 + r];
-        if (r != cra) c += v;
-      }
-#pragma unroll
-      for (int o = 1; o <= 4; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      const int col = (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
-      if (part == 0) {
-        tl.colsum[col] = c;
-        tl.cs_col[col] = tl.strip[qq * 128 + cra];  // carried (e^T A_I) B_J
-      }
-    }
-    bar_sync(BAR_PART, 256);  // the strip is rewritten by the next round
-  }
-  if (vt < 128) tl.rowsum[vt] = rsum;
-  bar_sync(BAR_PART, 256);
   const TileGeom x = load_geom(tl.geo);
   // Cumulative maxima of op(A)_I and op(B)_J over the updates so far (R1'): the running value
   // plus the encoders' maxima of interval t's stages (slot t & 7; PREPASS: whole-k presets).
@@ -1134,22 +1103,10 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   if (nfr == 0 && nfc == 0) return out;
   const bool multi = !(nfr == 1 && nfc == 1);
   const int fr = tl.first_row[par], fc = tl.first_col[par];
-  if (!multi) {
-    // Single error at the intersection (i0+fr, j0+fc): the caller subtracts the located
-    // magnitude d_col in its owner's register now, so the next intervals verify
-    // the corrected partial product; in recompute mode (R4) the element is replaced by a fresh
-    // k-long dot product in the epilogue (fix list), which equals the oracle's recomputed
-    // partial plus its later updates.
-    const int si = fr + x.oa, sj = fc + x.ob;
-    out.si = si;
-    out.sj = sj;
+  if (!multi) {  // single error at the intersection (i0+fr, j0+fc)
+    out.si = fr + x.oa;
+    out.sj = fc + x.ob;
     out.dcol = tl.dres[fc];
-    if (vt == 0 && P.correct_mode != 1) {
-      const int cell = si | (sj << 8);
-      int q = 0;
-      while (q < tl.nfix && tl.fix[q] != cell) ++q;
-      if (q == tl.nfix && q < MAX_FIX) tl.fix[tl.nfix++] = cell;
-    }
   }
   if (vt == 0) {
     atomicAdd(&P.counters[CNT_DETECTED], 1ull);
@@ -1163,6 +1120,95 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   }
   out.multi = multi ? 1 : 0;
   return out;
+}
+
+// Check at the end of an intermediate interval (Kc < k), with the accumulators LIVE in
+// registers (the k-loop continues): they are staged through a 16 KB shared-memory strip, one
+// (b, e) accumulator slot of every thread per round -- a 128-row x 16-column strip of the tile
+// (column stride STRIP_LD) -- and reduced from there, all reads conflict-free: each warp sums
+// 2 strip columns (lane = rows lane + 32 q, then a warp butterfly), thread vt keeps the
+// running sum of row vt & 127 over half of the strip's columns.  Staging only reads the
+// accumulators, so the DMMA k-loop keeps its register allocation (the rounds are a rolled
+// loop; a switch picks the accumulator slot).
+template <bool AKM, bool BKM>
+__device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, const double (&acc)[8][4][2], int t,
+                                               int64_t kt, int mw, int wm, int wn, int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+  const int vt = mw * 32 + lane;  // 0..255
+  const int cra = tl.geo.cra, crb = tl.geo.crb;
+  const int r = vt & 127, h = vt >> 7;
+  double rsum = 0.0;  // row r over the data columns of strip half h (checksum column crb excluded)
+  // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round 2 b + e
+  double *const st = tl.strip + (wn * 4 + tq) * STRIP_LD + wm * 64;
+#pragma unroll 1
+  for (int rd = 0; rd < 8; ++rd) {
+    switch (rd) {
+#define FT_STAGE_ROUND(B, E)                                                           \
+  case 2 * B + E:                                                                      \
+    _Pragma("unroll") for (int a = 0; a < 8; ++a) st[tile_row<AKM>(a, g)] = acc[a][B][E]; \
+    break;
+      FT_STAGE_ROUND(0, 0) FT_STAGE_ROUND(0, 1) FT_STAGE_ROUND(1, 0) FT_STAGE_ROUND(1, 1)
+      FT_STAGE_ROUND(2, 0) FT_STAGE_ROUND(2, 1) FT_STAGE_ROUND(3, 0) FT_STAGE_ROUND(3, 1)
+#undef FT_STAGE_ROUND
+    }
+    bar_sync(BAR_PART, 256);
+    const int b = rd >> 1, e = rd & 1;
+    auto tcol = [&](int qq) {  // tile column of strip column qq in this round
+      return (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
+    };
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2) {  // warp mw: strip columns 2 mw, 2 mw + 1
+      const int qq = 2 * mw + c2;
+      const double c = col_sum_warp(tl.strip + qq * STRIP_LD, lane, cra);
+      if (lane == 0) {
+        tl.colsum[tcol(qq)] = c;
+        tl.cs_col[tcol(qq)] = tl.strip[qq * STRIP_LD + cra];  // carried (e^T A_I) B_J
+      }
+    }
+    double rp[2] = {0.0, 0.0};
+#pragma unroll
+    for (int qq = 8 * h; qq < 8 * h + 8; ++qq) {
+      const double v = tl.strip[qq * STRIP_LD + r];
+      if (tcol(qq) != crb) rp[qq & 1] += v;
+      else tl.cs_row[r] = v;  // carried A_I (B_J e)
+    }
+    rsum += rp[0] + rp[1];
+    bar_sync(BAR_PART, 256);  // the strip is rewritten by the next round
+  }
+  tl.rowpart[h][r] = rsum;
+  bar_sync(BAR_PART, 256);
+  if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
+  bar_sync(BAR_PART, 256);
+  return check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
+}
+
+// The last interval's check, on the accumulators staged in shared memory for the epilogue
+// (ctile, pitch LDC_S): the accumulators are dead in registers, so it reads the whole tile in
+// one pass -- warp mw sums tile columns 16 mw .. 16 mw + 15 (lanes over rows, butterfly),
+// thread vt sums row vt & 127 over one half of the columns.
+template <bool AKM, bool BKM>
+__device__ __forceinline__ CheckOut check_tile(const Params &P, SmemTail &tl, const double *ctile, int t, int64_t kt,
+                                               int mw, int lane) {
+  const int vt = mw * 32 + lane;
+  const int cra = tl.geo.cra, crb = tl.geo.crb;
+#pragma unroll 4
+  for (int c = 16 * mw; c < 16 * mw + 16; ++c) {
+    const double s = col_sum_warp(ctile + c * LDC_S, lane, cra);
+    if (lane == 0) {
+      tl.colsum[c] = s;
+      tl.cs_col[c] = ctile[c * LDC_S + cra];  // carried (e^T A_I) B_J
+    }
+  }
+  const int r = vt & 127, h = vt >> 7;
+  double rp[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 16
+  for (int c = 64 * h; c < 64 * h + 64; ++c) rp[c & 3] += (c == crb) ? 0.0 : ctile[c * LDC_S + r];
+  tl.rowpart[h][r] = (rp[0] + rp[1]) + (rp[2] + rp[3]);
+  if (h == 0) tl.cs_row[r] = ctile[crb * LDC_S + r];  // carried A_I (B_J e)
+  bar_sync(BAR_PART, 256);
+  if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
+  bar_sync(BAR_PART, 256);
+  return check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
 }
 
 // ---------------- warpgroups 1-2: MMA warps (+ online verification and epilogue)
@@ -1206,10 +1252,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     if (lane == 0) {
       st_sv(ws, W_FNEXT, x.f_lo);
       st_sv(ws, W_NEXT_STAGE, x.f_lo < x.f_hi ? P.faults[x.f_lo].stage : 0x7fffffff);
-      // Stage index at which the next verification interval ends (Kc = KcS stages); the last
-      // interval is checked at the virtual stage nk + 1.
-      st_sv(ws, W_NEXT_CHECK, !verify ? 0x7fffffff
-                         : (t_done + 1 < P.T - 1 ? (t_done + 2) * max(1, (int)(P.Kc / BK)) : nk + 1));
+      // Stage index at which the next intermediate verification interval ends (Kc = KcS
+      // stages); the last interval is checked after the k-loop, on the staged tile.
+      st_sv(ws, W_NEXT_CHECK, verify && t_done + 1 < P.T - 1 ? (t_done + 2) * max(1, (int)(P.Kc / BK)) : 0x7fffffff);
       st_sv(ws, W_FAILED, -1);
     }
     __syncwarp();
@@ -1259,8 +1304,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       }
       s = gs - ld_sv(ws, W_BASE);
       // At the end of a segment: an interval ends at stage s (its check comes before the faults
-      // due at stage s, which belong to the next interval); the last interval is checked at the
-      // virtual stage nk + 1, after the faults with step_q == k.  One call site each, so the
+      // due at stage s, which belong to the next interval).  One call site each, so the
       // register allocation of the DMMA loop is not disturbed.
       // A correction located by the check is applied like a fault: -d_col at the located cell
       // (one select block for both, so the register allocation of the DMMA loop is undisturbed).
@@ -1268,11 +1312,16 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       double pend_d = 0.0;
       if (FT && s == ld_sv(ws, W_NEXT_CHECK)) {
         const int kcs = max(1, (int)(P.Kc / BK));
-        const int tcur = s > nk ? P.T - 1 : s / kcs - 1;
-        const CheckOut co = check_unit<AKM, BKM>(P, tl, acc, tcur, min64((int64_t)s * BK, P.k), mw, wm, wn, lane);
+        const int tcur = s / kcs - 1;
+        const CheckOut co = check_unit<AKM, BKM>(P, tl, acc, tcur, (int64_t)s * BK, mw, wm, wn, lane);
+        // A single error is subtracted now, so the next intervals verify the
+        // corrected partial product; in recompute mode (R4) the cell is also replaced by a fresh
+        // k-long dot product in the epilogue (fix list), which equals the oracle's recomputed
+        // partial plus its later updates.
         pend_si = co.si;
         pend_sj = co.sj;
         pend_d = -co.dcol;
+        if (vt == 0 && co.si >= 0 && P.correct_mode != 1) add_fix(tl, co.si, co.sj);
         __syncwarp();
         if (lane == 0) {
           if (co.multi) {  // recompute: the rest of this attempt is neither injected nor verified
@@ -1281,7 +1330,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
             st_sv(ws, W_FNEXT, x.f_hi);
             st_sv(ws, W_NEXT_STAGE, 0x7fffffff);
           } else {
-            st_sv(ws, W_NEXT_CHECK, tcur + 1 < P.T - 1 ? (tcur + 2) * kcs : (tcur + 1 == P.T - 1 ? nk + 1 : 0x7fffffff));
+            st_sv(ws, W_NEXT_CHECK, tcur + 1 < P.T - 1 ? (tcur + 2) * kcs : 0x7fffffff);
           }
         }
         __syncwarp();
@@ -1328,18 +1377,40 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
               acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v + dv : v;
             }
       }
-      if (s == nk && ld_sv(ws, W_NEXT_CHECK) == nk + 1) {  // go round once more for the last interval's check
-        ++s;
-        continue;
-      }
       if (s >= nk) break;
     }
     __syncwarp();
     if (lane == 0) st_sv(ws, W_BASE, ld_sv(ws, W_BASE) + nk);  // the next attempt's first stage
     __syncwarp();
+    int failed = ld_sv(ws, W_FAILED);  // the same in every MMA warp (a CTA-wide decision)
+    // Stage the accumulators into the ring as the C tile: every MMA warp has consumed its last
+    // stage (and every TMA write and checksum row has landed before that stage was consumed).
+    bar_sync(BAR_CTILE, 256);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int row = wm * 64 + tile_row<AKM>(a, g);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * 32 + tile_row<BKM>(b, 2 * t + e);
+          ctile[col * LDC_S + row] = acc[a][b][e];
+        }
+    }
+    bar_sync(BAR_CTILE, 256);
+    if (verify && failed < 0) {
+      // The last interval, verified before C is written, on the staged tile.
+      const CheckOut co = check_tile<AKM, BKM>(P, tl, ctile, P.T - 1, P.k, mw, lane);
+      if (co.multi) {
+        failed = P.T - 1;
+      } else if (co.si >= 0 && vt == 0) {
+        if (P.correct_mode == 1) ctile[co.sj * LDC_S + co.si] -= co.dcol;
+        else add_fix(tl, co.si, co.sj);                                   // R4: fresh dot product
+      }
+    }
+    if (failed >= 0) fence_proxy_async();  // generic writes to the ring before TMA refills it
     bar_sync(BAR_RING_FREE, NTHREADS);  // every stage consumed: the ring is free for the C tile
     if (!verify) break;
-    const int failed = ld_sv(ws, W_FAILED);  // the same in every MMA warp (a CTA-wide decision)
     if (vt == 0) {
       tl.retry = failed;
       if (failed >= 0) tl.nfix = 0;  // the recompute re-forms every element
@@ -1352,19 +1423,8 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     if (failed < 0) break;  // else out of the one-error model: recompute the unit (R6)
   }
 
-  // ---- store: C = alpha*acc + beta*C0 (two roundings each, no contraction), staged through
-  // shared memory for coalesced column stores.
-#pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int row = wm * 64 + tile_row<AKM>(a, g);
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = wn * 32 + tile_row<BKM>(b, 2 * t + e);
-        ctile[col * LDC_S + row] = acc[a][b][e];
-      }
-  }
+  // ---- epilogue: corrected cells (recompute mode), then C = alpha*acc + beta*C0 (two
+  // roundings each, no contraction) from the staged tile, coalesced column stores.
   bar_sync(BAR_CTILE, 256);
   const TileGeom ge = load_geom(tl.geo);
   if (FT) {
