@@ -1137,6 +1137,10 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   const int vt = mw * 32 + lane;  // 0..255
   const int cra = tl.geo.cra, crb = tl.geo.crb;
   const int r = vt & 127, h = vt >> 7;
+#ifdef FTBLAS_DEV
+  const long long dv_t0 = clock64();
+  long long dv_t1 = dv_t0;
+#endif
   double rsum = 0.0;  // row r over the data columns of strip half h (checksum column crb excluded)
   // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round 2 b + e
   double *const st = tl.strip + (wn * 4 + tq) * STRIP_LD + wm * 64;
@@ -1152,6 +1156,9 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
 #undef FT_STAGE_ROUND
     }
     bar_sync(BAR_PART, 256);
+#ifdef FTBLAS_DEV
+    if (rd == 0) dv_t1 = clock64();
+#endif
     const int b = rd >> 1, e = rd & 1;
     auto tcol = [&](int qq) {  // tile column of strip column qq in this round
       return (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
@@ -1179,7 +1186,19 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   bar_sync(BAR_PART, 256);
   if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
   bar_sync(BAR_PART, 256);
+#ifdef FTBLAS_DEV
+  const CheckOut dv_out = check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
+  if (FT_DEV_PROF(P) && vt == 0) {  // [arrival skew + first staging, reductions + decision], count
+    unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 8) * 2;
+    const long long t2 = clock64();
+    dp[0] += (unsigned long long)(dv_t1 - dv_t0);
+    dp[1] += (unsigned long long)(t2 - dv_t1);
+    dp[2] += 1ull;
+  }
+  return dv_out;
+#else
   return check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
+#endif
 }
 
 // The last interval's check, on the accumulators staged in shared memory for the epilogue
