@@ -1187,13 +1187,15 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
   bar_sync(BAR_PART, 256);
 #ifdef FTBLAS_DEV
+  const long long dv_t2 = clock64();
   const CheckOut dv_out = check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
-  if (FT_DEV_PROF(P) && vt == 0) {  // [arrival skew + first staging, reductions + decision], count
+  if (FT_DEV_PROF(P) && vt == 0) {  // [arrival skew + first staging, reductions], [count, decision]
     unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 8) * 2;
-    const long long t2 = clock64();
+    const long long t3 = clock64();
     dp[0] += (unsigned long long)(dv_t1 - dv_t0);
-    dp[1] += (unsigned long long)(t2 - dv_t1);
+    dp[1] += (unsigned long long)(dv_t2 - dv_t1);
     dp[2] += 1ull;
+    dp[3] += (unsigned long long)(t3 - dv_t2);
   }
   return dv_out;
 #else

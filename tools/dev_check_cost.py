@@ -43,4 +43,5 @@ calls = p[:, 2].sum().item()
 print(f"{M}x{N}x{K}: noft {noft:.2f} ms, ft {ft:.2f} ms ({100 * (ft - noft) / noft:.2f}%), "
       f"ft Kc={KC} {ftk:.2f} ms ({100 * (ftk - noft) / noft:.2f}%)", flush=True)
 print(f"intermediate checks: {calls:.0f} (2 timed runs); per check clk: skew+stage "
-      f"{p[:, 0].sum().item() / calls:.0f}, reduce+decide {p[:, 1].sum().item() / calls:.0f}", flush=True)
+      f"{p[:, 0].sum().item() / calls:.0f}, reductions {p[:, 1].sum().item() / calls:.0f}, "
+      f"decision {p[:, 3].sum().item() / calls:.0f}", flush=True)
