@@ -1039,15 +1039,19 @@ struct CheckOut {
   double dcol;  // the located magnitude d_col to subtract from it
 };
 
-// Sum over 4 rows of one staged column held by a lane (rows lane + 32 q), the checksum row
-// excluded, then over the warp: the column's reference sum e^T C_IJ in every lane.
-__device__ __forceinline__ double col_sum_warp(const double *col, int lane, int cra) {
-  double v[4];
+// Reference sums e^T C_IJ of two staged columns per warp: half-warp hw = lane >> 4 takes column
+// c0 + hw (stride ld), its lanes rows (lane & 15) + 16 q (consecutive rows: conflict-free), the
+// checksum row excluded; then a 4-level butterfly inside each half.  Lanes 0 and 16 return the
+// two sums.
+__device__ __forceinline__ double col_sum_pair(const double *col0, int ld, int lane, int cra) {
+  const double *col = col0 + (lane >> 4) * ld;
+  const int r0 = lane & 15;
+  double v[8];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) v[q] = (lane + 32 * q == cra) ? 0.0 : col[lane + 32 * q];
-  double c = (v[0] + v[1]) + (v[2] + v[3]);
+  for (int q = 0; q < 8; ++q) v[q] = (r0 + 16 * q == cra) ? 0.0 : col[r0 + 16 * q];
+  double c = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   return c;
 }
 
@@ -1126,7 +1130,7 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
 // registers (the k-loop continues): they are staged through a 16 KB shared-memory strip, one
 // (b, e) accumulator slot of every thread per round -- a 128-row x 16-column strip of the tile
 // (column stride STRIP_LD) -- and reduced from there, all reads conflict-free: each warp sums
-// 2 strip columns (lane = rows lane + 32 q, then a warp butterfly), thread vt keeps the
+// 2 strip columns (a half-warp each, 4-level butterflies), thread vt keeps the
 // running sum of row vt & 127 over half of the strip's columns.  Staging only reads the
 // accumulators, so the DMMA k-loop keeps its register allocation (the rounds are a rolled
 // loop; a switch picks the accumulator slot).
@@ -1163,11 +1167,10 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     auto tcol = [&](int qq) {  // tile column of strip column qq in this round
       return (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
     };
-#pragma unroll
-    for (int c2 = 0; c2 < 2; ++c2) {  // warp mw: strip columns 2 mw, 2 mw + 1
-      const int qq = 2 * mw + c2;
-      const double c = col_sum_warp(tl.strip + qq * STRIP_LD, lane, cra);
-      if (lane == 0) {
+    {  // warp mw: strip columns 2 mw, 2 mw + 1 (one per half-warp)
+      const double c = col_sum_pair(tl.strip + 2 * mw * STRIP_LD, STRIP_LD, lane, cra);
+      const int qq = 2 * mw + (lane >> 4);
+      if ((lane & 15) == 0) {
         tl.colsum[tcol(qq)] = c;
         tl.cs_col[tcol(qq)] = tl.strip[qq * STRIP_LD + cra];  // carried (e^T A_I) B_J
       }
@@ -1205,19 +1208,20 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
 
 // The last interval's check, on the accumulators staged in shared memory for the epilogue
 // (ctile, pitch LDC_S): the accumulators are dead in registers, so it reads the whole tile in
-// one pass -- warp mw sums tile columns 16 mw .. 16 mw + 15 (lanes over rows, butterfly),
+// one pass -- warp mw sums tile columns 16 mw .. 16 mw + 15 (two per pass, half-warp butterflies),
 // thread vt sums row vt & 127 over one half of the columns.
 template <bool AKM, bool BKM>
 __device__ __forceinline__ CheckOut check_tile(const Params &P, SmemTail &tl, const double *ctile, int t, int64_t kt,
                                                int mw, int lane) {
   const int vt = mw * 32 + lane;
   const int cra = tl.geo.cra, crb = tl.geo.crb;
-#pragma unroll 4
-  for (int c = 16 * mw; c < 16 * mw + 16; ++c) {
-    const double s = col_sum_warp(ctile + c * LDC_S, lane, cra);
-    if (lane == 0) {
-      tl.colsum[c] = s;
-      tl.cs_col[c] = ctile[c * LDC_S + cra];  // carried (e^T A_I) B_J
+#pragma unroll 2
+  for (int c = 16 * mw; c < 16 * mw + 16; c += 2) {  // two columns per pass, one per half-warp
+    const double s = col_sum_pair(ctile + c * LDC_S, LDC_S, lane, cra);
+    if ((lane & 15) == 0) {
+      const int cc = c + (lane >> 4);
+      tl.colsum[cc] = s;
+      tl.cs_col[cc] = ctile[cc * LDC_S + cra];  // carried (e^T A_I) B_J
     }
   }
   const int r = vt & 127, h = vt >> 7;
@@ -1230,6 +1234,31 @@ __device__ __forceinline__ CheckOut check_tile(const Params &P, SmemTail &tl, co
   if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
   bar_sync(BAR_PART, 256);
   return check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
+}
+
+// The DMMA k-loop of a sliver tile's warp over its first NA m-tiles and NB n-tiles only.
+template <bool AKM, bool BKM, int NA, int NB>
+__device__ __forceinline__ void kloop_narrow(SmemTail &tl, const double *ring, uint32_t ready, int &gs, int gs_end,
+                                             int wm, int wn, int g, int t, int lane, double (&acc)[8][4][2]) {
+  for (; gs < gs_end; ++gs) {
+    const int slot = gs % STAGES;
+    mbar_wait_u32(ready + 8u * slot, (gs / STAGES) & 1);
+    const double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double af[2][NA], bf[2][NB];
+      load_frags<AKM, NA>(sA, wm * 64, h, g, t, af);
+      load_frags<BKM, NB>(sB, wn * 32, h, g, t, bf);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+#pragma unroll
+          for (int b = 0; b < NB; ++b) dmma_8x8x4(acc[a][b], af[e][a], bf[e][b]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tl.empty[slot]);
+  }
 }
 
 // ---------------- warpgroups 1-2: MMA warps (+ online verification and epilogue)
@@ -1257,14 +1286,24 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   constexpr bool SKIP = FT || (AKM && !BKM);
   const bool active = FT ? (wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1))
                          : (!SKIP || (wm * 64 < x.bm_eff && wn * 32 < x.bn_eff));
+  // Sliver tiles (the last tile row / column of a size that is not a multiple of 127): a warp
+  // whose used rows (columns) of its 64 x 32 quarter fit in its first 2 m-tiles (n-tiles) -- 16
+  // rows (columns) in either fragment layout -- runs a narrow DMMA loop over those tiles only
+  // (bit 0: rows, bit 1: columns); the other accumulators stay zero.
+  // (kept in the warp's shared slot W_NARROW: no register held across the DMMA loops)
   double acc[8][4][2];
   // Segment state that changes only between segments lives in this warp's shared-memory slots
   // (lane-uniform), not in registers across the DMMA loop: next fault stage, next interval end,
   // next fault index, the interval of a recompute decision in this attempt.
   // (32-bit shared addresses through volatile ld/st.shared: no generic pointer held in registers)
   const uint32_t ws = smem_u32(&tl.wstate[mw][0]);
-  enum { W_NEXT_STAGE = 0, W_NEXT_CHECK, W_FNEXT, W_FAILED, W_BASE };
-  if (lane == 0) st_sv(ws, W_BASE, 0);
+  enum { W_NEXT_STAGE = 0, W_NEXT_CHECK, W_FNEXT, W_FAILED, W_BASE, W_NARROW };
+  if (lane == 0) {
+    st_sv(ws, W_BASE, 0);
+    st_sv(ws, W_NARROW, !FT ? 0
+                            : (max(x.oa + x.bm_eff, x.cra + 1) - wm * 64 <= 16 ? 1 : 0) |
+                                  (max(x.ob + x.bn_eff, x.crb + 1) - wn * 32 <= 16 ? 2 : 0));
+  }
   for (int attempt = 0;; ++attempt) {
     // Interval of the last recompute decision (tl.retry, -1 in the first attempt): intervals
     // <= t_done are neither re-injected nor re-verified (the unit restarts from k = 0).
@@ -1303,6 +1342,12 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&tl.empty[slot]);
         }
+      }
+      const int narrow = FT ? ld_sv(ws, W_NARROW) : 0;
+      if (FT && narrow) {  // sliver tiles: only the m / n tiles holding used rows / columns
+        if (narrow == 1) kloop_narrow<AKM, BKM, 2, 4>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+        else if (narrow == 2) kloop_narrow<AKM, BKM, 8, 2>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+        else kloop_narrow<AKM, BKM, 2, 2>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
       }
       for (; gs < gs_end; ++gs) {
         const int slot = gs % STAGES;
