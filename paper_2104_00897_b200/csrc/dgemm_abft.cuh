@@ -1143,13 +1143,16 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   const int r = vt & 127, h = vt >> 7;
 #ifdef FTBLAS_DEV
   const long long dv_t0 = clock64();
-  long long dv_t1 = dv_t0;
+  long long dv_t1 = dv_t0, dv_rs = dv_t0, dv_stage = 0, dv_red = 0;
 #endif
   double rsum = 0.0;  // row r over the data columns of strip half h (checksum column crb excluded)
   // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round 2 b + e
   double *const st = tl.strip + (wn * 4 + tq) * STRIP_LD + wm * 64;
 #pragma unroll 1
   for (int rd = 0; rd < 8; ++rd) {
+#ifdef FTBLAS_DEV
+    dv_rs = clock64();
+#endif
     switch (rd) {
 #define FT_STAGE_ROUND(B, E)                                                           \
   case 2 * B + E:                                                                      \
@@ -1161,7 +1164,9 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     }
     bar_sync(BAR_PART, 256);
 #ifdef FTBLAS_DEV
-    if (rd == 0) dv_t1 = clock64();
+    const long long dv_m = clock64();
+    if (rd == 0) dv_t1 = dv_m;
+    dv_stage += dv_m - dv_rs;
 #endif
     const int b = rd >> 1, e = rd & 1;
     auto tcol = [&](int qq) {  // tile column of strip column qq in this round
@@ -1184,6 +1189,9 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     }
     rsum += rp[0] + rp[1];
     bar_sync(BAR_PART, 256);  // the strip is rewritten by the next round
+#ifdef FTBLAS_DEV
+    dv_red += clock64() - dv_m;
+#endif
   }
   tl.rowpart[h][r] = rsum;
   bar_sync(BAR_PART, 256);
@@ -1199,6 +1207,8 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     dp[1] += (unsigned long long)(dv_t2 - dv_t1);
     dp[2] += 1ull;
     dp[3] += (unsigned long long)(t3 - dv_t2);
+    dp[4] += (unsigned long long)dv_stage;
+    dp[5] += (unsigned long long)dv_red;
   }
   return dv_out;
 #else
