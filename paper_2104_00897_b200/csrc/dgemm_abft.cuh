@@ -1143,7 +1143,7 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   const int r = vt & 127, h = vt >> 7;
 #ifdef FTBLAS_DEV
   const long long dv_t0 = clock64();
-  long long dv_t1 = dv_t0, dv_rs = dv_t0, dv_stage = 0, dv_red = 0;
+  long long dv_t1 = dv_t0, dv_rs = dv_t0, dv_stage = 0, dv_red = 0, dv_sts = 0, dv_col = 0;
 #endif
   double rsum = 0.0;  // row r over the data columns of strip half h (checksum column crb excluded)
   // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round 2 b + e
@@ -1162,6 +1162,9 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
       FT_STAGE_ROUND(2, 0) FT_STAGE_ROUND(2, 1) FT_STAGE_ROUND(3, 0) FT_STAGE_ROUND(3, 1)
 #undef FT_STAGE_ROUND
     }
+#ifdef FTBLAS_DEV
+    dv_sts += clock64() - dv_rs;
+#endif
     bar_sync(BAR_PART, 256);
 #ifdef FTBLAS_DEV
     const long long dv_m = clock64();
@@ -1180,6 +1183,10 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
         tl.cs_col[tcol(qq)] = tl.strip[qq * STRIP_LD + cra];  // carried (e^T A_I) B_J
       }
     }
+#ifdef FTBLAS_DEV
+    const long long dv_c = clock64();
+    dv_col += dv_c - dv_m;
+#endif
     double rp[2] = {0.0, 0.0};
 #pragma unroll
     for (int qq = 8 * h; qq < 8 * h + 8; ++qq) {
@@ -1209,6 +1216,8 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     dp[3] += (unsigned long long)(t3 - dv_t2);
     dp[4] += (unsigned long long)dv_stage;
     dp[5] += (unsigned long long)dv_red;
+    dp[6] += (unsigned long long)dv_sts;
+    dp[7] += (unsigned long long)dv_col;
   }
   return dv_out;
 #else

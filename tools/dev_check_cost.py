@@ -38,11 +38,12 @@ prof.zero_()
 F.ftblas_set_interval(KC)
 ftk = t(lambda: F.ftblas_dgemm("N", "N", M, N, K, 1.0, A, M, B, K, 0.0, C, M, report=False))
 F.ftblas_set_interval(0)
-p = prof[: ntiles * 24].view(ntiles, 12, 2)[:, 8:11, :].reshape(ntiles, 6).double()
+p = prof[: ntiles * 24].view(ntiles, 12, 2)[:, 8:12, :].reshape(ntiles, 8).double()
 calls = p[:, 2].sum().item()
 print(f"{M}x{N}x{K}: noft {noft:.2f} ms, ft {ft:.2f} ms ({100 * (ft - noft) / noft:.2f}%), "
       f"ft Kc={KC} {ftk:.2f} ms ({100 * (ftk - noft) / noft:.2f}%)", flush=True)
 print(f"intermediate checks: {calls:.0f} (2 timed runs); per check clk: skew+stage "
       f"{p[:, 0].sum().item() / calls:.0f}, reductions {p[:, 1].sum().item() / calls:.0f}, "
       f"decision {p[:, 3].sum().item() / calls:.0f}; over the 8 rounds: staging+barrier "
-      f"{p[:, 4].sum().item() / calls:.0f}, reduction+barrier {p[:, 5].sum().item() / calls:.0f}", flush=True)
+      f"{p[:, 4].sum().item() / calls:.0f}, reduction+barrier {p[:, 5].sum().item() / calls:.0f}; "
+      f"stores {p[:, 6].sum().item() / calls:.0f}, column pair {p[:, 7].sum().item() / calls:.0f}", flush=True)
