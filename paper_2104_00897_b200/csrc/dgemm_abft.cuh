@@ -675,7 +675,6 @@ __device__ __forceinline__ TileGeom load_geom(const TileGeom &g) {
 }
 
 constexpr int MAX_FIX = 32;  // distinct corrected cells per tile recomputed in the epilogue (R4)
-constexpr int STRIP_LD = 128;  // column stride of the verification strip (doubles)
 struct SmemTail {
   TileGeom geo;
   // Cluster-pair B encode: the partner's 8 k-slot sums of B_J e per stage and its half maximum;
@@ -688,7 +687,7 @@ struct SmemTail {
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
   // Online verification (check_unit): the staging strip (128 rows x 16 columns), the reference
   // sums, the carried checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
-  double strip[16 * STRIP_LD], colsum[128], rowsum[128], rowpart[2][128], cs_col[128], cs_row[128];
+  double colpart[2][128], rowpart4[4][128], colsum[128], rowsum[128], rowpart[2][128], cs_col[128], cs_row[128];
   double dres[256];
   double red[NTHREADS / 32];
   unsigned int amax_hi, bmax_hi;   // PREPASS: the blocks' whole-k maxima (R1' high words)
@@ -1127,97 +1126,76 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
 }
 
 // Check at the end of an intermediate interval (Kc < k), with the accumulators LIVE in
-// registers (the k-loop continues): they are staged through a 16 KB shared-memory strip, one
-// (b, e) accumulator slot of every thread per round -- a 128-row x 16-column strip of the tile
-// (column stride STRIP_LD) -- and reduced from there, all reads conflict-free: each warp sums
-// 2 strip columns (a half-warp each, 4-level butterflies), thread vt keeps the
-// running sum of row vt & 127 over half of the strip's columns.  Staging only reads the
-// accumulators, so the DMMA k-loop keeps its register allocation (the rounds are a rolled
-// loop; a switch picks the accumulator slot).
+// registers (the k-loop continues): straight from the registers, in two sequential passes with
+// few live temporaries -- column partials one n-tile at a time (over this thread's 8 rows, then
+// a butterfly over the 8 lanes sharing the column), then row partials one m-tile at a time
+// (over its 8 columns, then a butterfly over the 4 lanes sharing the row); the 2 x 4 warp grid's
+// partials meet in shared memory (6 KB; no staging of the tile).  The checksum row / column are
+// excluded by index.  The loop-carried segment state lives in shared memory, so the DMMA k-loop
+// keeps its register allocation (tools/kloop_stats.py).
 template <bool AKM, bool BKM>
 __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, const double (&acc)[8][4][2], int t,
                                                int64_t kt, int mw, int wm, int wn, int lane) {
   const int g = lane >> 2, tq = lane & 3;
   const int vt = mw * 32 + lane;  // 0..255
-  const int cra = tl.geo.cra, crb = tl.geo.crb;
-  const int r = vt & 127, h = vt >> 7;
 #ifdef FTBLAS_DEV
   const long long dv_t0 = clock64();
-  long long dv_t1 = dv_t0, dv_rs = dv_t0, dv_stage = 0, dv_red = 0, dv_sts = 0, dv_col = 0;
 #endif
-  double rsum = 0.0;  // row r over the data columns of strip half h (checksum column crb excluded)
-  // strip column q = wn * 4 + tq holds tile column wn * 32 + tile_row(b, 2 tq + e) in round 2 b + e
-  double *const st = tl.strip + (wn * 4 + tq) * STRIP_LD + wm * 64;
-#pragma unroll 1
-  for (int rd = 0; rd < 8; ++rd) {
-#ifdef FTBLAS_DEV
-    dv_rs = clock64();
-#endif
-    switch (rd) {
-#define FT_STAGE_ROUND(B, E)                                                           \
-  case 2 * B + E:                                                                      \
-    _Pragma("unroll") for (int a = 0; a < 8; ++a) st[tile_row<AKM>(a, g)] = acc[a][B][E]; \
-    break;
-      FT_STAGE_ROUND(0, 0) FT_STAGE_ROUND(0, 1) FT_STAGE_ROUND(1, 0) FT_STAGE_ROUND(1, 1)
-      FT_STAGE_ROUND(2, 0) FT_STAGE_ROUND(2, 1) FT_STAGE_ROUND(3, 0) FT_STAGE_ROUND(3, 1)
-#undef FT_STAGE_ROUND
-    }
-#ifdef FTBLAS_DEV
-    dv_sts += clock64() - dv_rs;
-#endif
-    bar_sync(BAR_PART, 256);
-#ifdef FTBLAS_DEV
-    const long long dv_m = clock64();
-    if (rd == 0) dv_t1 = dv_m;
-    dv_stage += dv_m - dv_rs;
-#endif
-    const int b = rd >> 1, e = rd & 1;
-    auto tcol = [&](int qq) {  // tile column of strip column qq in this round
-      return (qq >> 2) * 32 + (BKM ? tile_row<true>(b, 2 * (qq & 3) + e) : tile_row<false>(b, 2 * (qq & 3) + e));
-    };
-    {  // warp mw: strip columns 2 mw, 2 mw + 1 (one per half-warp)
-      const double c = col_sum_pair(tl.strip + 2 * mw * STRIP_LD, STRIP_LD, lane, cra);
-      const int qq = 2 * mw + (lane >> 4);
-      if ((lane & 15) == 0) {
-        tl.colsum[tcol(qq)] = c;
-        tl.cs_col[tcol(qq)] = tl.strip[qq * STRIP_LD + cra];  // carried (e^T A_I) B_J
-      }
-    }
-#ifdef FTBLAS_DEV
-    const long long dv_c = clock64();
-    dv_col += dv_c - dv_m;
-#endif
-    double rp[2] = {0.0, 0.0};
+  const int cra = tl.geo.cra, crb = tl.geo.crb;
 #pragma unroll
-    for (int qq = 8 * h; qq < 8 * h + 8; ++qq) {
-      const double v = tl.strip[qq * STRIP_LD + r];
-      if (tcol(qq) != crb) rp[qq & 1] += v;
-      else tl.cs_row[r] = v;  // carried A_I (B_J e)
+  for (int b = 0; b < 4; ++b) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = wn * 32 + tile_row<BKM>(b, 2 * tq + e);
+      double c = 0.0;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const double v = acc[a][b][e];
+        if (wm * 64 + tile_row<AKM>(a, g) != cra) c += v;
+        else tl.cs_col[col] = v;  // carried (e^T A_I) B_J
+      }
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (g == 0) tl.colpart[wm][col] = c;
     }
-    rsum += rp[0] + rp[1];
-    bar_sync(BAR_PART, 256);  // the strip is rewritten by the next round
-#ifdef FTBLAS_DEV
-    dv_red += clock64() - dv_m;
-#endif
   }
-  tl.rowpart[h][r] = rsum;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int row = wm * 64 + tile_row<AKM>(a, g);
+    double r = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double v = acc[a][b][e];
+        if (wn * 32 + tile_row<BKM>(b, 2 * tq + e) != crb) r += v;
+        else tl.cs_row[row] = v;  // carried A_I (B_J e)
+      }
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    if (tq == 0) tl.rowpart4[wn][row] = r;
+  }
   bar_sync(BAR_PART, 256);
-  if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
+#ifdef FTBLAS_DEV
+  const long long dv_t1 = clock64();
+#endif
+  if (vt < 128) {
+    tl.colsum[vt] = tl.colpart[0][vt] + tl.colpart[1][vt];
+  } else {
+    const int r = vt - 128;
+    tl.rowsum[r] = (tl.rowpart4[0][r] + tl.rowpart4[1][r]) + (tl.rowpart4[2][r] + tl.rowpart4[3][r]);
+  }
   bar_sync(BAR_PART, 256);
 #ifdef FTBLAS_DEV
   const long long dv_t2 = clock64();
   const CheckOut dv_out = check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
-  if (FT_DEV_PROF(P) && vt == 0) {  // [arrival skew + first staging, reductions], [count, decision]
+  if (FT_DEV_PROF(P) && vt == 0) {  // [arrival + register partials, combine], [count, decision]
     unsigned long long *dp = FT_DEV_PROF(P) + ((size_t)blockIdx.x * 12 + 8) * 2;
     const long long t3 = clock64();
     dp[0] += (unsigned long long)(dv_t1 - dv_t0);
     dp[1] += (unsigned long long)(dv_t2 - dv_t1);
     dp[2] += 1ull;
     dp[3] += (unsigned long long)(t3 - dv_t2);
-    dp[4] += (unsigned long long)dv_stage;
-    dp[5] += (unsigned long long)dv_red;
-    dp[6] += (unsigned long long)dv_sts;
-    dp[7] += (unsigned long long)dv_col;
   }
   return dv_out;
 #else
