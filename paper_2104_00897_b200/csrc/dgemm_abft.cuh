@@ -685,8 +685,8 @@ struct SmemTail {
   uint64_t mfull[STAGES], mfree[STAGES];
   int share;  // this CTA encodes half of B and swaps it with its cluster partner
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
-  // Online verification (check_unit): the staging strip (128 rows x 16 columns), the reference
-  // sums, the carried checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
+  // Online verification (check_unit / check_tile): per-warp partial sums, the reference sums,
+  // the carried checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
   double colpart[2][128], rowpart4[4][128], colsum[128], rowsum[128], rowpart[2][128], cs_col[128], cs_row[128];
   double dres[256];
   double red[NTHREADS / 32];
