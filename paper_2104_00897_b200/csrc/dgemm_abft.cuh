@@ -48,6 +48,7 @@ constexpr int STAGE_ELEMS = 2 * TILE_ELEMS;
 constexpr int STAGE_BYTES = STAGE_ELEMS * 8;
 constexpr int LDC_S = 129;                // epilogue C-tile pitch (doubles)
 constexpr int REG_CS = 152, REG_MMA = 176; // setmaxnreg split: 128*152 + 256*176 = 384*168
+                                           // (protected TT: 128*136 + 256*184, same total)
 static_assert(BM * LDC_S <= STAGES * STAGE_ELEMS, "C tile must fit in the stage ring");
 
 struct FaultDev {        // one armed fault, sorted by (tile, stage)
@@ -1657,10 +1658,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // The two roles never re-converge, so ptxas can give each its own register budget.
   if (is_cs_warp(x.warp)) {
-    setmaxnreg_dec<REG_CS>();
+    // K-major A with MN-major B (TT) needs 8 more registers in the protected DMMA loop.
+    if (FT && AKM && !BKM) setmaxnreg_dec<REG_CS - 16>(); else setmaxnreg_dec<REG_CS>();
     checksum_role<AKM, BKM, FT>(tmA, tmB, P, x);
   } else {
-    setmaxnreg_inc<REG_MMA>();
+    if (FT && AKM && !BKM) setmaxnreg_inc<REG_MMA + 8>(); else setmaxnreg_inc<REG_MMA>();
     mma_role<AKM, BKM, FT>(P, x);
   }
   // A sharing pair stays resident until the partner has made its last remote access.
