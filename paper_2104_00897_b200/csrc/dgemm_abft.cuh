@@ -116,7 +116,7 @@ struct Params {
   unsigned long long *dev_prof;   // per-CTA [warp][wait, work] clock64 sums (null = off)
   int dev_mode;                   // 1 skip pass 2, 2 skip the encode, 4 never flag, 8 MMA waits for
                                   // the TMA bytes only, 16 encoders skip the TMA wait, 32 unprotected
-                                  // kernel on the 127 grid, 128 no clusters
+                                  // kernel on the 127 grid, 128 no clusters, 1024 skip the last check
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
@@ -246,6 +246,18 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
+}
+// Waits of the checksum / producer warps, which run ahead of the MMA warps: poll with a short
+// sleep between tests instead of spinning, so their waiting issues next to nothing on the SM
+// sub-partitions the DMMA warps share (ncu: the spinning producer wait was 18% of the protected
+// kernel's instructions at 8192^3).
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity);
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+#ifdef FTBLAS_DEV
+  mbar_wait(bar, parity);
+#else
+  while (!mbar_test(bar, parity)) __nanosleep(64);
+#endif
 }
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
@@ -761,7 +773,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   // Lane 0: load stage s into its ring slot once the slot's previous stage is consumed.
   auto issue = [&](int s) {
     const int gs = stage_base + s, slot = gs % STAGES;
-    if (gs >= STAGES) mbar_wait(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
+    if (gs >= STAGES) mbar_wait_sleep(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
     double *sa = ring + slot * STAGE_ELEMS;
     mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
     const int k0 = (int)x.k0 + s * BK;
@@ -1462,7 +1474,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         }
     }
     bar_sync(BAR_CTILE, 256);
-    if (verify && failed < 0) {
+    if (verify && failed < 0 && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
       // The last interval, verified before C is written, on the staged tile.
       const CheckOut co = check_tile<AKM, BKM>(P, tl, ctile, P.T - 1, P.k, mw, lane);
       if (co.multi) {

@@ -1,5 +1,6 @@
 """Dev: FT overhead (NN, m x n x k from env M N K, default 8192^3) under FTBLAS_DEV_MODE variants
-(1 skip pass 2, 2 skip encode, 4 never flag, 32 noft on the 127 grid, 128 no clusters)."""
+(1 skip pass 2, 2 skip encode, 4 never flag, 32 noft on the 127 grid, 128 no clusters, 1024 skip
+the last check)."""
 import sys, os, json, subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 code = r'''
@@ -17,7 +18,7 @@ C = torch.zeros(M * N, dtype=torch.float64, device="cuda")
 res = {}
 for name in ["noft", "ft", "noft", "ft"]:
     ts = []
-    for r in range(4):
+    for r in range(int(os.environ.get("REPS", "4"))):
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
         if name == "ft": F.ftblas_dgemm("N", "N", M, N, K, 1.0, A, M, B, K, 0.0, C, M, report=False)
