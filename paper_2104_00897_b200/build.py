@@ -10,6 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libftblas.so")
 LIB_DEV = os.path.join(HERE, "libftblas_dev.so")
+LIB_WATCH = os.path.join(HERE, "libftblas_watch.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
@@ -20,15 +21,19 @@ def sources():
                   + [os.path.join(ROOT, "include", "ftblas.h")])
 
 
-def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, dev: bool = False, watchdog: bool = False) -> str:
     """libftblas.so (release).  dev=True: libftblas_dev.so, the same sources with -DFTBLAS_DEV
-    (the development switches of tools/dev_*.py; never loaded by the product or the tests)."""
-    lib = LIB_DEV if dev else LIB
+    (the development switches of tools/dev_*.py; never loaded by the product or the tests);
+    watchdog=True: libftblas_watch.so, dev + -DFTBLAS_WATCHDOG (mbarrier-wait watchdog of
+    tools/hang_probe.py)."""
+    lib = LIB_WATCH if watchdog else (LIB_DEV if dev else LIB)
+    dev = dev or watchdog
     newest = max(os.path.getmtime(s) for s in sources())
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
         return lib
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *(["-DFTBLAS_DEV"] if dev else []), "-o", lib, os.path.join(CSRC, "ftblas.cu")]
+    flags = (["-DFTBLAS_DEV"] if dev else []) + (["-DFTBLAS_WATCHDOG"] if watchdog else [])
+    cmd = [nvcc, *NVCC_FLAGS, *flags, "-o", lib, os.path.join(CSRC, "ftblas.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

@@ -187,8 +187,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-#ifdef FTBLAS_DEV
-// Development builds: every mbarrier wait has a watchdog that reports (once) a wait that has
+#ifdef FTBLAS_WATCHDOG
+// Watchdog builds (-DFTBLAS_WATCHDOG, tools/hang_probe.py): every mbarrier wait reports (once) a wait that has
 // not completed after ~2^27 polls -- locates a hang instead of timing out silently.
 __device__ __forceinline__ bool mbar_try_u32(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -218,7 +218,7 @@ __device__ __noinline__ void mbar_watchdog(uint32_t bar, uint32_t parity, int wh
 #define FT_WATCH(bar, parity, where) mbar_watchdog((bar), (parity), (where))
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-#ifdef FTBLAS_DEV
+#ifdef FTBLAS_WATCHDOG
   FT_WATCH(static_cast<uint32_t>(__cvta_generic_to_shared(bar)), parity, __LINE__);
   return;
 #endif
@@ -233,7 +233,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-#ifdef FTBLAS_DEV
+#ifdef FTBLAS_WATCHDOG
   FT_WATCH(bar, parity, __LINE__);
   return;
 #endif
@@ -253,7 +253,7 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
 // kernel's instructions at 8192^3).
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-#ifdef FTBLAS_DEV
+#ifdef FTBLAS_WATCHDOG
   mbar_wait(bar, parity);
 #else
   while (!mbar_test(bar, parity)) __nanosleep(64);

@@ -424,10 +424,12 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.correct_mode = tl_correct;
   p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL) ? 1 : 0;  // request; launch_one decides
 #ifdef FTBLAS_DEV
+#ifdef FTBLAS_WATCHDOG
   if (const char *dw = std::getenv("FTBLAS_DEV_WATCH")) {  // hang watchdog slot (tools/hang_probe.py)
     unsigned long long *w = reinterpret_cast<unsigned long long *>(std::strtoull(dw, nullptr, 0));
     CUDA_TRY(cudaMemcpyToSymbol(ftk::g_dev_watch, &w, sizeof w));
   }
+#endif
   // development build only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
   p.dev_mode = dev_mode;
