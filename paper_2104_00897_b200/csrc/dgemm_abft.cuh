@@ -890,7 +890,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
         };
         if (pubs && doB && b_sub) fetch_b();
-        if (!(FT_DEV_MODE(P) & 16)) mbar_wait(&tl.full[slot], (gs / STAGES) & 1);
+        if (!(FT_DEV_MODE(P) & 16)) mbar_wait_sleep(&tl.full[slot], (gs / STAGES) & 1);
         if (pubs && doA) check_a(s, pa);
         bool bcopy = false;
         if (pubs && doB && b_sub) {

@@ -15,6 +15,7 @@ g = torch.Generator(device="cuda").manual_seed(0)
 A = torch.rand(M * K, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
 B = torch.rand(K * N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
 C = torch.zeros(M * N, dtype=torch.float64, device="cuda")
+F.ftblas_set_encode(int(os.environ.get("ENC", "0")))
 res = {}
 for name in ["noft", "ft", "noft", "ft"]:
     ts = []
@@ -26,7 +27,7 @@ for name in ["noft", "ft", "noft", "ft"]:
         e1.record(); torch.cuda.synchronize()
         if r: ts.append(e0.elapsed_time(e1))
     res[name] = min(ts)
-print(json.dumps({"mode": os.environ.get("FTBLAS_DEV_MODE", "0"), "MNK": [M, N, K], "noft_ms": res["noft"], "ft_ms": res["ft"],
+print(json.dumps({"mode": os.environ.get("FTBLAS_DEV_MODE", "0"), "enc": os.environ.get("ENC", "0"), "MNK": [M, N, K], "noft_ms": res["noft"], "ft_ms": res["ft"],
                   "overhead_pct": 100 * (res["ft"] - res["noft"]) / res["noft"]}), flush=True)
 ''' % ROOT
 for mode in (sys.argv[1:] or ["0", "5", "6"]):
