@@ -116,7 +116,8 @@ struct Params {
   unsigned long long *dev_prof;   // per-CTA [warp][wait, work] clock64 sums (null = off)
   int dev_mode;                   // 1 skip pass 2, 2 skip the encode, 4 never flag, 8 MMA waits for
                                   // the TMA bytes only, 16 encoders skip the TMA wait, 32 unprotected
-                                  // kernel on the 127 grid, 128 no clusters, 1024 skip the last check
+                                  // kernel on the 127 grid, 128 no clusters, 1024 skip the last check,
+                                  // 2048 no proxy fence, 4096 no interval maxima (timing only)
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
@@ -979,12 +980,12 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           }
          }
         }
-        if (!P.Ac && lane == 0) {  // the interval's maxima, read by the MMA warps at its check
+        if (!P.Ac && lane == 0 && !(FT_DEV_MODE(P) & 4096)) {  // the interval's maxima, read by the MMA warps at its check
           const int tint = min(s / KcS, P.T - 1) & 7;
           if (doA) atomicMax(&tl.int_am[tint], amax_hi);
           if (doB) atomicMax(&tl.int_bm[tint], bmax_hi);
         }
-        fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
+        if (!(FT_DEV_MODE(P) & 2048)) fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
         __syncwarp();
         if (lane == 0) {  // one arrival per operand job (the barrier expects two per stage)
           mbar_arrive(&tl.enc[slot]);
