@@ -875,8 +875,6 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       if (split && s >= N_ENC_WARPS) { split = false; s = warp + N_ENC_WARPS; }
       if (s >= nk) break;
       const bool doA = !split || ((((s >> 1) & 1) == 0) == (warp < 2));
-      // this warp still has to send the TMA loads of its next stage s + 4 (slot of s - 2)
-      bool early_pending = (s & 3) == warp && s + N_ENC_WARPS >= STAGES && s + N_ENC_WARPS < nk;
       const bool doB = !split || !doA;
       if (verify) {
         const int gs = stage_base + s, slot = gs % STAGES;
@@ -893,24 +891,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
         };
         if (pubs && doB && b_sub) fetch_b();
-        // Wait for this stage's bytes -- and meanwhile send the TMA loads of this warp's next
-        // stage (s + 4) as soon as its ring slot is free: its issue must not wait for this
-        // stage's data, or each warp would keep only one stage in flight (the unprotected
-        // producer keeps all 6).
-        if (!(FT_DEV_MODE(P) & 16)) {
-          while (!mbar_test(&tl.full[slot], (gs / STAGES) & 1)) {
-            if (early_pending) {
-              const int gs2 = stage_base + s + N_ENC_WARPS;
-              if (mbar_test(&tl.empty[gs2 % STAGES], ((gs2 / STAGES) - 1) & 1)) {
-                if (lane == 0) issue(s + N_ENC_WARPS);  // the slot is free: no wait inside
-                early_pending = false;
-                __syncwarp();
-                continue;
-              }
-            }
-            __nanosleep(32);
-          }
-        }
+        if (!(FT_DEV_MODE(P) & 16)) mbar_wait_sleep(&tl.full[slot], (gs / STAGES) & 1);
         if (pubs && doA) check_a(s, pa);
         bool bcopy = false;
         if (pubs && doB && b_sub) {
@@ -1018,7 +999,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         }
       }
       const int s2 = s + N_ENC_WARPS;  // the next stage of this warp's TMA ring slots
-      if (early_pending && lane == 0) issue(s2);
+      if (lane == 0 && (s & 3) == warp && s2 >= STAGES && s2 < nk) issue(s2);
       __syncwarp();
     }
     stage_base += nk;
