@@ -21,15 +21,21 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ftblas_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# ORACLE_SANITIZE=1 (tests/test_sanitize.py): the same source under AddressSanitizer and
+# UndefinedBehaviorSanitizer, errors fatal; the process must preload libasan.
+_SANITIZE = os.environ.get("ORACLE_SANITIZE") == "1"
+_LIB = os.path.join(_HERE, "liboracle_san.so" if _SANITIZE else "liboracle.so")
 
 CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+SAN_CFLAGS = ["-g", "-fsanitize=address", "-fsanitize=undefined", "-fno-sanitize-recover=all",
+              "-fno-omit-frame-pointer"]
 
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no -ffast-math, no FP contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+        extra = SAN_CFLAGS if _SANITIZE else []
+        subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 

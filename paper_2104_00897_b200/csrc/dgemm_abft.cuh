@@ -135,6 +135,25 @@ struct Params {
 #define FT_DEV_PROF(P) ((unsigned long long *)nullptr)
 #endif
 
+// Bounds / invariant assertions of the checked build (-DFTBLAS_CHECKED, libftblas_checked.so,
+// the stand-in for compute-sanitizer, which this pool does not run): a failed check prints its
+// site and traps, so the test that reached it fails with a sticky launch error.  Compiled out of
+// libftblas.so.
+#ifdef FTBLAS_CHECKED
+#define FT_CHECK(cond)                                                                       \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("FT_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,  \
+             (int)blockIdx.x, (int)threadIdx.x);                                             \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define FT_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -842,6 +861,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       const int p = AKM ? 2 * lane : lane;
       const int64_t pg = x.k0 + (int64_t)s * BK + p;
       double *dst = P.Ash + x.ti * P.ldash + pg;
+      FT_CHECK(x.ti < P.tiles_m && sg < P.nk && (pg >= x.k1 || pg + (AKM ? 1 : 0) < P.ldash));
       if (AKM) {
         if (lane < 8 && pg < x.k1) st_relaxed_gpu(dst, a0);
         if (lane < 8 && pg + 1 < x.k1) st_relaxed_gpu(dst + 1, a1);
@@ -974,6 +994,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
             if (b_pub) {  // tile row 0: publish this stage's B_J e for the other tile rows
               __syncwarp();
               const int64_t pg = x.k0 + (int64_t)s * BK + lane;
+              FT_CHECK(x.tj < P.tiles_n && sg < P.nk && (pg >= x.k1 || pg < P.ldbsh));
               if (lane < 16 && pg < x.k1) st_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg, sB[sidx<BKM>(x.crb, lane)]);
               if (lane == 0) st_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + sg, hmb);
             }
@@ -1129,6 +1150,7 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
     atomicAdd(&P.counters[CNT_DETECTED], 1ull);
     atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
     const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
+    FT_CHECK(fr >= 0 && fr < 128 && fc >= 0 && fc < 128);
     if ((long long)slot < P.ev_cap)
       P.events[slot] = multi ? EventDev{(long long)(x.i0 + P.ev_row_off), (long long)(x.j0 + P.ev_col_off), 2, t,
                                         nfr ? tl.dres[128 + fr] : 0.0, nfc ? tl.dres[fc] : 0.0}
@@ -1423,7 +1445,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
           pend_si = -1;
         } else if (s == ld_sv(ws, W_NEXT_STAGE)) {
           const int fnext = ld_sv(ws, W_FNEXT);
+          FT_CHECK(fnext >= x.f_lo && fnext < x.f_hi && x.f_hi <= P.nfaults);
           const FaultDev f = P.faults[fnext];
+          FT_CHECK(f.tile == x.tile && f.li < 127 && f.lj < 127 && f.li >= -1 && f.lj >= -1);
           // a fault belongs to interval min(stage / KcS, T - 1); a retry skips the decided ones
           if (min(f.stage / max(1, (int)(P.Kc / BK)), P.T - 1) > tl.retry) {
             const TileGeom gf = load_geom(tl.geo);
@@ -1510,6 +1534,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     for (int q = 0; q < nfix; ++q) {
       const int si = tl.fix[q] & 255, sj = tl.fix[q] >> 8;
       const int64_t gi = ge.i0 + si - ge.oa, gj = ge.j0 + sj - ge.ob;
+      FT_CHECK(nfix <= MAX_FIX && gi >= ge.i0 && gi < ge.i0 + ge.bm_eff && gj >= ge.j0 && gj < ge.j0 + ge.bn_eff);
       double part = 0.0;
       for (int64_t p = vt; p < P.k; p += 256) {
         const double av = AKM ? P.A[p + gi * P.lda] : P.A[gi + p * P.lda];
@@ -1532,6 +1557,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   const int i = vt & 127;
   const double alpha = P.alpha, beta = P.beta;
   if (i < ge.bm_eff) {
+    FT_CHECK(ge.i0 + i < P.m && ge.j0 + ge.bn_eff <= P.n && i + ge.oa < 128 && ge.bn_eff + ge.ob <= 128);
     double *crow = P.C + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
 #pragma unroll 4
     for (int j = vt >> 7; j < ge.bn_eff; j += 2) {

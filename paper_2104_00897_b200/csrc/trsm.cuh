@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) trsm_leaf_kernel(const LeafParam
   extern __shared__ double sm[];
   double *Sc = sm, *rd1 = sm + LEAF * LEAF, *rd2 = rd1 + LEAF;
   const int nb = P.nb, tid = threadIdx.x, lane = tid & 31, nslots = (nb + 31) >> 5;
+  FT_CHECK(nb >= 1 && nb <= LEAF && (LEAF_THREADS & 31) == 0);
   for (int e = tid; e < LEAF * LEAF; e += blockDim.x) {
     const int i = e / LEAF, p = e % LEAF;
     Sc[e] = p < nb && i < nb ? leaf_a(P, p, i) : (p == i ? 1.0 : 0.0);
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) trsm_leaf_kernel(const LeafParam
         if (cc >= 0 && cc < NCOL && (int)(code % LEAF) % 32 == lane)
 #pragma unroll
           for (int c = 0; c < NCOL; ++c)
-            if (c == cc) { fi[c] = (int)(code % LEAF); fstep[c] = (int)P.f[e].step; fdel[c] = P.f[e].delta; }
+            if (c == cc) { FT_CHECK(code % LEAF < nb); fi[c] = (int)(code % LEAF); fstep[c] = (int)P.f[e].step; fdel[c] = P.f[e].delta; }
       }
     double b[NCH][4];
 #pragma unroll

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(256) verify_kernel(const VerifyParams P) {
   const bool multi = !(nfr == 1 && nfc == 1);
   const int fr = first_row, fc = first_col;
   if (!multi) {
+    FT_CHECK(fr < bm && fc < bn);
     const int64_t gi = i0 + fr, gj = j0 + fc;
     double *tij = P.T + gi + gj * P.ldt;
     if (P.correct_mode == 1) {

@@ -13,6 +13,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+def pytest_sessionstart(session):
+    # FTBLAS_TEST_LIB: run the suite on another build of the same ABI -- libftblas_checked.so
+    # (device bounds assertions, host ASan/UBSan; tests/test_sanitize.py, tools/gpu_checked.sh).
+    lib = os.environ.get("FTBLAS_TEST_LIB")
+    if lib:
+        from paper_2104_00897_b200 import ftblas
+        ftblas.load(os.path.join(ROOT, "paper_2104_00897_b200", lib))
+
+
 def pytest_collection_modifyitems(config, items):
     try:
         import torch
