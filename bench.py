@@ -287,9 +287,10 @@ def oracle_parity(W, torch, A_dev, B_dev, C_dev, rep, BM, BN, BK, units_wanted, 
 
 
 # ------------------------------------------------------------------ per-config lines (N = 1)
-def per_config_runs(torch, F, stream, dev, seed, steps=8, warmup=2):
-    """Short interleaved protected / unprotected runs of the other BASELINE configs; each pair
-    is timed with its own CUDA events.  The protected call carries its report (a host
+def per_config_runs(torch, F, stream, dev, seed, steps=8, warmup=1, reps=3):
+    """Short interleaved protected / unprotected runs of the other BASELINE configs: per kind,
+    blocks of `steps` back-to-back calls timed with CUDA events, the kinds interleaved block by
+    block, the median block reported.  The protected call carries its report (a host
     synchronisation per call); `async_tflops` is the protected call without a report."""
     out = {}
     for cfg in ("C1", "C2", "C3", "C3NT", "C3TN", "C3TT", "C4a", "C4b"):
@@ -312,18 +313,22 @@ def per_config_runs(torch, F, stream, dev, seed, steps=8, warmup=2):
             return F.ftblas_dgemm(ta, tb, m, n, k, W["alpha"], A, lda, B, ldb, W["beta"], C, m,
                                   report=(kind == "ft"))
 
+        # Blocks of `steps` back-to-back calls per kind, the kinds interleaved block by block
+        # (a call's host-side issue overlaps the previous call's kernel, as in a loop of calls;
+        # the protected call with its report synchronises inside every call).
         times = {"ft": [], "noft": [], "async": []}
         rep = None
-        for it in range(warmup + steps):
+        for it in range(warmup + reps):
             for kind in ("ft", "noft", "async"):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
                 e0.record(stream)
-                r = call(kind)
+                for _ in range(steps):
+                    r = call(kind)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 if it >= warmup:
-                    times[kind].append(e0.elapsed_time(e1))
+                    times[kind].append(e0.elapsed_time(e1) / steps)
                 if r is not None:
                     rep = r
         Aop = A.view(k, m).t() if ta == "N" else A.view(m, k)
@@ -344,7 +349,7 @@ def per_config_runs(torch, F, stream, dev, seed, steps=8, warmup=2):
                     "async_tflops": fl / t_as / 1e9, "async_overhead_pct": 100.0 * (t_as - t_no) / t_no,
                     "cublas_tflops": fl / min(cb) / 1e9, "ms": {"protected": t_ft, "unprotected": t_no},
                     "detected": rep.detected, "corrected": rep.corrected, "recomputed": rep.recomputed,
-                    "pairs": steps}
+                    "calls_per_block": steps, "blocks": reps}
         del A, B, C, C0
         torch.cuda.empty_cache()
     return out

@@ -1,32 +1,28 @@
 // dgemm_abft.cuh — sm_100a kernel of the online ABFT DGEMM (FT-BLAS, arXiv 2104.00897).
 //
-// One CTA computes one BM x BN = 128 x 128 tile of C = alpha*op(A)*op(B) + beta*C; the tile
-// is one verification unit (§II.A restricted to the tile; R5).
+// One CTA computes one BM x BN = 128 x 128 MMA tile of C = alpha*op(A)*op(B) + beta*C.  In the
+// protected kernel the tile is the unit's full checksum block C^f = [A_I; e^T A_I][B_J, B_J e]
+// restricted to 127 x 127 data rows / columns: staged row cra holds e^T A_I,
+// staged column crb holds B_J e, so the DMMA stream that forms C also carries the checksums
+// (outer-product maintenance) and the unit is 127 x 127 (R16).
 //
 // Warp-specialised (384 threads = 3 warpgroups):
-//   warpgroup 0  (warps 0-3, 152 registers): "checksum warps".  Warp 0 lane 0 is also the
-//                TMA producer: it streams the BK = 16 deep A and B tiles of every stage into
-//                a 5-deep shared-memory ring (cp.async.bulk.tensor, 128-byte swizzle,
-//                mbarrier complete_tx).  In the protected kernel each checksum warp c owns
-//                k-slots p = 4c..4c+3 of every stage and, from the SAME staged tiles the MMA
-//                reads ("each B element reused three times", §V.B):
-//                  encode  a_sum[p] = sum_{i in I} op(A)_ip,  b_sum[p] = sum_{j in J} op(B)_pj
-//                          (e^T A, B e) and the running max|op(A)_I|, max|op(B)_J|
-//                  carry   cs_col[j] += a_sum[p] op(B)_pj,  cs_row[i] += op(A)_ip b_sum[p]
-//                          (outer-product maintenance)
-//   warpgroups 1-2 (warps 4-11, 176 registers): 8 MMA warps in a 2 x 4 grid of 64 x 32 warp
-//                tiles; acc += A_tile*B_tile with DMMA.8x8x4 (mma.sync m8n8k4 f64 — the only
-//                FP64 tensor instruction of sm_100a; tcgen05 has no f64 kind).  They also host
-//                the fault-injection hook (a delta added to the owning accumulator when the
-//                k-loop reaches the fault's quantised step).
-//   Every consumer warp waits on the stage's full barrier and arrives on its empty barrier:
-//   no CTA-wide barrier inside the k-loop, so warps drift and hide each other's latency.
-//
-// Epilogue (all warps): stage the accumulator through shared memory; reference checksums
-// r_col = e^T C_IJ, r_row = C_IJ e from the computed C; residuals
-// d = r - cs; flag where not |d| <= tau (R1); exactly one flagged row and column
-// -> locate and correct in place; any other pattern -> recompute the
-// tile once (R6).  Store C = alpha*acc + beta*C0 (C0 not read when beta == 0).
+//   warps 0-7 (176 registers): MMA warps in a 2 x 4 grid of 64 x 32 warp tiles, acc += A*B
+//                with DMMA.8x8x4 (mma.sync m8n8k4 f64 -- the only FP64 tensor instruction of
+//                sm_100a; tcgen05 has no f64 kind); the fault hook between fault-free k-loop
+//                segments; the online verification from the live accumulators at every
+//                interval end (reference sums e^T C and C e, residuals against
+//                the carried checksums, tau, locate / correct / recompute) and the epilogue.
+//   warps 8-11 (152 registers): encoder warps.  Warp w issues the TMA loads of stages
+//                s = w (mod 4) into a 6-deep shared-memory ring (cp.async.bulk.tensor, 128-byte
+//                swizzle, mbarrier complete_tx) and, in the protected kernel, writes the stage's
+//                16 k-slots of e^T A_I and B_J e into the staged checksum row / column: copied
+//                from the tile that published them through L2, or encoded from the staged tile
+//                (integer fixed point, R17, R22).
+//   No CTA-wide barrier inside the k-loop: MMA warps wait on a stage's `enc` (protected) or
+//   `full` (unprotected) mbarrier and arrive on its `empty` one.
+// k-split (launches of <= 18 tiles, Kc = k): each tile runs as several CTAs over contiguous
+// k ranges; the last to finish sums the partial C^f blocks in split order, verifies and stores.
 #pragma once
 #include <cstdint>
 #include <cstdio>
@@ -84,6 +80,15 @@ struct Params {
   // tile column, so they stage the same B_J: each encodes half of its 16 k-slots and the pair
   // swaps halves through distributed shared memory.  `total` = real CTAs of this launch.
   int cluster2, total;
+  // k-split of a launch with few tiles (Kc = k only): CTA b runs split q = b % ksplit of tile
+  // b / ksplit -- stages [q nk / ksplit, (q+1) nk / ksplit) -- and writes its partial C^f
+  // block (data and carried checksums) to part[(tile * ksplit + q) * 16384 + idx * 256 + thread]
+  // and its stage maxima to part_max; the last split of a tile to finish (ticket) sums the
+  // partials in split order (deterministic), verifies the whole C^f block and stores the tile.
+  int ksplit;
+  double *part;
+  unsigned *part_max;
+  int *tickets;  // per tile, zeroed by the host
   const FaultDev *faults;
   int nfaults;
   int correct_mode;               // 0 recompute, 1 subtract
@@ -117,7 +122,8 @@ struct Params {
   int dev_mode;                   // 1 skip pass 2, 2 skip the encode, 4 never flag, 8 MMA waits for
                                   // the TMA bytes only, 16 encoders skip the TMA wait, 32 unprotected
                                   // kernel on the 127 grid, 128 no clusters, 1024 skip the last check,
-                                  // 2048 no proxy fence, 4096 no interval maxima (timing only)
+                                  // 2048 no proxy fence before slot refills, 4096 no interval maxima
+                                  // (timing only)
   unsigned long long *counters;   // [CNT_N]
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
@@ -718,9 +724,9 @@ struct SmemTail {
   uint64_t mfull[STAGES], mfree[STAGES];
   int share;  // this CTA encodes half of B and swaps it with its cluster partner
   uint64_t full[STAGES], enc[STAGES], empty[STAGES];
-  // Online verification (check_unit / check_tile): per-warp partial sums, the reference sums,
-  // the carried checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
-  double colpart[2][128], rowpart4[4][128], colsum[128], rowsum[128], rowpart[2][128], cs_col[128], cs_row[128];
+  // Online verification (check_unit): per-warp partial sums, the reference sums, the carried
+  // checksums, residuals (0..127 columns, 128..255 rows), dot-product partials.
+  double colpart[2][128], rowpart4[4][128], colsum[128], rowsum[128], cs_col[128], cs_row[128];
   double dres[256];
   double red[NTHREADS / 32];
   unsigned int amax_hi, bmax_hi;   // PREPASS: the blocks' whole-k maxima (R1' high words)
@@ -730,6 +736,7 @@ struct SmemTail {
   int nfix, fix[MAX_FIX];          // corrected cells (staged row | col << 8) to recompute (R4)
   int wstate[N_MMA_WARPS][8];      // per MMA warp: segment state of the k-loop (mma_role)
   int retry;                       // -1: done; else the interval whose check asked for a recompute
+  int ticket;                      // k-split: arrival order of this split among the tile's splits
 };
 constexpr size_t SMEM_BYTES = 1024 + sizeof(double) * STAGES * STAGE_ELEMS + sizeof(SmemTail);
 
@@ -762,6 +769,8 @@ struct Ctx {
   SmemTail *tl;
   int tid, lane, warp, tile, ti, tj, i0, j0, bm_eff, bn_eff, nk, f_lo, f_hi;
   int64_t k0, k1;
+  int q, s0, nk_all;  // k-split: this CTA's split and its first global stage; stages of all of k
+  int tile_slot;      // the tile's index in launch order (its k-split partials / ticket)
   // Protected tiles: TMA boxes start at the even coordinate xs = x0 - (x0 & 1) (the contiguous
   // dimension of a TMA box must start 16-byte aligned), so tile-local data row i sits in
   // staged row i + o (o = x0 & 1) and the checksum row/column takes the free row cr.
@@ -787,28 +796,37 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
                                               const Ctx &x) {
   SmemTail &tl = *x.tl;
   double *const ring = x.ring;
-  const int lane = x.lane, warp = cs_warp(x.warp), nk = x.nk;
+  const int lane = x.lane, warp = cs_warp(x.warp);
+  // The attempt's k range: this CTA's split first; a recompute (R6) covers the whole k.
+  int nk = x.nk;
+  int64_t k0 = x.k0, k1 = x.k1;
   const int xa = x.i0 - x.oa, xbj = x.j0 - x.ob;  // even box origins
   int stage_base = 0;
   // Lane 0: load stage s into its ring slot once the slot's previous stage is consumed.
   auto issue = [&](int s) {
     const int gs = stage_base + s, slot = gs % STAGES;
-    if (gs >= STAGES) mbar_wait_sleep(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
+    if (gs >= STAGES) {
+      mbar_wait_sleep(&tl.empty[slot], ((gs / STAGES) - 1) & 1);
+      // The slot's checksum row / column was written through the generic proxy (encoder warps,
+      // acquired here through enc -> MMA warps -> empty); order it before TMA (async proxy)
+      // refills the slot.  Issued here, off the path of the stage the MMA warps wait for.
+      if (FT && !(FT_DEV_MODE(P) & 2048)) fence_proxy_async();
+    }
     double *sa = ring + slot * STAGE_ELEMS;
     mbar_arrive_expect_tx(&tl.full[slot], STAGE_BYTES);
-    const int k0 = (int)x.k0 + s * BK;
+    const int kc = (int)k0 + s * BK;
     if (AKM) {
-      tma_load_2d(sa, &tmA, k0, xa, &tl.full[slot]);
+      tma_load_2d(sa, &tmA, kc, xa, &tl.full[slot]);
     } else {
 #pragma unroll
-      for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, k0, &tl.full[slot]);
+      for (int xb = 0; xb < 8; ++xb) tma_load_2d(sa + xb * 256, &tmA, xa + 16 * xb, kc, &tl.full[slot]);
     }
     double *sb = sa + TILE_ELEMS;
     if (BKM) {
-      tma_load_2d(sb, &tmB, k0, xbj, &tl.full[slot]);
+      tma_load_2d(sb, &tmB, kc, xbj, &tl.full[slot]);
     } else {
 #pragma unroll
-      for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, k0, &tl.full[slot]);
+      for (int xb = 0; xb < 8; ++xb) tma_load_2d(sb + xb * 256, &tmB, xbj + 16 * xb, kc, &tl.full[slot]);
     }
   };
   const uint32_t rank = P.cluster2 ? cluster_rank() : 0u;
@@ -823,15 +841,15 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   auto fetch_a = [&](int s) {
     PubA f{false, 0.0, 0.0, 0xFFFFFFFFu};
     if (!a_sub) return f;
-    const int64_t sg = x.k0 / BK + s;  // global stage index
+    const int64_t sg = k0 / BK + s;  // global stage index
     const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
-    const int64_t pg = x.k0 + (int64_t)s * BK + p;
+    const int64_t pg = k0 + (int64_t)s * BK + p;
     const double *src = P.Ash + x.ti * P.ldash + pg;
     if (AKM) {
-      f.a0 = lane < 8 && pg < x.k1 ? ld_relaxed_gpu(src) : 0.0;
-      f.a1 = lane < 8 && pg + 1 < x.k1 ? ld_relaxed_gpu(src + 1) : 0.0;
+      f.a0 = lane < 8 && pg < k1 ? ld_relaxed_gpu(src) : 0.0;
+      f.a1 = lane < 8 && pg + 1 < k1 ? ld_relaxed_gpu(src + 1) : 0.0;
     } else {
-      f.a0 = lane < 16 && pg < x.k1 ? ld_relaxed_gpu(src) : 0.0;
+      f.a0 = lane < 16 && pg < k1 ? ld_relaxed_gpu(src) : 0.0;
     }
     f.am = ld_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg);
     return f;
@@ -857,15 +875,15 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     enc_operand<AKM>(sA, lane, x.cra, a0, a1, hm);
     amax = max(amax, hm);
     if (a_pub) {
-      const int64_t sg = x.k0 / BK + s;
+      const int64_t sg = k0 / BK + s;
       const int p = AKM ? 2 * lane : lane;
-      const int64_t pg = x.k0 + (int64_t)s * BK + p;
+      const int64_t pg = k0 + (int64_t)s * BK + p;
       double *dst = P.Ash + x.ti * P.ldash + pg;
-      FT_CHECK(x.ti < P.tiles_m && sg < P.nk && (pg >= x.k1 || pg + (AKM ? 1 : 0) < P.ldash));
+      FT_CHECK(x.ti < P.tiles_m && sg < P.nk && (pg >= k1 || pg + (AKM ? 1 : 0) < P.ldash));
       if (AKM) {
-        if (lane < 8 && pg < x.k1) st_relaxed_gpu(dst, a0);
-        if (lane < 8 && pg + 1 < x.k1) st_relaxed_gpu(dst + 1, a1);
-      } else if (lane < 16 && pg < x.k1) {
+        if (lane < 8 && pg < k1) st_relaxed_gpu(dst, a0);
+        if (lane < 8 && pg + 1 < k1) st_relaxed_gpu(dst + 1, a1);
+      } else if (lane < 16 && pg < k1) {
         st_relaxed_gpu(dst, a0);
       }
       if (lane == 0) st_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg, hm);
@@ -906,9 +924,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         double pb = 0.0;
         uint32_t pbm = 0xFFFFFFFFu;
         auto fetch_b = [&]() {
-          const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-          pb = lane < 16 && pg < x.k1 ? ld_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
-          pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (x.k0 / BK + s));
+          const int64_t pg = k0 + (int64_t)s * BK + lane;
+          pb = lane < 16 && pg < k1 ? ld_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
+          pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (k0 / BK + s));
         };
         if (pubs && doB && b_sub) fetch_b();
         if (!(FT_DEV_MODE(P) & 16)) mbar_wait_sleep(&tl.full[slot], (gs / STAGES) & 1);
@@ -926,10 +944,10 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         double *sA = ring + slot * STAGE_ELEMS, *sB = sA + TILE_ELEMS;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
         if (P.Ac) {  // PREPASS: copy the pre-encoded 16 k-slots of e^T A_I / B_J e
-          const int64_t p = x.k0 + s * BK + lane;
+          const int64_t p = k0 + s * BK + lane;
           if (lane < 16) {
-            if (doA) sA[sidx<AKM>(x.cra, lane)] = p < x.k1 ? P.Ac[x.ti + p * P.ldac] : 0.0;
-            if (doB) sB[sidx<BKM>(x.crb, lane)] = p < x.k1 ? P.Br[x.tj + p * P.ldbr] : 0.0;
+            if (doA) sA[sidx<AKM>(x.cra, lane)] = p < k1 ? P.Ac[x.ti + p * P.ldac] : 0.0;
+            if (doB) sB[sidx<BKM>(x.crb, lane)] = p < k1 ? P.Br[x.tj + p * P.ldbr] : 0.0;
           }
         } else if (FT_DEV_MODE(P) & 1) {  // development: pass 1 only
           if (doA) amax_hi = max(amax_hi, (uint32_t)__float_as_int(warp_max_nan(enc_pass1<AKM>(sA, lane, x.cra))));
@@ -946,7 +964,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           }
          }
          if (doB) {
-          const int64_t sg = x.k0 / BK + s;  // global stage index
+          const int64_t sg = k0 / BK + s;  // global stage index
           if (bcopy) {  // B_J e of this stage as published by tile row 0
             if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pb;
             bmax_hi = max(bmax_hi, pbm);
@@ -993,9 +1011,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
             bmax_hi = max(bmax_hi, hmb);
             if (b_pub) {  // tile row 0: publish this stage's B_J e for the other tile rows
               __syncwarp();
-              const int64_t pg = x.k0 + (int64_t)s * BK + lane;
-              FT_CHECK(x.tj < P.tiles_n && sg < P.nk && (pg >= x.k1 || pg < P.ldbsh));
-              if (lane < 16 && pg < x.k1) st_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg, sB[sidx<BKM>(x.crb, lane)]);
+              const int64_t pg = k0 + (int64_t)s * BK + lane;
+              FT_CHECK(x.tj < P.tiles_n && sg < P.nk && (pg >= k1 || pg < P.ldbsh));
+              if (lane < 16 && pg < k1) st_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg, sB[sidx<BKM>(x.crb, lane)]);
               if (lane == 0) st_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + sg, hmb);
             }
           }
@@ -1006,7 +1024,6 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           if (doA) atomicMax(&tl.int_am[tint], amax_hi);
           if (doB) atomicMax(&tl.int_bm[tint], bmax_hi);
         }
-        if (!(FT_DEV_MODE(P) & 2048)) fence_proxy_async();  // generic writes into a TMA-filled buffer that TMA will refill
         __syncwarp();
         if (lane == 0) {  // one arrival per operand job (the barrier expects two per stage)
           mbar_arrive(&tl.enc[slot]);
@@ -1030,6 +1047,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     const int r = tl.retry;
     if (r < 0) return;
     t_done = r;
+    nk = x.nk_all;  // a recompute covers the whole k (a k-split tile is recomputed unsplit)
+    k0 = 0;
+    k1 = P.k;
   }
 }
 
@@ -1072,22 +1092,6 @@ struct CheckOut {
   int si, sj;   // single error: the located staged cell (si = -1: none)
   double dcol;  // the located magnitude d_col to subtract from it
 };
-
-// Reference sums e^T C_IJ of two staged columns per warp: half-warp hw = lane >> 4 takes column
-// c0 + hw (stride ld), its lanes rows (lane & 15) + 16 q (consecutive rows: conflict-free), the
-// checksum row excluded; then a 4-level butterfly inside each half.  Lanes 0 and 16 return the
-// two sums.
-__device__ __forceinline__ double col_sum_pair(const double *col0, int ld, int lane, int cra) {
-  const double *col = col0 + (lane >> 4) * ld;
-  const int r0 = lane & 15;
-  double v[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = (r0 + 16 * q == cra) ? 0.0 : col[r0 + 16 * q];
-  double c = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  return c;
-}
 
 // Residuals, threshold, flags, classification and report of one unit at the end of
 // interval t, from the reference sums (tl.colsum, tl.rowsum) and the carried checksums
@@ -1239,36 +1243,6 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
 #endif
 }
 
-// The last interval's check, on the accumulators staged in shared memory for the epilogue
-// (ctile, pitch LDC_S): the accumulators are dead in registers, so it reads the whole tile in
-// one pass -- warp mw sums tile columns 16 mw .. 16 mw + 15 (two per pass, half-warp butterflies),
-// thread vt sums row vt & 127 over one half of the columns.
-template <bool AKM, bool BKM>
-__device__ __forceinline__ CheckOut check_tile(const Params &P, SmemTail &tl, const double *ctile, int t, int64_t kt,
-                                               int mw, int lane) {
-  const int vt = mw * 32 + lane;
-  const int cra = tl.geo.cra, crb = tl.geo.crb;
-#pragma unroll 2
-  for (int c = 16 * mw; c < 16 * mw + 16; c += 2) {  // two columns per pass, one per half-warp
-    const double s = col_sum_pair(ctile + c * LDC_S, LDC_S, lane, cra);
-    if ((lane & 15) == 0) {
-      const int cc = c + (lane >> 4);
-      tl.colsum[cc] = s;
-      tl.cs_col[cc] = ctile[cc * LDC_S + cra];  // carried (e^T A_I) B_J
-    }
-  }
-  const int r = vt & 127, h = vt >> 7;
-  double rp[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 16
-  for (int c = 64 * h; c < 64 * h + 64; ++c) rp[c & 3] += (c == crb) ? 0.0 : ctile[c * LDC_S + r];
-  tl.rowpart[h][r] = (rp[0] + rp[1]) + (rp[2] + rp[3]);
-  if (h == 0) tl.cs_row[r] = ctile[crb * LDC_S + r];  // carried A_I (B_J e)
-  bar_sync(BAR_PART, 256);
-  if (vt < 128) tl.rowsum[vt] = tl.rowpart[0][vt] + tl.rowpart[1][vt];
-  bar_sync(BAR_PART, 256);
-  return check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
-}
-
 // The DMMA k-loop of a sliver tile's warp over its first NA m-tiles and NB n-tiles only.
 template <bool AKM, bool BKM, int NA, int NB>
 __device__ __forceinline__ void kloop_narrow(SmemTail &tl, const double *ring, uint32_t ready, int &gs, int gs_end,
@@ -1300,7 +1274,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   SmemTail &tl = *x.tl;
   double *const ring = x.ring;
   double *const ctile = ring;  // epilogue reuse of the ring
-  const int lane = x.lane, nk = x.nk;
+  const int lane = x.lane;
   // Warp w runs on SM sub-partition w & 3.  The 64 x 32 quarter (wm, wn) of warp w has
   // wn = (w + 2 wm) & 3, so each warp row spans all four sub-partitions and the two warps of a
   // warp column sit on different ones (a partial edge tile's active warps share the DMMA pipes
@@ -1330,21 +1304,40 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   // next fault index, the interval of a recompute decision in this attempt.
   // (32-bit shared addresses through volatile ld/st.shared: no generic pointer held in registers)
   const uint32_t ws = smem_u32(&tl.wstate[mw][0]);
-  enum { W_NEXT_STAGE = 0, W_NEXT_CHECK, W_FNEXT, W_FAILED, W_BASE, W_NARROW };
+  enum { W_NEXT_STAGE = 0, W_NEXT_CHECK, W_FNEXT, W_FAILED, W_BASE, W_NARROW, W_NK, W_SOFF };
   if (lane == 0) {
     st_sv(ws, W_BASE, 0);
     st_sv(ws, W_NARROW, !FT ? 0
                             : (max(x.oa + x.bm_eff, x.cra + 1) - wm * 64 <= 16 ? 1 : 0) |
                                   (max(x.ob + x.bn_eff, x.crb + 1) - wn * 32 <= 16 ? 2 : 0));
   }
+#ifdef FTBLAS_DEV_TIMELINE
+  // tools/dev_timeline.py (timeline build, -DFTBLAS_DEV_TIMELINE only): MMA warp 0's
+  // [globaltimer at start, first stage ready, k-loop end, role end] (clock64 offsets) in the
+  // CTA's dev_prof slots 10..11 (u64 20..23; the start clock parks in 23, so no register is held
+  // across the k-loop).
+#define FT_TL(i) (P.dev_prof[(size_t)blockIdx.x * 24 + 20 + (i)])
+  if (P.dev_prof && vt == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    FT_TL(0) = gt;
+    FT_TL(3) = (unsigned long long)clock64();
+    mbar_wait_u32(smem_u32(tl.full) + (FT ? STAGES * 8u : 0u), 0);
+    FT_TL(1) = (unsigned long long)clock64() - FT_TL(3);
+  }
+#endif
   for (int attempt = 0;; ++attempt) {
     // Interval of the last recompute decision (tl.retry, -1 in the first attempt): intervals
     // <= t_done are neither re-injected nor re-verified (the unit restarts from k = 0).
     const int t_done = tl.retry;
     const bool verify = FT && t_done < P.T - 1;
     if (lane == 0) {
+      // The attempt's stages: this CTA's k-split first (local stage 0 = global stage s0); a
+      // recompute covers the whole k.  Fault stages are global: compared as stage - s0.
+      st_sv(ws, W_NK, attempt == 0 ? x.nk : x.nk_all);
+      st_sv(ws, W_SOFF, attempt == 0 ? x.s0 : 0);
       st_sv(ws, W_FNEXT, x.f_lo);
-      st_sv(ws, W_NEXT_STAGE, x.f_lo < x.f_hi ? P.faults[x.f_lo].stage : 0x7fffffff);
+      st_sv(ws, W_NEXT_STAGE, x.f_lo < x.f_hi ? P.faults[x.f_lo].stage - (attempt == 0 ? x.s0 : 0) : 0x7fffffff);
       // Stage index at which the next intermediate verification interval ends (Kc = KcS
       // stages); the last interval is checked after the k-loop, on the staged tile.
       st_sv(ws, W_NEXT_CHECK, verify && t_done + 1 < P.T - 1 ? (t_done + 2) * max(1, (int)(P.Kc / BK)) : 0x7fffffff);
@@ -1367,7 +1360,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     for (int s = 0;;) {
       const int base = ld_sv(ws, W_BASE);
       int gs = base + s;
-      const int gs_end = base + __shfl_sync(0xffffffffu, min(min(ld_sv(ws, W_NEXT_STAGE), ld_sv(ws, W_NEXT_CHECK)), nk), 0);
+      const int gs_end = base + __shfl_sync(0xffffffffu, min(min(ld_sv(ws, W_NEXT_STAGE), ld_sv(ws, W_NEXT_CHECK)), ld_sv(ws, W_NK)), 0);
       if (SKIP && !active) {  // nothing of this warp's quarter is used: release the stages only
         for (; gs < gs_end; ++gs) {
           const int slot = gs % STAGES;
@@ -1459,7 +1452,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
           __syncwarp();
           if (lane == 0) {
             st_sv(ws, W_FNEXT, fnext + 1);
-            st_sv(ws, W_NEXT_STAGE, fnext + 1 < x.f_hi ? P.faults[fnext + 1].stage : 0x7fffffff);
+            st_sv(ws, W_NEXT_STAGE, fnext + 1 < x.f_hi ? P.faults[fnext + 1].stage - ld_sv(ws, W_SOFF) : 0x7fffffff);
           }
           __syncwarp();
         } else {
@@ -1478,12 +1471,119 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
               acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v + dv : v;
             }
       }
-      if (s >= nk) break;
+      if (s >= ld_sv(ws, W_NK)) break;
     }
     __syncwarp();
-    if (lane == 0) st_sv(ws, W_BASE, ld_sv(ws, W_BASE) + nk);  // the next attempt's first stage
+    if (lane == 0) st_sv(ws, W_BASE, ld_sv(ws, W_BASE) + ld_sv(ws, W_NK));  // the next attempt's first stage
     __syncwarp();
     int failed = ld_sv(ws, W_FAILED);  // the same in every MMA warp (a CTA-wide decision)
+    bool owner = true;  // this CTA verifies and stores the tile (k-split: the tile's last split)
+    if (P.ksplit > 1 && attempt == 0) {
+      // k-split: publish this split's partial C^f block and stage maxima; the tile's last split
+      // to finish (ticket) sums all partials in split order and carries on with the whole
+      // block, the others are done.
+      // (split and tile slot recomputed from blockIdx: nothing extra held across the k-loop)
+      const int S = P.ksplit, q = (int)blockIdx.x % S, slot = (int)blockIdx.x / S;
+      double *pp = P.part + (size_t)(slot * S + q) * (BM * BN);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) pp[((a * 4 + b) * 2 + e) * 256 + vt] = acc[a][b][e];
+      if (FT && vt == 0) {
+        P.part_max[2 * (slot * S + q)] = tl.int_am[0];
+        P.part_max[2 * (slot * S + q) + 1] = tl.int_bm[0];
+      }
+      __threadfence();
+      bar_sync(BAR_CTILE, 256);
+      if (vt == 0) tl.ticket = atomicAdd(&P.tickets[slot], 1);
+      bar_sync(BAR_CTILE, 256);
+      owner = tl.ticket == S - 1;
+      if (owner) {
+        __threadfence();
+        // (every split's partial from memory, this one's included: the same sum in the same
+        // order whichever split arrives last)
+        const double *p0 = P.part + (size_t)slot * S * (BM * BN) + vt;
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[a][b][e] = __ldcg(p0 + ((a * 4 + b) * 2 + e) * 256);
+        for (int r = 1; r < S; ++r) {
+          const double *pr = p0 + (size_t)r * (BM * BN);
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) acc[a][b][e] += __ldcg(pr + ((a * 4 + b) * 2 + e) * 256);
+        }
+        // The tile's faults after its last update (stage nk): on the summed block, as the unsplit
+        // kernel adds them after its last stage.
+        if (P.nfaults > 0) {
+          const TileGeom gf = load_geom(tl.geo);
+          const int tile = gf.ti + gf.tj * P.tiles_m, nk_all = (int)((P.k + BK - 1) / BK);
+          int lo = 0, hi = P.nfaults;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const FaultDev &f = P.faults[mid];
+            if (f.tile < tile || (f.tile == tile && f.stage < nk_all)) lo = mid + 1; else hi = mid;
+          }
+          for (int fi = lo; fi < P.nfaults && P.faults[fi].tile == tile; ++fi) {
+            const FaultDev f = P.faults[fi];
+            const int si = f.li < 0 ? gf.cra : f.li + gf.oa, sj = f.lj < 0 ? gf.crb : f.lj + gf.ob;
+            const int fidx = acc_owner_index<AKM, BKM>(si, sj, wm, wn, lane);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const double v = acc[a][b][e];
+                  acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v + f.delta : v;
+                }
+          }
+        }
+        if (FT && vt == 0) {  // the maxima over all of k (R1')
+          uint32_t am = 0u, bm = 0u;
+          for (int r = 0; r < S; ++r) {
+            am = max(am, __ldcg(P.part_max + 2 * (slot * S + r)));
+            bm = max(bm, __ldcg(P.part_max + 2 * (slot * S + r) + 1));
+          }
+          tl.int_am[0] = am;
+          tl.int_bm[0] = bm;
+        }
+        bar_sync(BAR_CTILE, 256);
+      }
+    }
+#ifdef FTBLAS_DEV_TIMELINE
+    if (P.dev_prof && vt == 0 && attempt == 0) FT_TL(2) = (unsigned long long)clock64() - FT_TL(3);
+#endif
+    if (owner && verify && failed < 0 && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
+      // The last interval, verified before C is written, from the registers
+      // (its first barrier is also the point where every MMA warp has drained its DMMA stream).
+      const CheckOut co = check_unit<AKM, BKM>(P, tl, acc, P.T - 1, P.k, mw, wm, wn, lane);
+      if (co.multi) {
+        failed = P.T - 1;
+      } else if (co.si >= 0) {
+        if (P.correct_mode == 1) {  // subtract d_col at the located cell
+          const int fidx = acc_owner_index<AKM, BKM>(co.si, co.sj, wm, wn, lane);
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const double v = acc[a][b][e];
+                acc[a][b][e] = ((a * 4 + b) * 2 + e == fidx) ? v - co.dcol : v;
+              }
+        } else if (vt == 0) {
+          add_fix(tl, co.si, co.sj);  // R4: fresh dot product in the epilogue
+        }
+      }
+    }
     // Stage the accumulators into the ring as the C tile: every MMA warp has consumed its last
     // stage (and every TMA write and checksum row has landed before that stage was consumed).
     bar_sync(BAR_CTILE, 256);
@@ -1499,16 +1599,6 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         }
     }
     bar_sync(BAR_CTILE, 256);
-    if (verify && failed < 0 && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
-      // The last interval, verified before C is written, on the staged tile.
-      const CheckOut co = check_tile<AKM, BKM>(P, tl, ctile, P.T - 1, P.k, mw, lane);
-      if (co.multi) {
-        failed = P.T - 1;
-      } else if (co.si >= 0 && vt == 0) {
-        if (P.correct_mode == 1) ctile[co.sj * LDC_S + co.si] -= co.dcol;
-        else add_fix(tl, co.si, co.sj);                                   // R4: fresh dot product
-      }
-    }
     if (failed >= 0) fence_proxy_async();  // generic writes to the ring before TMA refills it
     bar_sync(BAR_RING_FREE, NTHREADS);  // every stage consumed: the ring is free for the C tile
     if (!verify) break;
@@ -1523,6 +1613,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     bar_sync(BAR_DECIDE, NTHREADS);  // encoders learn whether (and from where) to run again
     if (failed < 0) break;  // else out of the one-error model: recompute the unit (R6)
   }
+  // k-split: another split of this tile verifies and stores it (a recompute only ever runs in
+  // the owner, so the ticket of its first attempt decides)
+  if (P.ksplit > 1 && tl.ticket != P.ksplit - 1) return;
 
   // ---- epilogue: corrected cells (recompute mode), then C = alpha*acc + beta*C0 (two
   // roundings each, no contraction) from the staged tile, coalesced column stores.
@@ -1566,6 +1659,10 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       *dst = (beta != 0.0) ? __dadd_rn(v, __dmul_rn(beta, *dst)) : v;
     }
   }
+#ifdef FTBLAS_DEV_TIMELINE
+  if (P.dev_prof && vt == 0) FT_TL(3) = (unsigned long long)clock64() - FT_TL(3);
+#undef FT_TL
+#endif
 }
 
 template <bool AKM, bool BKM, bool FT>
@@ -1618,7 +1715,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     ti_ = r0 + L;  // partial last tile column, its rows top to bottom
     tj_ = P.tiles_n - 1;
   };
-  const int Lg = (int)blockIdx.x;
+  const int Lg = (int)blockIdx.x / P.ksplit;  // tile in launch order (k-split: P.ksplit CTAs each)
   const bool ghost = P.cluster2 && Lg >= P.total;  // pads an odd grid to whole clusters
   int ti, tj;
   map_tile(ghost ? Lg - 1 : Lg, ti, tj);
@@ -1631,8 +1728,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     share = ptj == tj;
   }
   x.tile = ti + tj * P.tiles_m;  // fault bucket key
-  x.k0 = 0;
-  x.k1 = P.k;
+  x.tile_slot = Lg;
+  x.nk_all = (int)((P.k + BK - 1) / BK);
+  x.q = (int)blockIdx.x % P.ksplit;
+  x.s0 = (int)((int64_t)x.q * x.nk_all / P.ksplit);
+  const int s1 = (int)((int64_t)(x.q + 1) * x.nk_all / P.ksplit);
+  x.k0 = (int64_t)x.s0 * BK;
+  x.k1 = min64((int64_t)s1 * BK, P.k);
   // Protected tiles advance by the 127 data rows/cols of C^f; the unprotected twin uses the
   // full 128 x 128 MMA tile for data.
   const bool g127 = FT || (FT_DEV_MODE(P) & 32);  // dev mode 32: unprotected kernel on the 127 grid
@@ -1682,13 +1784,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     fence_mbar_init();
   }
   // Faults of this tile: [f_lo, f_hi) in the (tile, stage)-sorted list.
+  // (k-split: those with stage in [s0, s1); the last split also takes the faults at stage nk,
+  // i.e. after the last update)
   x.f_lo = x.f_hi = 0;
   if (P.nfaults > 0) {
+    auto before = [&](const FaultDev &f, int st) { return f.tile < x.tile || (f.tile == x.tile && f.stage < st); };
     int lo = 0, hi = P.nfaults;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.faults[mid].tile < x.tile) lo = mid + 1; else hi = mid; }
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (before(P.faults[mid], x.s0)) lo = mid + 1; else hi = mid; }
     x.f_lo = lo;
+    // (the faults after the last update, stage nk, go to the tile's owner in a k-split launch)
+    const int s_end = P.ksplit == 1 ? 0x7fffffff : s1;
     hi = P.nfaults;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (P.faults[mid].tile <= x.tile) lo = mid + 1; else hi = mid; }
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (before(P.faults[mid], s_end)) lo = mid + 1; else hi = mid; }
     x.f_hi = lo;
   }
   __syncthreads();

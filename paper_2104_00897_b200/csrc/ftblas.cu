@@ -420,9 +420,18 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.Kc = Kc;
   p.T = (int)T;
   p.ntiles = p.tiles_m * p.tiles_n;
+  // k-split of launches with very few tiles (C^f partials summed in split order and verified by
+  // the tile's last split, dgemm_abft.cuh): 8 splits of >= 2 stages each when they fit in one
+  // wave of the SMs (<= 18 tiles on 148 SMs; the latency-bound small problems).  The partial
+  // sums round differently from one k-loop, so such a call is not bitwise equal to the same
+  // tiles computed unsplit (within the parity bound).  Verification intervals (Kc < k) keep
+  // whole tiles.
+  p.ksplit = 1;
+  if (T == 1 && (int64_t)p.ntiles * 8 <= (int64_t)num_sms())
+    p.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)p.nk / 2, 8));
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
   p.correct_mode = tl_correct;
-  p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL) ? 1 : 0;  // request; launch_one decides
+  p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL && p.ksplit == 1) ? 1 : 0;  // request; launch_one decides
 #ifdef FTBLAS_DEV
 #ifdef FTBLAS_WATCHDOG
   if (const char *dw = std::getenv("FTBLAS_DEV_WATCH")) {  // hang watchdog slot (tools/hang_probe.py)
@@ -433,6 +442,10 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // development build only: per-CTA per-warp clock64 wait/work sums (tools/dev_prof.py)
   if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
   p.dev_mode = dev_mode;
+#endif
+#ifdef FTBLAS_DEV_TIMELINE
+  // timeline build only (tools/dev_timeline.py): per-CTA clocks of MMA warp 0
+  if (const char *dp = std::getenv("FTBLAS_DEV_PROF")) p.dev_prof = reinterpret_cast<unsigned long long *>(std::strtoull(dp, nullptr, 0));
 #endif
   p.wait_pub = (ft && tl_encode == FTBLAS_ENCODE_FUSED_WAIT) ? 1 : 0;
 
@@ -469,7 +482,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // slice maxima and the published sums, filled with all-ones bytes (= not yet published).
   // Launches of a single wave skip it (every tile starts together, so a consumer would almost
   // never find a stage published) unless dev modes 256 / 512 force the copy paths.
-  const bool one_wave = (int64_t)p.ntiles <= (int64_t)num_sms() && !p.wait_pub;
+  const bool one_wave = (int64_t)p.ntiles * p.ksplit <= (int64_t)num_sms() && !p.wait_pub;
   const bool fused_shared = tl_encode == FTBLAS_ENCODE_FUSED || tl_encode == FTBLAS_ENCODE_FUSED_WAIT;
   const bool ashare = ft && fused_shared && p.tiles_n > 1 && !one_wave;
   const bool bshare = ft && fused_shared && p.tiles_m > 1 && !one_wave;
@@ -478,6 +491,11 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // zeroed, the publication region filled with 0xFF; counters and the first events are read
   // back by one copy (finish_report).
   const size_t base_bytes = al256(64 + ev_bytes + f_bytes);
+  // k-split: the partial C^f blocks, their stage maxima and the per-tile tickets
+  const size_t split_bytes = p.ksplit > 1 ? al256(sizeof(double) * ftk::BM * ftk::BN * (size_t)p.ntiles * p.ksplit) +
+                                                al256(sizeof(unsigned) * 2 * (size_t)p.ntiles * p.ksplit) +
+                                                al256(sizeof(int) * (size_t)p.ntiles)
+                                          : 0;
   const size_t hm_bytes = al256(sizeof(unsigned) * (p.tiles_m + p.tiles_n));
   const size_t pre_bytes = prepass ? hm_bytes + sizeof(double) * (size_t)(p.tiles_m + p.tiles_n) * k : 0;
   const size_t hma_bytes = ashare ? al256(sizeof(unsigned) * (size_t)p.tiles_m * nsg) : 0;
@@ -486,8 +504,17 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   const size_t bsh_bytes = bshare ? hmb_bytes + sizeof(double) * (size_t)p.tiles_n * (size_t)k : 0;
   Cleanup cl(st);
   char *scratch = nullptr;
-  CUDA_TRY(cl.alloc(&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes));
+  CUDA_TRY(cl.alloc(&scratch, base_bytes + pre_bytes + ash_bytes + bsh_bytes + split_bytes));
   char *const cnt_ptr = scratch;
+  if (p.ksplit > 1) {
+    char *sp = scratch + base_bytes + pre_bytes + ash_bytes + bsh_bytes;
+    p.part = reinterpret_cast<double *>(sp);
+    sp += al256(sizeof(double) * ftk::BM * ftk::BN * (size_t)p.ntiles * p.ksplit);
+    p.part_max = reinterpret_cast<unsigned *>(sp);
+    sp += al256(sizeof(unsigned) * 2 * (size_t)p.ntiles * p.ksplit);
+    p.tickets = reinterpret_cast<int *>(sp);
+    CUDA_TRY(cudaMemsetAsync(p.tickets, 0, sizeof(int) * (size_t)p.ntiles, st));
+  }
   if (ashare) {
     char *sb = scratch + base_bytes + pre_bytes;
     p.hmA = reinterpret_cast<unsigned *>(sb);
@@ -555,7 +582,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   if (int e = make_tmap(&tmA, p.A, p.lda, akm, m, k)) return e;
   if (int e = make_tmap(&tmB, p.B, p.ldb, bkm, n, k)) return e;
   // One launch: every CTA verifies its tile online after every Kc updates (T checks).
-  const dim3 grid((unsigned)p.ntiles);  // 1-D: grouped raster in the kernel
+  const dim3 grid((unsigned)(p.ntiles * p.ksplit));  // 1-D: grouped raster in the kernel
   const int lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
   if (lrc) return lrc;
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass, field
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -177,12 +178,27 @@ def _report(r: ErrReport, evbuf) -> Report:
                   r.unit_cols, r.unit_k, r.step_quantum, ev)
 
 
+_tls = threading.local()
+
+
+def _event_buffer(capacity):
+    """Per-thread report buffer of `capacity` events, reused across calls (the Report copies the
+    events out; allocating and zeroing a fresh ctypes array cost ~20 us per call)."""
+    cache = getattr(_tls, "evbufs", None)
+    if cache is None:
+        cache = _tls.evbufs = {}
+    buf = cache.get(capacity)
+    if buf is None:
+        buf = cache[capacity] = (Event * capacity)()
+    return buf
+
+
 def _protected(fn, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, report,
                events_capacity, raw_status):
     L = load()
     f = getattr(L, fn)
     if report:
-        evbuf = (Event * max(events_capacity, 1))()
+        evbuf = _event_buffer(max(events_capacity, 1))
         r = ErrReport()
         r.events = evbuf
         r.events_capacity = events_capacity
@@ -226,7 +242,7 @@ def ftblas_dgemm_host(transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, l
                       report=True, events_capacity=4096):
     """Protected DGEMM on HOST buffers (numpy arrays / host addresses); C updated in place."""
     L = load()
-    evbuf = (Event * max(events_capacity, 1))()
+    evbuf = _event_buffer(max(events_capacity, 1))
     r = ErrReport()
     r.events = evbuf
     r.events_capacity = events_capacity
@@ -284,7 +300,7 @@ def ftblas_dtrsm(side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, *, repor
     """FT-DTRSM (NEXT-3): B := alpha op(A)^-1 B (side 'L') or alpha B op(A)^-1 (side 'R') on
     device pointers; returns a Report."""
     L = load()
-    evbuf = (Event * max(events_capacity, 1))()
+    evbuf = _event_buffer(max(events_capacity, 1))
     r = ErrReport()
     r.events = evbuf
     r.events_capacity = events_capacity

@@ -23,3 +23,20 @@ def ftf():
     F.ftblas_inject_arm([(17, 203, 128, 1e3)])
     F.ftblas_dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m)
 print("ft report + fault   %.1f us" % wall(ftf))
+# host-side cost of one call (the time the Python call itself takes; the GPU runs behind)
+def host(fn, r=200):
+    for _ in range(10): fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(r):
+        t0 = time.perf_counter(); fn(); ts.append(time.perf_counter() - t0)
+    torch.cuda.synchronize()
+    ts.sort()
+    return ts[len(ts) // 2] * 1e6
+import ctypes
+L = F.load()
+pA, pB, pC = A.data_ptr(), B.data_ptr(), C.data_ptr()
+print("host: noft binding       %.1f us" % host(lambda: F.ftblas_dgemm_noft("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m)))
+print("host: noft raw ctypes    %.1f us" % host(lambda: L.ftblas_dgemm_noft(b"N", b"N", m, n, k, 1.0, pA, m, pB, k, 0.0, pC, m)))
+print("host: ft no report       %.1f us" % host(lambda: F.ftblas_dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m, report=False)))
+print("host: ft raw no report   %.1f us" % host(lambda: L.ftblas_dgemm(b"N", b"N", m, n, k, 1.0, pA, m, pB, k, 0.0, pC, m, None)))
