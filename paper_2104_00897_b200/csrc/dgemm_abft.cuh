@@ -838,20 +838,34 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   const bool b_pub = P.Bsh && x.ti == 0;
   struct PubA { bool ok; double a0, a1; uint32_t am; };
   // Relaxed loads of stage s's published e^T A_I words (not used until after the TMA wait).
+  // Per attempt (the k range changes for a recompute): this lane's published words of the
+  // attempt's first stage and its slot offsets of the checksum row / column (the copy path of
+  // ~99% of the stages at C5 then costs a handful of instructions next to the DMMA stream).
+  const int pa = AKM ? 2 * lane : lane;  // this lane's k-slot(s) of e^T A_I within a stage
+  const double *srcA = nullptr, *srcB = nullptr;
+  const unsigned *hmAp = nullptr, *hmBp = nullptr;
+  int offA = 0, offB = 0;
+  auto attempt_setup = [&]() {
+    srcA = P.Ash ? P.Ash + x.ti * P.ldash + k0 + pa : nullptr;
+    hmAp = P.hmA ? P.hmA + (size_t)x.ti * P.nk + k0 / BK : nullptr;
+    srcB = P.Bsh ? P.Bsh + x.tj * P.ldbsh + k0 + lane : nullptr;
+    hmBp = P.hmB ? P.hmB + (size_t)x.tj * P.nk + k0 / BK : nullptr;
+    offA = sidx<AKM>(x.cra, AKM ? 2 * (lane & 7) : (lane & 15));
+    offB = sidx<BKM>(x.crb, lane & 15);
+  };
+  attempt_setup();
   auto fetch_a = [&](int s) {
     PubA f{false, 0.0, 0.0, 0xFFFFFFFFu};
     if (!a_sub) return f;
-    const int64_t sg = k0 / BK + s;  // global stage index
-    const int p = AKM ? 2 * lane : lane;  // this lane's k-slot(s) within the stage
-    const int64_t pg = k0 + (int64_t)s * BK + p;
-    const double *src = P.Ash + x.ti * P.ldash + pg;
+    const int kl = (int)(k1 - k0) - s * BK;  // k-slots of this stage inside k
+    const double *src = srcA + s * BK;
     if (AKM) {
-      f.a0 = lane < 8 && pg < k1 ? ld_relaxed_gpu(src) : 0.0;
-      f.a1 = lane < 8 && pg + 1 < k1 ? ld_relaxed_gpu(src + 1) : 0.0;
+      f.a0 = lane < 8 && pa < kl ? ld_relaxed_gpu(src) : 0.0;
+      f.a1 = lane < 8 && pa + 1 < kl ? ld_relaxed_gpu(src + 1) : 0.0;
     } else {
-      f.a0 = lane < 16 && pg < k1 ? ld_relaxed_gpu(src) : 0.0;
+      f.a0 = lane < 16 && pa < kl ? ld_relaxed_gpu(src) : 0.0;
     }
-    f.am = ld_relaxed_gpu(P.hmA + (size_t)x.ti * P.nk + sg);
+    f.am = ld_relaxed_gpu(hmAp + s);
     return f;
   };
   // Whole stage published?  (warp-uniform; encode mode FUSED_WAIT waits for it)
@@ -919,18 +933,17 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         uint32_t amax_hi = 0u, bmax_hi = 0u;  // this stage's slice maxima (R1' high words)
         const long long t0 = FT_DEV_PROF(P) ? clock64() : 0;
         const bool pubs = !(P.Ac || (FT_DEV_MODE(P) & 3));
-        PubA pa = pubs && doA ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
+        PubA pa_ = pubs && doA ? fetch_a(s) : PubA{false, 0.0, 0.0, 0u};
         // B_J e words of this stage: relaxed loads before the TMA wait as well
         double pb = 0.0;
         uint32_t pbm = 0xFFFFFFFFu;
         auto fetch_b = [&]() {
-          const int64_t pg = k0 + (int64_t)s * BK + lane;
-          pb = lane < 16 && pg < k1 ? ld_relaxed_gpu(P.Bsh + x.tj * P.ldbsh + pg) : 0.0;
-          pbm = ld_relaxed_gpu(P.hmB + (size_t)x.tj * P.nk + (k0 / BK + s));
+          pb = lane < 16 && lane < (int)(k1 - k0) - s * BK ? ld_relaxed_gpu(srcB + s * BK) : 0.0;
+          pbm = ld_relaxed_gpu(hmBp + s);
         };
         if (pubs && doB && b_sub) fetch_b();
         if (!(FT_DEV_MODE(P) & 16)) mbar_wait_sleep(&tl.full[slot], (gs / STAGES) & 1);
-        if (pubs && doA) check_a(s, pa);
+        if (pubs && doA) check_a(s, pa_);
         bool bcopy = false;
         if (pubs && doB && b_sub) {
           bcopy = __all_sync(0xffffffffu, pub_ok(pb) && pub_ok(pbm));
@@ -956,17 +969,17 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
           // development: no encode (checksum rows zero)
         } else {
          if (doA) {
-          enc_a(sA, s, pa, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
+          enc_a(sA, s, pa_, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           if (AKM) {
-            if (lane < 8) *reinterpret_cast<double2 *>(sA + sidx<true>(x.cra, 2 * lane)) = make_double2(a0, a1);
+            if (lane < 8) *reinterpret_cast<double2 *>(sA + offA) = make_double2(a0, a1);
           } else {
-            if (lane < 16) sA[sidx<false>(x.cra, lane)] = a0;
+            if (lane < 16) sA[offA] = a0;
           }
          }
          if (doB) {
           const int64_t sg = k0 / BK + s;  // global stage index
           if (bcopy) {  // B_J e of this stage as published by tile row 0
-            if (lane < 16) sB[sidx<BKM>(x.crb, lane)] = pb;
+            if (lane < 16) sB[offB] = pb;
             bmax_hi = max(bmax_hi, pbm);
           } else {
             uint32_t hmb = 0u;
@@ -1020,7 +1033,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
          }
         }
         if (!P.Ac && lane == 0 && !(FT_DEV_MODE(P) & 4096)) {  // the interval's maxima, read by the MMA warps at its check
-          const int tint = min(s / KcS, P.T - 1) & 7;
+          const int tint = P.T == 1 ? 0 : min(s / KcS, P.T - 1) & 7;
           if (doA) atomicMax(&tl.int_am[tint], amax_hi);
           if (doB) atomicMax(&tl.int_bm[tint], bmax_hi);
         }
@@ -1050,6 +1063,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
     nk = x.nk_all;  // a recompute covers the whole k (a k-split tile is recomputed unsplit)
     k0 = 0;
     k1 = P.k;
+    attempt_setup();
   }
 }
 
@@ -1181,6 +1195,11 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
 #ifdef FTBLAS_DEV
   const long long dv_t0 = clock64();
 #endif
+  // Every MMA warp has issued its last DMMA of the interval before anyone sums: a dependent
+  // FP64 add next to a running DMMA stream waits ~270-1000 clocks (profiles/
+  // fp64_latency_under_dmma.json), ~8 once the FP64 pipe is free (end-of-tile check 7.4k ->
+  // see DESIGN.md section 6).
+  bar_sync(BAR_PART, 256);
   const int cra = tl.geo.cra, crb = tl.geo.crb;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
@@ -1317,6 +1336,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   // CTA's dev_prof slots 10..11 (u64 20..23; the start clock parks in 23, so no register is held
   // across the k-loop).
 #define FT_TL(i) (P.dev_prof[(size_t)blockIdx.x * 24 + 20 + (i)])
+  // (u64 16..18: after the last check, after the ring is released, before the stores)
   if (P.dev_prof && vt == 0) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -1584,6 +1604,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
         }
       }
     }
+#ifdef FTBLAS_DEV_TIMELINE
+    if (P.dev_prof && vt == 0 && attempt == 0) FT_TL(-4) = (unsigned long long)clock64() - FT_TL(3);
+#endif
     // Stage the accumulators into the ring as the C tile: every MMA warp has consumed its last
     // stage (and every TMA write and checksum row has landed before that stage was consumed).
     bar_sync(BAR_CTILE, 256);
@@ -1601,6 +1624,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     bar_sync(BAR_CTILE, 256);
     if (failed >= 0) fence_proxy_async();  // generic writes to the ring before TMA refills it
     bar_sync(BAR_RING_FREE, NTHREADS);  // every stage consumed: the ring is free for the C tile
+#ifdef FTBLAS_DEV_TIMELINE
+    if (P.dev_prof && vt == 0 && attempt == 0) FT_TL(-3) = (unsigned long long)clock64() - FT_TL(3);
+#endif
     if (!verify) break;
     if (vt == 0) {
       tl.retry = failed;
@@ -1620,6 +1646,9 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   // ---- epilogue: corrected cells (recompute mode), then C = alpha*acc + beta*C0 (two
   // roundings each, no contraction) from the staged tile, coalesced column stores.
   bar_sync(BAR_CTILE, 256);
+#ifdef FTBLAS_DEV_TIMELINE
+  if (P.dev_prof && vt == 0) FT_TL(-2) = (unsigned long long)clock64() - FT_TL(3);
+#endif
   const TileGeom ge = load_geom(tl.geo);
   if (FT) {
     // Recompute mode (R4): each corrected element becomes a fresh dot product over all k.

@@ -32,12 +32,17 @@ e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record(); call(); e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
-p = prof.view(-1, 12, 2)[:, 10:12, :].reshape(-1, 4).double()
-p = p[p[:, 0] > 0]
-m = p[:, 1:].mean(0)
+pv = prof.view(-1, 24).double()
+p = pv[:, 20:24]
+sel = p[:, 0] > 0
+p, q = p[sel], pv[sel][:, 16:19]
+m, mq = p[:, 1:].mean(0), q.mean(0)
 stages = (K + 15) // 16
 print(json.dumps({
     "mode": "noft" if noft else "ft", "MNK": [M, N, K], "trans": tr, "ms": ms, "ctas": int(p.shape[0]),
     "first_ready_clk": round(m[0].item()), "kloop_clk_per_stage": round((m[1] - m[0]).item() / stages, 1),
     "ideal_clk_per_stage": 4096, "epilogue_clk": round((m[2] - m[1]).item()), "tile_clk": round(m[2].item()),
+    "epilogue_split_clk": {"check": round((mq[0] - m[1]).item()) if not noft else 0,
+                           "stage_and_ring_release": round((mq[1] - (mq[0] if not noft else m[1])).item()),
+                           "decide_to_store": round((mq[2] - mq[1]).item()), "store": round((m[2] - mq[2]).item())},
 }), flush=True)

@@ -32,7 +32,10 @@ def run(m, n, k, ta="N", tb="N", reps=5):
            "overhead_pct": 100 * (res["ft"] - res["noft"]) / res["noft"]}
     print(json.dumps(out), flush=True)
 
-for shp in [(2048, 2048, 2048, "N", "N"), (8192, 8192, 8192, "N", "N"), (8192, 8192, 8192, "T", "N"),
-            (8192, 8192, 8192, "N", "T"), (8192, 8192, 8192, "T", "T"), (16384, 16384, 1024, "N", "N"),
-            (16384, 512, 16384, "N", "N")]:
-    run(*shp)
+shapes = [(2048, 2048, 2048, "N", "N"), (8192, 8192, 8192, "N", "N"), (8192, 8192, 8192, "T", "N"),
+          (8192, 8192, 8192, "N", "T"), (8192, 8192, 8192, "T", "T"), (16384, 16384, 1024, "N", "N"),
+          (16384, 512, 16384, "N", "N")]
+if os.environ.get("C5"):
+    shapes.append((32768, 32768, 32768, "N", "N"))
+for shp in shapes:
+    run(*shp, reps=int(os.environ.get("REPS", "5")) if shp[0] < 32768 else 2)
