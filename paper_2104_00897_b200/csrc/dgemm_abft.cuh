@@ -282,7 +282,18 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
 #ifdef FTBLAS_WATCHDOG
   mbar_wait(bar, parity);
 #else
-  while (!mbar_test(bar, parity)) __nanosleep(64);
+  // try_wait with a suspend-time hint: the warp is suspended until the phase completes (or the
+  // hint's 20 us pass), instead of polling with test_wait + nanosleep (ncu at 8192^3: the
+  // polling loop was more than half of the unprotected kernel's issued instructions).
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000)
+      : "memory");
 #endif
 }
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
