@@ -1190,6 +1190,93 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
   return out;
 }
 
+// Register partials of a check, reduce-scatter form.  Columns: two batches of 4 columns
+// q = 4j + i (q = 2b + e), 4 independent chains over this thread's 8 rows; the 8 lanes sharing
+// the columns (lane bits 2..4) reduce-scatter them (2 + 1 shuffles, then 1 for the last pair):
+// lanes g, g ^ 1 end with column i = h1 + 2 h2.  Rows: two batches of 4 rows a = 4j + i over
+// this thread's 8 columns; the 4 lanes sharing the rows (lane bits 0..1) reduce-scatter them
+// (2 + 1 shuffles): lane tq ends with row a = 4j + tq.  The checksum row cra / column crb are
+// left out of the sums and stored as the carried checksums.  STD: they sit at tile row /
+// column 0 or DM (every tile but the partial edge tiles), i.e. in register (a, g) = (0, 0) of
+// warp row 0 or (7, 7) of warp row 1 (column: (b, e, tq) = (0, 0, 0) of warp column 0 or
+// (3, 1, 3) of warp column 3) in both fragment layouts, so only those registers need a select.
+template <bool AKM, bool BKM, bool STD>
+__device__ __forceinline__ void partials_rs(SmemTail &tl, const double (&acc)[8][4][2], int lg, int lt, int lwm, int lwn,
+                                            int cra, int crb) {
+  const bool exA0 = STD && cra == 0 && lwm == 0 && lg == 0, exA7 = STD && cra == DM && lwm == 1 && lg == 7;
+  const bool exB0 = STD && crb == 0 && lwn == 0 && lt == 0, exB7 = STD && crb == DM && lwn == 3 && lt == 3;
+  {
+    const bool h2 = (lg >> 2) & 1, h1 = (lg >> 1) & 1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double c[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int b = 2 * j + (i >> 1), e = i & 1;
+        double x = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          if (STD) {
+            x += ((a == 0 && exA0) || (a == 7 && exA7)) ? 0.0 : acc[a][b][e];
+          } else {
+            if (lwm * 64 + tile_row<AKM>(a, lg) != cra) x += acc[a][b][e];
+            else tl.cs_col[lwn * 32 + tile_row<BKM>(b, 2 * lt + e)] = acc[a][b][e];  // carried (e^T A_I) B_J
+          }
+        }
+        c[i] = x;
+      }
+      double c2[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)  // i = u + 2 h2
+        c2[u] = (h2 ? c[u + 2] : c[u]) + __shfl_xor_sync(0xffffffffu, h2 ? c[u] : c[u + 2], 16);
+      double c1 = (h1 ? c2[1] : c2[0]) + __shfl_xor_sync(0xffffffffu, h1 ? c2[0] : c2[1], 8);  // i = h1 + 2 h2
+      c1 += __shfl_xor_sync(0xffffffffu, c1, 4);
+      if ((lg & 1) == 0) tl.colpart[lwm][lwn * 32 + tile_row<BKM>(2 * j + (h2 ? 1 : 0), 2 * lt + (h1 ? 1 : 0))] = c1;
+    }
+  }
+  {
+    const bool h1 = (lt >> 1) & 1, h0 = lt & 1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double r[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double x = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (STD) {
+              x += ((b == 0 && e == 0 && exB0) || (b == 3 && e == 1 && exB7)) ? 0.0 : acc[4 * j + i][b][e];
+            } else {
+              if (lwn * 32 + tile_row<BKM>(b, 2 * lt + e) != crb) x += acc[4 * j + i][b][e];
+              else tl.cs_row[lwm * 64 + tile_row<AKM>(4 * j + i, lg)] = acc[4 * j + i][b][e];  // carried A_I (B_J e)
+            }
+          }
+        r[i] = x;
+      }
+      double r2[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)  // i = u + 2 h1
+        r2[u] = (h1 ? r[u + 2] : r[u]) + __shfl_xor_sync(0xffffffffu, h1 ? r[u] : r[u + 2], 2);
+      const double r1 = (h0 ? r2[1] : r2[0]) + __shfl_xor_sync(0xffffffffu, h0 ? r2[0] : r2[1], 1);  // i = tq
+      tl.rowpart4[lwn][lwm * 64 + tile_row<AKM>(4 * j + lt, lg)] = r1;
+    }
+  }
+  if (STD) {  // the carried checksums (e^T A_I) B_J and A_I (B_J e)
+    if (exA0 || exA7) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) tl.cs_col[lwn * 32 + tile_row<BKM>(b, 2 * lt + e)] = exA0 ? acc[0][b][e] : acc[7][b][e];
+    }
+    if (exB0 || exB7) {
+#pragma unroll
+      for (int a = 0; a < 8; ++a) tl.cs_row[lwm * 64 + tile_row<AKM>(a, lg)] = exB0 ? acc[a][0][0] : acc[a][3][1];
+    }
+  }
+}
+
 // Check at the end of an intermediate interval (Kc < k), with the accumulators LIVE in
 // registers (the k-loop continues): straight from the registers, in two sequential passes with
 // few live temporaries -- column partials one n-tile at a time (over this thread's 8 rows, then
@@ -1198,7 +1285,7 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
 // partials meet in shared memory (6 KB; no staging of the tile).  The checksum row / column are
 // excluded by index.  The loop-carried segment state lives in shared memory, so the DMMA k-loop
 // keeps its register allocation (tools/kloop_stats.py).
-template <bool AKM, bool BKM>
+template <bool AKM, bool BKM, bool RS>
 __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, const double (&acc)[8][4][2], int t,
                                                int64_t kt, int mw, int wm, int wn, int lane) {
   const int g = lane >> 2, tq = lane & 3;
@@ -1211,39 +1298,56 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   // fp64_latency_under_dmma.json), ~8 once the FP64 pipe is free (end-of-tile check 7.4k ->
   // see DESIGN.md section 6).
   bar_sync(BAR_PART, 256);
+#ifdef FTBLAS_DEV
+  const long long dv_ta = clock64();
+  // drain probe: a shared store of this warp's last DMMA result issues only once it has landed
+  *reinterpret_cast<volatile double *>(&tl.red[mw]) = acc[7][3][1];
+  const long long dv_tb = clock64();
+#endif
   const int cra = tl.geo.cra, crb = tl.geo.crb;
+  if (!RS) {
+    // (the serial form: one column / row chain at a time with full butterflies; used where the
+    // reduce-scatter form below pushes the DMMA k-loop into spills)
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int col = wn * 32 + tile_row<BKM>(b, 2 * tq + e);
-      double c = 0.0;
-#pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        const double v = acc[a][b][e];
-        if (wm * 64 + tile_row<AKM>(a, g) != cra) c += v;
-        else tl.cs_col[col] = v;  // carried (e^T A_I) B_J
-      }
-#pragma unroll
-      for (int o = 4; o <= 16; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      if (g == 0) tl.colpart[wm][col] = c;
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int row = wm * 64 + tile_row<AKM>(a, g);
-    double r = 0.0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+  #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const double v = acc[a][b][e];
-        if (wn * 32 + tile_row<BKM>(b, 2 * tq + e) != crb) r += v;
-        else tl.cs_row[row] = v;  // carried A_I (B_J e)
+        const int col = wn * 32 + tile_row<BKM>(b, 2 * tq + e);
+        double c = 0.0;
+  #pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const double v = acc[a][b][e];
+          if (wm * 64 + tile_row<AKM>(a, g) != cra) c += v;
+          else tl.cs_col[col] = v;  // carried (e^T A_I) B_J
+        }
+  #pragma unroll
+        for (int o = 4; o <= 16; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (g == 0) tl.colpart[wm][col] = c;
       }
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    if (tq == 0) tl.rowpart4[wn][row] = r;
+    }
+  #pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int row = wm * 64 + tile_row<AKM>(a, g);
+      double r = 0.0;
+  #pragma unroll
+      for (int b = 0; b < 4; ++b)
+  #pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double v = acc[a][b][e];
+          if (wn * 32 + tile_row<BKM>(b, 2 * tq + e) != crb) r += v;
+          else tl.cs_row[row] = v;  // carried A_I (B_J e)
+        }
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      r += __shfl_xor_sync(0xffffffffu, r, 2);
+      if (tq == 0) tl.rowpart4[wn][row] = r;
+    }
+  } else {
+    // Lane / warp coordinates laundered here, so the index arithmetic is not hoisted out of the
+    // k-loop's segment loop (where it would hold registers across the DMMA stream).
+    int lg = g, lt = tq, lwm = wm, lwn = wn;
+    asm volatile("" : "+r"(lg), "+r"(lt), "+r"(lwm), "+r"(lwn));
+    if ((cra == 0 || cra == DM) && (crb == 0 || crb == DM)) partials_rs<AKM, BKM, true>(tl, acc, lg, lt, lwm, lwn, cra, crb);
+    else partials_rs<AKM, BKM, false>(tl, acc, lg, lt, lwm, lwn, cra, crb);
   }
   bar_sync(BAR_PART, 256);
 #ifdef FTBLAS_DEV
@@ -1266,6 +1370,8 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     dp[1] += (unsigned long long)(dv_t2 - dv_t1);
     dp[2] += 1ull;
     dp[3] += (unsigned long long)(t3 - dv_t2);
+    dp[4] += (unsigned long long)(dv_ta - dv_t0);  // arrival skew (first barrier)
+    dp[5] += (unsigned long long)(dv_tb - dv_ta);  // drain of this warp's DMMA stream
   }
   return dv_out;
 #else
@@ -1436,7 +1542,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       if (FT && s == ld_sv(ws, W_NEXT_CHECK)) {
         const int kcs = max(1, (int)(P.Kc / BK));
         const int tcur = s / kcs - 1;
-        const CheckOut co = check_unit<AKM, BKM>(P, tl, acc, tcur, (int64_t)s * BK, mw, wm, wn, lane);
+        const CheckOut co = check_unit<AKM, BKM, BKM>(P, tl, acc, tcur, (int64_t)s * BK, mw, wm, wn, lane);
         // A single error is subtracted now, so the next intervals verify the
         // corrected partial product; in recompute mode (R4) the cell is also replaced by a fresh
         // k-long dot product in the epilogue (fix list), which equals the oracle's recomputed
@@ -1595,7 +1701,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     if (owner && verify && failed < 0 && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
       // The last interval, verified before C is written, from the registers
       // (its first barrier is also the point where every MMA warp has drained its DMMA stream).
-      const CheckOut co = check_unit<AKM, BKM>(P, tl, acc, P.T - 1, P.k, mw, wm, wn, lane);
+      const CheckOut co = check_unit<AKM, BKM, true>(P, tl, acc, P.T - 1, P.k, mw, wm, wn, lane);
       if (co.multi) {
         failed = P.T - 1;
       } else if (co.si >= 0) {
@@ -1692,11 +1798,30 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   if (i < ge.bm_eff) {
     FT_CHECK(ge.i0 + i < P.m && ge.j0 + ge.bn_eff <= P.n && i + ge.oa < 128 && ge.bn_eff + ge.ob <= 128);
     double *crow = P.C + (int64_t)(ge.i0 + i) + (int64_t)ge.j0 * P.ldc;
+    if (beta != 0.0) {
+      // C0 loaded EPI_B columns at a time ahead of their stores: in a load-then-store loop the
+      // compiler cannot hoist a load above the previous (possibly aliasing) store, so every
+      // column paid a full memory round trip (~30 us per 2048^3 tile wave).
+      constexpr int EPI_B = 8;
+      for (int j0 = vt >> 7; j0 < ge.bn_eff; j0 += 2 * EPI_B) {
+        double c0[EPI_B];
+#pragma unroll
+        for (int u = 0; u < EPI_B; ++u) {
+          const int j = j0 + 2 * u;
+          c0[u] = j < ge.bn_eff ? crow[(int64_t)j * P.ldc] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < EPI_B; ++u) {
+          const int j = j0 + 2 * u;
+          if (j < ge.bn_eff)
+            crow[(int64_t)j * P.ldc] =
+                __dadd_rn(__dmul_rn(alpha, ctile[(j + ge.ob) * LDC_S + i + ge.oa]), __dmul_rn(beta, c0[u]));
+        }
+      }
+    } else {
 #pragma unroll 4
-    for (int j = vt >> 7; j < ge.bn_eff; j += 2) {
-      const double v = __dmul_rn(alpha, ctile[(j + ge.ob) * LDC_S + i + ge.oa]);
-      double *dst = crow + (int64_t)j * P.ldc;
-      *dst = (beta != 0.0) ? __dadd_rn(v, __dmul_rn(beta, *dst)) : v;
+      for (int j = vt >> 7; j < ge.bn_eff; j += 2)
+        crow[(int64_t)j * P.ldc] = __dmul_rn(alpha, ctile[(j + ge.ob) * LDC_S + i + ge.oa]);
     }
   }
 #ifdef FTBLAS_DEV_TIMELINE

@@ -44,6 +44,5 @@ print(f"{M}x{N}x{K}: noft {noft:.2f} ms, ft {ft:.2f} ms ({100 * (ft - noft) / no
       f"ft Kc={KC} {ftk:.2f} ms ({100 * (ftk - noft) / noft:.2f}%)", flush=True)
 print(f"intermediate checks: {calls:.0f} (2 timed runs); per check clk: skew+stage "
       f"{p[:, 0].sum().item() / calls:.0f}, reductions {p[:, 1].sum().item() / calls:.0f}, "
-      f"decision {p[:, 3].sum().item() / calls:.0f}; over the 8 rounds: staging+barrier "
-      f"{p[:, 4].sum().item() / calls:.0f}, reduction+barrier {p[:, 5].sum().item() / calls:.0f}; "
-      f"stores {p[:, 6].sum().item() / calls:.0f}, column pair {p[:, 7].sum().item() / calls:.0f}", flush=True)
+      f"decision {p[:, 3].sum().item() / calls:.0f}; of the first: arrival skew (first barrier) "
+      f"{p[:, 4].sum().item() / calls:.0f}, drain of the warp's DMMA stream {p[:, 5].sum().item() / calls:.0f}", flush=True)
