@@ -1285,7 +1285,7 @@ __device__ __forceinline__ void partials_rs(SmemTail &tl, const double (&acc)[8]
 // partials meet in shared memory (6 KB; no staging of the tile).  The checksum row / column are
 // excluded by index.  The loop-carried segment state lives in shared memory, so the DMMA k-loop
 // keeps its register allocation (tools/kloop_stats.py).
-template <bool AKM, bool BKM, bool RS>
+template <bool AKM, bool BKM, int RS>
 __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, const double (&acc)[8][4][2], int t,
                                                int64_t kt, int mw, int wm, int wn, int lane) {
   const int g = lane >> 2, tq = lane & 3;
@@ -1305,9 +1305,12 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
   const long long dv_tb = clock64();
 #endif
   const int cra = tl.geo.cra, crb = tl.geo.crb;
-  if (!RS) {
-    // (the serial form: one column / row chain at a time with full butterflies; used where the
-    // reduce-scatter form below pushes the DMMA k-loop into spills)
+  // RS 0: the serial form below; 1: the reduce-scatter form for the standard checksum positions,
+  // else the serial form; 2: the reduce-scatter form always.  (Chosen per call site and layout
+  // so that the DMMA k-loop around an intermediate check keeps its registers.)
+  const bool std_geo = (cra == 0 || cra == DM) && (crb == 0 || crb == DM);
+  if (RS == 0 || (RS == 1 && !std_geo)) {
+    // serial: one column / row chain at a time with full butterflies
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
   #pragma unroll
@@ -1346,8 +1349,8 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     // k-loop's segment loop (where it would hold registers across the DMMA stream).
     int lg = g, lt = tq, lwm = wm, lwn = wn;
     asm volatile("" : "+r"(lg), "+r"(lt), "+r"(lwm), "+r"(lwn));
-    if ((cra == 0 || cra == DM) && (crb == 0 || crb == DM)) partials_rs<AKM, BKM, true>(tl, acc, lg, lt, lwm, lwn, cra, crb);
-    else partials_rs<AKM, BKM, false>(tl, acc, lg, lt, lwm, lwn, cra, crb);
+    if (std_geo) partials_rs<AKM, BKM, true>(tl, acc, lg, lt, lwm, lwn, cra, crb);
+    else if (RS == 2) partials_rs<AKM, BKM, false>(tl, acc, lg, lt, lwm, lwn, cra, crb);
   }
   bar_sync(BAR_PART, 256);
 #ifdef FTBLAS_DEV
@@ -1542,7 +1545,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       if (FT && s == ld_sv(ws, W_NEXT_CHECK)) {
         const int kcs = max(1, (int)(P.Kc / BK));
         const int tcur = s / kcs - 1;
-        const CheckOut co = check_unit<AKM, BKM, BKM>(P, tl, acc, tcur, (int64_t)s * BK, mw, wm, wn, lane);
+        const CheckOut co = check_unit<AKM, BKM, BKM ? 2 : (AKM ? 0 : 1)>(P, tl, acc, tcur, (int64_t)s * BK, mw, wm, wn, lane);
         // A single error is subtracted now, so the next intervals verify the
         // corrected partial product; in recompute mode (R4) the cell is also replaced by a fresh
         // k-long dot product in the epilogue (fix list), which equals the oracle's recomputed
@@ -1701,7 +1704,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     if (owner && verify && failed < 0 && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
       // The last interval, verified before C is written, from the registers
       // (its first barrier is also the point where every MMA warp has drained its DMMA stream).
-      const CheckOut co = check_unit<AKM, BKM, true>(P, tl, acc, P.T - 1, P.k, mw, wm, wn, lane);
+      const CheckOut co = check_unit<AKM, BKM, 2>(P, tl, acc, P.T - 1, P.k, mw, wm, wn, lane);
       if (co.multi) {
         failed = P.T - 1;
       } else if (co.si >= 0) {
