@@ -46,3 +46,21 @@ print(json.dumps({
                            "stage_and_ring_release": round((mq[1] - (mq[0] if not noft else m[1])).item()),
                            "decide_to_store": round((mq[2] - mq[1]).item()), "store": round((m[2] - mq[2]).item())},
 }), flush=True)
+# grid-level view: CTA start (globaltimer, ns) and end (start + role clocks at the SM clock)
+ghz = float(os.environ.get("SM_GHZ", "1.965"))
+st = p[:, 0] - p[:, 0].min()
+en = st + p[:, 3] / ghz
+span = en.max().item()
+ss, es = st.sort().values, en.sort().values
+nsm = torch.cuda.get_device_properties(0).multi_processor_count
+print(json.dumps({
+    "span_us": span / 1e3, "event_ms": ms, "busy_frac_of_sms_x_span": (p[:, 3] / ghz).sum().item() / (nsm * span),
+    "mean_cta_us": (p[:, 3] / ghz).mean().item() / 1e3,
+    "start_us": {"cta_%d" % nsm: ss[min(nsm, len(ss) - 1)].item() / 1e3, "last": ss[-1].item() / 1e3},
+    "end_us": {"first": es[0].item() / 1e3, "median": es[len(es) // 2].item() / 1e3, "last": es[-1].item() / 1e3},
+}), flush=True)
+if os.environ.get("TL_DUMP"):  # per CTA: blockIdx, start (ns from the first), duration (ns), first-ready clk, k-loop end clk
+    import numpy as np
+    idx = torch.nonzero(sel).flatten().cpu().numpy()
+    np.save(os.environ["TL_DUMP"], np.stack([idx, st.cpu().numpy(), (p[:, 3] / ghz).cpu().numpy(),
+                                             p[:, 1].cpu().numpy(), p[:, 2].cpu().numpy()], 1))
