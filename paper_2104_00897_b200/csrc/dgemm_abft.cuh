@@ -748,6 +748,9 @@ struct SmemTail {
   int wstate[N_MMA_WARPS][8];      // per MMA warp: segment state of the k-loop (mma_role)
   int retry;                       // -1: done; else the interval whose check asked for a recompute
   int ticket;                      // k-split: arrival order of this split among the tile's splits
+  // tau factors (2 gamma(kt + len) + 8u) kt len of intervals t < TAU_TAB, [0]: columns (len =
+  // bm_eff), [1]: rows (len = bn_eff); filled while the first stage loads (check_decide)
+  double tau_f[2][64];
 };
 constexpr size_t SMEM_BYTES = 1024 + sizeof(double) * STAGES * STAGE_ELEMS + sizeof(SmemTail);
 
@@ -1118,6 +1121,15 @@ struct CheckOut {
   double dcol;  // the located magnitude d_col to subtract from it
 };
 
+// DESIGN.md R1, R17: 2 gamma(kt + len) for the two sums plus 2^-50 = 8u for the fixed-point
+// encode (per element below 2^-50 max|x|, summed over len rows and kt k-slots), times kt len;
+// tau = min(factor * amax * bmax, DBL_MAX) (R13: a NaN or infinite residual always flags).
+constexpr int TAU_TAB = 64;
+__device__ __forceinline__ double tau_factor(int64_t kt, int len) {
+  const double nu = (double)(kt + len) * 0x1p-53;
+  return (2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len;
+}
+
 // Residuals, threshold, flags, classification and report of one unit at the end of
 // interval t, from the reference sums (tl.colsum, tl.rowsum) and the carried checksums
 // (tl.cs_col, tl.cs_row) already in shared memory.  All 256 MMA threads.
@@ -1149,11 +1161,10 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
   const double amx = __longlong_as_double((long long)(((unsigned long long)amax_hi << 32) | 0xFFFFFFFFull));
   const double bmx = __longlong_as_double((long long)(((unsigned long long)bmax_hi << 32) | 0xFFFFFFFFull));
   const int len = is_row ? x.bn_eff : x.bm_eff;
-  const double nu = (double)(kt + len) * 0x1p-53;
-  // DESIGN.md R1, R17: 2 gamma(kt + len) for the two sums plus 2^-50 = 8u for the fixed-point
-  // encode (per element below 2^-50 max|x|, summed over len rows and kt k-slots); clamped to the
-  // largest finite double (R13): a NaN or infinite residual always flags.
-  const double tau = fmin((2.0 * (nu / (1.0 - nu)) + 0x1p-50) * (double)kt * (double)len * amx * bmx, 0x1.fffffffffffffp1023);
+  // (the factor of interval t, formed before the k-loop for t < TAU_TAB: same expression, same
+  // rounding; the check's own dependent chain is two products)
+  const double fct = t < TAU_TAB ? tl.tau_f[is_row ? 1 : 0][t] : tau_factor(kt, len);
+  const double tau = fmin(fct * amx * bmx, 0x1.fffffffffffffp1023);
   const bool flag = valid && !(fabs(d) <= tau) && !(FT_DEV_MODE(P) & 4);
   tl.dres[vt] = d;
   if (flag) atomicMin(is_row ? &tl.first_row[par] : &tl.first_col[par], cidx);
@@ -1449,6 +1460,14 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     st_sv(ws, W_NARROW, !FT ? 0
                             : (max(x.oa + x.bm_eff, x.cra + 1) - wm * 64 <= 16 ? 1 : 0) |
                                   (max(x.ob + x.bn_eff, x.crb + 1) - wn * 32 <= 16 ? 2 : 0));
+  }
+  if (FT) {  // the checks' tau factors, while the first stage loads (the FP64 pipe is idle here)
+    const int kcs = max(1, (int)(P.Kc / BK)), nt = min(P.T, TAU_TAB);
+    for (int q = vt; q < 2 * nt; q += 256) {
+      const int t = q >> 1;
+      const int64_t kt = t < P.T - 1 ? (int64_t)(t + 1) * kcs * BK : P.k;  // the check's kt (mma_role calls)
+      tl.tau_f[q & 1][t] = tau_factor(kt, (q & 1) ? x.bn_eff : x.bm_eff);
+    }
   }
 #ifdef FTBLAS_DEV_TIMELINE
   // tools/dev_timeline.py (timeline build, -DFTBLAS_DEV_TIMELINE only): MMA warp 0's

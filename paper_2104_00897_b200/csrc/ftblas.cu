@@ -22,6 +22,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <functional>
 
 namespace {
 
@@ -375,6 +376,47 @@ struct ReportSink {
   int64_t col_off = 0;  // global column of this piece's column 0
 };
 
+// k-split of few-wave launches with a long k (C4b: 516 full tiles + 134 sliver tiles on 148
+// SMs is 3.5 waves of full tiles, i.e. 4 rounds): the split that minimises the launch's makespan,
+// estimated by list scheduling the CTAs in launch order (full tiles, then the protected kernel's
+// sliver tiles, which the raster puts last) on the SMs, in stage units.  A split CTA costs its
+// k-range plus the tile's fixed cost (first stage, check, store: ~3 stages) plus the partial
+// block's write and, for the tile's last split, the read of the S partials (~0.6 stage each).
+// A sliver tile of the protected kernel (at most 15 data rows / columns: the narrow DMMA loop)
+// costs 0.32 of a full one (timeline build at C4b: 701 against 2192 us); the unprotected
+// kernel has no narrow loop, all its tiles count as full.  Split only for an estimated gain of
+// 3% or more, >= 64 stages per split and at most 8192 split CTAs (1 GB of partial blocks).
+int wave_ksplit(bool ft, int64_t m, int64_t n, int tm, int tn, int nk, int nsm) {
+  const int64_t tiles_m = (m + tm - 1) / tm, tiles_n = (n + tn - 1) / tn;
+  const bool sliver_r = ft && m % tm != 0 && m % tm < 16, sliver_c = ft && n % tn != 0 && n % tn < 16;
+  const int64_t full_m = tiles_m - (sliver_r ? 1 : 0), full_n = tiles_n - (sliver_c ? 1 : 0);
+  const int64_t nfull = full_m * full_n, nsliver = tiles_m * tiles_n - nfull;
+  if (nfull > 16 * (int64_t)nsm) return 1;  // many waves: the last partial wave costs < 1/16
+  auto makespan = [&](int S) {
+    std::vector<double> free_at((size_t)nsm, 0.0);  // min-heap of the SMs' next free time
+    auto run = [&](int64_t cnt, double cost) {
+      for (int64_t c = 0; c < cnt; ++c) {
+        std::pop_heap(free_at.begin(), free_at.end(), std::greater<double>());
+        free_at.back() += cost;
+        std::push_heap(free_at.begin(), free_at.end(), std::greater<double>());
+      }
+    };
+    const double red = S > 1 ? 0.5 + 0.6 * S : 0.0;
+    run(nfull * S, (double)nk / S + 3.0 + red);
+    run(nsliver * S, 0.32 * nk / S + 3.0 + red);
+    return *std::max_element(free_at.begin(), free_at.end());
+  };
+  const double t1 = makespan(1);
+  int best = 1;
+  double best_t = 0.97 * t1;
+  for (int S = 2; S <= 4; ++S) {
+    if (nk / S < 64 || (nfull + nsliver) * S > 8192) break;
+    const double t = makespan(S);
+    if (t < best_t) { best = S; best_t = t; }
+  }
+  return best;
+}
+
 // The core entry: device pointers, protected (FT) or not, explicit fault list.
 int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char tb, int64_t m, int64_t n,
                int64_t k, double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
@@ -429,6 +471,8 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.ksplit = 1;
   if (T == 1 && (int64_t)p.ntiles * 8 <= (int64_t)num_sms())
     p.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)p.nk / 2, 8));
+  else if (T == 1)
+    p.ksplit = wave_ksplit(ft, m, n, tm, tn, p.nk, num_sms());
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
   p.correct_mode = tl_correct;
   p.cluster2 = (ft && tl_encode == FTBLAS_ENCODE_FUSED_LOCAL && p.ksplit == 1) ? 1 : 0;  // request; launch_one decides

@@ -112,3 +112,23 @@ def test_intervals_no_false_positives_and_subtract():
                         subtract=True)
     assert rep.corrected == 2 and np.array_equal(Cg, A @ B)
     assert_reports_match(rep, orep)
+
+
+@pytest.mark.parametrize("trans", ["NN", "TT"])
+def test_intervals_beyond_tau_table(trans):
+    """T = 100 intervals (Kc = 16, k = 1600): the kernel forms the tau factors of intervals
+    t < 64 before the k-loop and computes the later ones inline at the check (TAU_TAB); events in
+    both ranges, a recompute decided at t = 80 (two faults, two rows and two columns) and
+    verification of the intervals after it, all equal to the oracle's."""
+    rng = np.random.default_rng(420)
+    m, n, k, Kc = 200, 190, 1600, 16
+    A, B, C0 = rand(rng, m, k), rand(rng, k, n), rand(rng, m, n)
+    faults = [(5, 6, 3 * 16 + 2, 4.0),                           # t = 3 (table)
+              (150, 20, 70 * 16, -9.0),                          # t = 70 (inline)
+              (40, 50, 80 * 16 + 1, 2.0), (41, 60, 80 * 16 + 3, 3.0),  # t = 80: recompute
+              (41, 60, 90 * 16, 5.0),                            # t = 90, after the recompute
+              (199, 189, k, 1e3)]                                # the last interval (t = 99)
+    _, rep, orep = run(stored(A, trans[0]), stored(B, trans[1]), C0, Kc, ta=trans[0], tb=trans[1],
+                       alpha=1.0, beta=0.5, faults=faults)
+    assert_reports_match(rep, orep, stored(A, trans[0]), stored(B, trans[1]), trans[0], trans[1], k)
+    assert rep.units_checked == 4 * 100 and rep.recomputed == 1 and rep.corrected == 4
