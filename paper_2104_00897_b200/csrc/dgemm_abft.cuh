@@ -1457,9 +1457,12 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   enum { W_NEXT_STAGE = 0, W_NEXT_CHECK, W_FNEXT, W_FAILED, W_BASE, W_NARROW, W_NK, W_SOFF };
   if (lane == 0) {
     st_sv(ws, W_BASE, 0);
+    // (bits 4 / 8: the used rows / columns fit in the first m-tile / n-tile of a K-major
+    // operand, 8 rows / columns)
+    const int ur = max(x.oa + x.bm_eff, x.cra + 1) - wm * 64, uc = max(x.ob + x.bn_eff, x.crb + 1) - wn * 32;
     st_sv(ws, W_NARROW, !FT ? 0
-                            : (max(x.oa + x.bm_eff, x.cra + 1) - wm * 64 <= 16 ? 1 : 0) |
-                                  (max(x.ob + x.bn_eff, x.crb + 1) - wn * 32 <= 16 ? 2 : 0));
+                            : (ur <= 16 ? 1 : 0) | (uc <= 16 ? 2 : 0) | (AKM && ur <= 8 ? 4 : 0) |
+                                  (BKM && uc <= 8 ? 8 : 0));
   }
   if (FT) {  // the checks' tau factors, while the first stage loads (the FP64 pipe is idle here)
     const int kcs = max(1, (int)(P.Kc / BK)), nt = min(P.T, TAU_TAB);
@@ -1530,7 +1533,13 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       }
       const int narrow = FT ? ld_sv(ws, W_NARROW) : 0;
       if (FT && narrow) {  // sliver tiles: only the m / n tiles holding used rows / columns
-        if (narrow == 1) kloop_narrow<AKM, BKM, 2, 4>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+        if (AKM && (narrow & 4)) {
+          if (narrow & 2) kloop_narrow<AKM, BKM, 1, 2>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+          else kloop_narrow<AKM, BKM, 1, 4>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+        } else if (BKM && (narrow & 8)) {
+          if (narrow & 1) kloop_narrow<AKM, BKM, 2, 1>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+          else kloop_narrow<AKM, BKM, 8, 1>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
+        } else if (narrow == 1) kloop_narrow<AKM, BKM, 2, 4>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
         else if (narrow == 2) kloop_narrow<AKM, BKM, 8, 2>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
         else kloop_narrow<AKM, BKM, 2, 2>(tl, ring, ready, gs, gs_end, wm, wn, g, t, lane, acc);
       }

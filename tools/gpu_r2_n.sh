@@ -1,0 +1,10 @@
+# GPU tests + quick perf
+set -x
+python -c "import oracle; oracle.build()"
+: > gpurun_out/${TAG}_pytest.log
+for f in $(ls tests/test_gpu_*.py); do
+  timeout 600 python -m pytest $f -m gpu -q -x -p no:cacheprovider >> gpurun_out/${TAG}_pytest.log 2>&1
+  echo "$f rc=$?" | tee -a gpurun_out/${TAG}_pytest.log
+done
+grep -E "passed|failed|error" gpurun_out/${TAG}_pytest.log
+timeout 600 python tools/quick_perf.py | tee gpurun_out/${TAG}_qp.jsonl
