@@ -170,21 +170,29 @@ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? 
 // Relaxed (morally strong, unordered) accesses for the checksum publication (R22): every
 // published word is validated on its own against the all-ones fill, so no flag, fence or
 // acquire is needed and the loads do not block until their values are used.
+// The published words are read by every tile of their tile row / column over the whole launch
+// while A and B stream through L2: loads and stores carry an L2 evict_last policy so that the
+// small publication region stays resident (a consumer's first stage waits for these loads).
+#define FT_PUB_POLICY "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
 __device__ __forceinline__ double ld_relaxed_gpu(const double *p) {
   double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  asm volatile("{\n.reg .b64 pol;\n" FT_PUB_POLICY "ld.relaxed.gpu.global.L2::cache_hint.f64 %0, [%1], pol;\n}\n"
+               : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned *p) {
   unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p));
+  asm volatile("{\n.reg .b64 pol;\n" FT_PUB_POLICY "ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], pol;\n}\n"
+               : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ void st_relaxed_gpu(double *p, double v) {
-  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+  asm volatile("{\n.reg .b64 pol;\n" FT_PUB_POLICY "st.relaxed.gpu.global.L2::cache_hint.f64 [%0], %1, pol;\n}\n"
+               ::"l"(p), "d"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_gpu(unsigned *p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+  asm volatile("{\n.reg .b64 pol;\n" FT_PUB_POLICY "st.relaxed.gpu.global.L2::cache_hint.u32 [%0], %1, pol;\n}\n"
+               ::"l"(p), "r"(v) : "memory");
 }
 // The publication buffers are filled with all-ones bytes before the launch: an all-ones double
 // is a NaN that fx_to_double never produces, an all-ones maximum has the sign bit that R1'
