@@ -30,7 +30,9 @@
  *   - Work is enqueued on the calling thread's stream (ftblas_set_stream; default: the
  *     legacy default stream 0).
  *   - The library owns lazily allocated per-device scratch (report counters, event ring,
- *     fault lists, host-API staging buffers); ftblas_finalize() releases it.
+ *     fault lists, host-API staging buffers), stream-ordered from the device's default memory
+ *     pool, whose release threshold it sets to a quarter of the device memory (scratch up to
+ *     that stays cached between calls); ftblas_finalize() releases it.
  *
  * Status codes (return value of every int function):
  *     0  success — INCLUDING when soft errors were detected and corrected; detection is

@@ -170,10 +170,14 @@ int ensure_device_init() {
   CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_init_mu);
   if (dev >= 0 && dev < 64 && !g_init_done[dev]) {
-    // Keep stream-ordered scratch cached in the device's default pool.
+    // Keep stream-ordered scratch cached in the device's default pool, up to a quarter of the
+    // device memory (the C5 host-buffer pipeline's panels fit; larger transient scratch is
+    // returned at the next synchronisation instead of staying reserved until ftblas_finalize).
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = UINT64_MAX;
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t thr = (uint64_t)total_b / 4;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     g_init_done[dev] = true;
   }

@@ -163,3 +163,23 @@ def test_many_events_both_readbacks_and_capacity():
     F.ftblas_inject_arm(faults)
     rep2 = F.ftblas_dgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, events_capacity=50)
     assert rep2.n_events == 300 and events_key(rep2.events) == events_key(orep.events)[:50]
+
+
+@pytest.mark.parametrize("trans", ["NN", "TT"])
+def test_few_wave_ksplit_parity(trans):
+    """A launch the host splits in k (wave_ksplit: 156 tiles on 148 SMs, k = 2048 -> 2 splits
+    of 64 stages, 312 CTAs in 3 rounds instead of 2 full-length ones), with faults in both
+    splits' k-ranges, after the last update (step = k: the owner adds it to the summed block)
+    and a two-fault unit (recomputed unsplit by the tile's owner), beta != 0: values within the
+    bound and events / counters equal to the oracle's on every fault unit + seeded units."""
+    m, n, k = 12 * 127, 13 * 127, 2048
+    faults = [(10, 20, 0, 3.0),                          # split 0, first update
+              (400, 700, 1000, -50.0),                   # split 0 (stages 0..63)
+              (900, 1200, 1500, 7.5),                    # split 1 (stages 64..127)
+              (1523, 1650, k, 1e3),                      # after the last update, corner unit
+              (3 * 127 + 5, 4 * 127 + 6, 300, 2.0),      # two faults in one unit: recompute
+              (3 * 127 + 60, 4 * 127 + 90, 1800, -4.0)]
+    c = synth.make_case("fewwave_" + trans, trans[0], trans[1], m, n, k, alpha=1.5, beta=0.5,
+                        seed=77, faults=faults)
+    rep, orep, _ = run_config(c, extra_units=12)
+    assert (rep.detected, rep.corrected, rep.recomputed) == (5, 4, 1)
