@@ -86,6 +86,8 @@ struct Params {
   // and its stage maxima to part_max; the last split of a tile to finish (ticket) sums the
   // partials in split order (deterministic), verifies the whole C^f block and stores the tile.
   int ksplit;
+  int kcoop;  // 1: the splits of a tile are co-resident (cooperative launch): the S splits sum
+              // one slice of the block each (distributed reduction) instead of the last one alone
   double *part;
   unsigned *part_max;
   int *tickets;  // per tile, zeroed by the host
@@ -184,6 +186,11 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned *p) {
   unsigned v;
   asm volatile("{\n.reg .b64 pol;\n" FT_PUB_POLICY "ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], pol;\n}\n"
                : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_relaxed_gpu(double *p, double v) {
@@ -1332,28 +1339,28 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
     // serial: one column / row chain at a time with full butterflies
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-  #pragma unroll
+#pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = wn * 32 + tile_row<BKM>(b, 2 * tq + e);
         double c = 0.0;
-  #pragma unroll
+#pragma unroll
         for (int a = 0; a < 8; ++a) {
           const double v = acc[a][b][e];
           if (wm * 64 + tile_row<AKM>(a, g) != cra) c += v;
           else tl.cs_col[col] = v;  // carried (e^T A_I) B_J
         }
-  #pragma unroll
+#pragma unroll
         for (int o = 4; o <= 16; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (g == 0) tl.colpart[wm][col] = c;
       }
     }
-  #pragma unroll
+#pragma unroll
     for (int a = 0; a < 8; ++a) {
       const int row = wm * 64 + tile_row<AKM>(a, g);
       double r = 0.0;
-  #pragma unroll
+#pragma unroll
       for (int b = 0; b < 4; ++b)
-  #pragma unroll
+#pragma unroll
         for (int e = 0; e < 2; ++e) {
           const double v = acc[a][b][e];
           if (wn * 32 + tile_row<BKM>(b, 2 * tq + e) != crb) r += v;
@@ -1399,6 +1406,34 @@ __device__ __forceinline__ CheckOut check_unit(const Params &P, SmemTail &tl, co
 #else
   return check_decide<AKM, BKM>(P, tl, t, kt, mw, lane);
 #endif
+}
+
+// k-split with co-resident splits (P.kcoop): wait for the tile's S partial blocks, sum slice q
+// of the accumulator registers [64q/S, 64(q+1)/S) over them in split order into partial 0,
+// then (split S-1) wait for every slice.  Out of line: it touches memory only, and inlined it
+// moved the register allocation of the DMMA k-loops.
+__device__ __forceinline__ void ksplit_coop_reduce(const Params &P, SmemTail &tl, const double *p0, int slot, int q,
+                                                int S, int vt) {
+  if (vt == 0) {
+    tl.ticket = q;
+    atomicAdd(&P.tickets[slot], 1);
+    while (ld_acquire_gpu(&P.tickets[slot]) < S) __nanosleep(32);
+  }
+  bar_sync(BAR_CTILE, 256);
+  double *const sum0 = const_cast<double *>(p0);
+  for (int reg = (64 * q) / S; reg < (64 * (q + 1)) / S; ++reg) {
+    double v = __ldcg(p0 + reg * 256);
+    for (int r = 1; r < S; ++r) v += __ldcg(p0 + (size_t)r * (BM * BN) + reg * 256);
+    __stcg(sum0 + reg * 256, v);
+  }
+  __threadfence();
+  bar_sync(BAR_CTILE, 256);
+  if (vt == 0) {
+    atomicAdd(&P.tickets[slot], 1);
+    if (q == S - 1)
+      while (ld_acquire_gpu(&P.tickets[slot]) < 2 * S) __nanosleep(32);
+  }
+  bar_sync(BAR_CTILE, 256);
 }
 
 // The DMMA k-loop of a sliver tile's warp over its first NA m-tiles and NB n-tiles only.
@@ -1673,29 +1708,50 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       }
       __threadfence();
       bar_sync(BAR_CTILE, 256);
-      if (vt == 0) tl.ticket = atomicAdd(&P.tickets[slot], 1);
-      bar_sync(BAR_CTILE, 256);
-      owner = tl.ticket == S - 1;
-      if (owner) {
-        __threadfence();
-        // (every split's partial from memory, this one's included: the same sum in the same
-        // order whichever split arrives last)
+      if (P.kcoop) {
+        // Co-resident splits (cooperative launch): split q sums its slice of the accumulator
+        // registers over the S partials in split order into partial 0 (the same sum per
+        // element as one CTA summing them all), then split S-1 carries on with the whole block.
+        // (One CTA reading all S blocks was 12 of C1's 27 us.)
         const double *p0 = P.part + (size_t)slot * S * (BM * BN) + vt;
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) acc[a][b][e] = __ldcg(p0 + ((a * 4 + b) * 2 + e) * 256);
-        for (int r = 1; r < S; ++r) {
-          const double *pr = p0 + (size_t)r * (BM * BN);
+        ksplit_coop_reduce(P, tl, p0, slot, q, S, vt);
+        owner = tl.ticket == S - 1;
+        if (owner) {
+          __threadfence();
 #pragma unroll
           for (int a = 0; a < 8; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) acc[a][b][e] += __ldcg(pr + ((a * 4 + b) * 2 + e) * 256);
+              for (int e = 0; e < 2; ++e) acc[a][b][e] = __ldcg(p0 + ((a * 4 + b) * 2 + e) * 256);
         }
+      } else {
+        if (vt == 0) tl.ticket = atomicAdd(&P.tickets[slot], 1);
+        bar_sync(BAR_CTILE, 256);
+        owner = tl.ticket == S - 1;
+        if (owner) {
+          __threadfence();
+          // (every split's partial from memory, this one's included: the same sum in the same
+          // order whichever split arrives last)
+          const double *p0 = P.part + (size_t)slot * S * (BM * BN) + vt;
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) acc[a][b][e] = __ldcg(p0 + ((a * 4 + b) * 2 + e) * 256);
+          for (int r = 1; r < S; ++r) {
+            const double *pr = p0 + (size_t)r * (BM * BN);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) acc[a][b][e] += __ldcg(pr + ((a * 4 + b) * 2 + e) * 256);
+          }
+        }
+      }
+      if (owner) {
         // The tile's faults after its last update (stage nk): on the summed block, as the unsplit
         // kernel adds them after its last stage.
         if (P.nfaults > 0) {

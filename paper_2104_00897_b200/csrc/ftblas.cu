@@ -130,6 +130,27 @@ int launch_one(const CUtensorMap &ta, const CUtensorMap &tb, const ftk::Params &
     return 0;
   }
   p.cluster2 = 0;
+  if (p.kcoop) {
+    // k-split of a single-wave launch: a cooperative launch makes the splits of a tile
+    // co-resident, so they can reduce their partial blocks together (dgemm_abft.cuh); if the
+    // driver refuses it, the ticket reduction (the last split sums alone) needs no co-residency.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(ftk::NTHREADS);
+    cfg.dynamicSmemBytes = ftk::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kfn, ta, tb, p) == cudaSuccess) {
+      ++tl_launches;
+      return 0;
+    }
+    (void)cudaGetLastError();
+    p.kcoop = 0;
+  }
   kfn<<<grid, ftk::NTHREADS, ftk::SMEM_BYTES, st>>>(ta, tb, p);
   ++tl_launches;
   CUDA_TRY(cudaGetLastError());
@@ -473,8 +494,10 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   // tiles computed unsplit (within the parity bound).  Verification intervals (Kc < k) keep
   // whole tiles.
   p.ksplit = 1;
-  if (T == 1 && (int64_t)p.ntiles * 8 <= (int64_t)num_sms())
+  if (T == 1 && (int64_t)p.ntiles * 8 <= (int64_t)num_sms()) {
     p.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)p.nk / 2, 8));
+    p.kcoop = p.ksplit > 1 ? 1 : 0;  // one wave: the splits reduce together (launch_one)
+  }
   else if (T == 1)
     p.ksplit = wave_ksplit(ft, m, n, tm, tn, p.nk, num_sms());
   if (err) err->unit_k = (int32_t)std::min<int64_t>(Kc, INT32_MAX);
