@@ -487,16 +487,18 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   p.Kc = Kc;
   p.T = (int)T;
   p.ntiles = p.tiles_m * p.tiles_n;
-  // k-split of launches with very few tiles (C^f partials summed in split order and verified by
-  // the tile's last split, dgemm_abft.cuh): 8 splits of >= 2 stages each when they fit in one
-  // wave of the SMs (<= 18 tiles on 148 SMs; the latency-bound small problems).  The partial
-  // sums round differently from one k-loop, so such a call is not bitwise equal to the same
-  // tiles computed unsplit (within the parity bound).  Verification intervals (Kc < k) keep
-  // whole tiles.
+  // k-split of launches of at most half a wave of tiles (C^f partials summed in split order and
+  // verified by the tile's last split, dgemm_abft.cuh): up to 8 splits of >= 2 stages each, as
+  // many as fit in one wave (C1: 9 tiles x 8; 512^3: 25 x 5; the latency-bound small
+  // problems).  The partial sums round differently from one k-loop, so such a call is not
+  // bitwise equal to the same tiles computed unsplit, or split another way (a row panel of it),
+  // but within the parity bound.  Verification intervals (Kc < k) keep whole tiles.
   p.ksplit = 1;
-  if (T == 1 && (int64_t)p.ntiles * 8 <= (int64_t)num_sms()) {
-    p.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)p.nk / 2, 8));
-    p.kcoop = p.ksplit > 1 ? 1 : 0;  // one wave: the splits reduce together (launch_one)
+  if (T == 1 && (int64_t)p.ntiles * 2 <= (int64_t)num_sms()) {
+    // single wave: up to 8 splits of >= 2 stages per tile, as many as fit on the SMs
+    p.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>((int64_t)p.nk / 2, 8),
+                                                           (int64_t)num_sms() / p.ntiles));
+    p.kcoop = p.ksplit > 1 ? 1 : 0;  // the splits reduce together (launch_one)
   }
   else if (T == 1)
     p.ksplit = wave_ksplit(ft, m, n, tm, tn, p.nk, num_sms());

@@ -98,7 +98,10 @@ def test_world2_panels_on_one_gpu_match_single_call():
     assert cnt == [rep.units_checked, rep.detected, rep.corrected, rep.recomputed, rep.n_events]
     assert (rep.corrected, rep.recomputed) == (4, 1)
     assert [e[:4] for e in ev] == [e[:4] for e in rep.events]
-    assert np.array_equal(C, dC.view(n, m).t().cpu().numpy())
+    # Values: the single call (64 tiles) and the panels (32 each) split k differently
+    # (single-wave k-split: 2 and 4 splits), so they agree within the parity bound, not bitwise.
+    Cs = dC.view(n, m).t().cpu().numpy()
+    assert np.all(np.abs(C - Cs) <= 2 * (2 * k * 2.0 ** -53) * (np.abs(A) @ np.abs(B)))
 
 
 def test_bench_torchrun_gloo_one_device():
