@@ -410,7 +410,7 @@ struct ReportSink {
 // A sliver tile of the protected kernel (at most 15 data rows / columns: the narrow DMMA loop)
 // costs 0.32 of a full one (timeline build at C4b: 701 against 2192 us); the unprotected
 // kernel has no narrow loop, all its tiles count as full.  Split only for an estimated gain of
-// 3% or more, >= 64 stages per split and at most 8192 split CTAs (1 GB of partial blocks).
+// 3% or more, >= 16 stages per split and at most 8192 split CTAs (1 GB of partial blocks).
 int wave_ksplit(bool ft, int64_t m, int64_t n, int tm, int tn, int nk, int nsm) {
   const int64_t tiles_m = (m + tm - 1) / tm, tiles_n = (n + tn - 1) / tn;
   const bool sliver_r = ft && m % tm != 0 && m % tm < 16, sliver_c = ft && n % tn != 0 && n % tn < 16;
@@ -435,7 +435,7 @@ int wave_ksplit(bool ft, int64_t m, int64_t n, int tm, int tn, int nk, int nsm) 
   int best = 1;
   double best_t = 0.97 * t1;
   for (int S = 2; S <= 4; ++S) {
-    if (nk / S < 64 || (nfull + nsliver) * S > 8192) break;
+    if (nk / S < 16 || (nfull + nsliver) * S > 8192) break;
     const double t = makespan(S);
     if (t < best_t) { best = S; best_t = t; }
   }

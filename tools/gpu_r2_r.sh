@@ -8,5 +8,5 @@ for f in $(ls tests/test_gpu_*.py); do
 done
 grep -E "passed|failed|error" gpurun_out/${TAG}_pytest.log
 timeout 600 python tools/quick_perf.py | tee gpurun_out/${TAG}_qp.jsonl
-SHAPES=256x256x256NN,512x512x512NN timeout 300 python tools/quick_perf.py | tee -a gpurun_out/${TAG}_qp.jsonl
+SHAPES=256x256x256NN,512x512x512NN,1024x1024x1024NN,1536x1536x1536NN,1024x1024x4096NN timeout 300 python tools/quick_perf.py | tee -a gpurun_out/${TAG}_qp.jsonl
 timeout 300 bash tools/host_cost.sh 2>&1 | tee gpurun_out/${TAG}_host_cost.log
