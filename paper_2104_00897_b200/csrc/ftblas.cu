@@ -22,6 +22,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <map>
 #include <functional>
 
 namespace {
@@ -418,18 +419,26 @@ int wave_ksplit(bool ft, int64_t m, int64_t n, int tm, int tn, int nk, int nsm) 
   const int64_t nfull = full_m * full_n, nsliver = tiles_m * tiles_n - nfull;
   if (nfull > 16 * (int64_t)nsm) return 1;  // many waves: the last partial wave costs < 1/16
   auto makespan = [&](int S) {
-    std::vector<double> free_at((size_t)nsm, 0.0);  // min-heap of the SMs' next free time
+    // SM loads as groups {load: number of SMs}; a batch of identical CTAs fills the least
+    // loaded group first (the list schedule of identical CTAs, a few steps per round instead
+    // of a heap operation per CTA: this runs on every call)
+    std::map<double, int64_t> g;
+    g[0.0] = nsm;
     auto run = [&](int64_t cnt, double cost) {
-      for (int64_t c = 0; c < cnt; ++c) {
-        std::pop_heap(free_at.begin(), free_at.end(), std::greater<double>());
-        free_at.back() += cost;
-        std::push_heap(free_at.begin(), free_at.end(), std::greater<double>());
+      while (cnt > 0) {
+        const auto it = g.begin();
+        const double L = it->first;
+        const int64_t k = it->second, take = std::min(k, cnt);
+        g.erase(it);
+        g[L + cost] += take;
+        if (k > take) g[L] += k - take;
+        cnt -= take;
       }
     };
     const double red = S > 1 ? 0.5 + 0.6 * S : 0.0;
     run(nfull * S, (double)nk / S + 3.0 + red);
     run(nsliver * S, 0.32 * nk / S + 3.0 + red);
-    return *std::max_element(free_at.begin(), free_at.end());
+    return g.rbegin()->first;
   };
   const double t1 = makespan(1);
   int best = 1;
