@@ -93,8 +93,12 @@ typedef struct {
   double delta;
 } ftblas_fault_t;
 
-/* Protected DGEMM.  Stream-ordered; synchronises the stream only when err != NULL (to
- * fill the report).  Consumes (and disarms) any faults armed on this thread. */
+/* Protected DGEMM.  Stream-ordered; with err != NULL it returns once the report is complete,
+ * i.e. once every result of the call (C, counters, events) has been written: launches of up to
+ * 4 waves write the report into mapped pinned host memory themselves (their last CTA, after all
+ * others are done) and the call polls it -- the launch may still be retiring when the call
+ * returns; longer launches read it back and synchronise the stream.  Consumes (and disarms) any
+ * faults armed on this thread. */
 int ftblas_dgemm(char transA, char transB, int64_t m, int64_t n, int64_t k, double alpha,
                  const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                  double *C, int64_t ldc, ftblas_err_report_t *err);

@@ -60,6 +60,8 @@ struct EventDev {
 };
 
 enum { CNT_DETECTED = 0, CNT_CORRECTED, CNT_RECOMPUTED, CNT_EVENTS, CNT_N };
+constexpr int CNT_DONE = 4;  // CTAs finished (device-written report); inside the 64-byte counter slot
+constexpr int REP_EVENTS = 32;  // events the device-written report carries (the rest: a read-back)
 
 struct Params {
   int64_t m, n, k;
@@ -126,7 +128,13 @@ struct Params {
                                   // kernel on the 127 grid, 128 no clusters, 1024 skip the last check,
                                   // 2048 no proxy fence before slot refills, 4096 no interval maxima
                                   // (timing only)
-  unsigned long long *counters;   // [CNT_N]
+  unsigned long long *counters;   // [CNT_N] (+ CNT_DONE)
+  // Device-written report (ftblas.cu finish_report_mapped): the launch's last CTA copies the
+  // counters and the first rep_events events into this mapped pinned host buffer and then
+  // writes rep_seq to its word 0; null: the host reads the report back itself.
+  unsigned long long *host_rep;
+  unsigned long long rep_seq;
+  int rep_events;
   int64_t ev_row_off;             // added to event rows (row panels of the host-buffer pipeline)
   int64_t ev_col_off;             // added to event columns (column chunks of the host-buffer pipeline)
   EventDev *events;
@@ -771,7 +779,8 @@ constexpr size_t SMEM_BYTES = 1024 + sizeof(double) * STAGES * STAGE_ELEMS + siz
 
 // Named barriers (id 0 is __syncthreads).  Both roles execute the same sequence of the
 // CTA-wide ones; the 256-thread ones are private to the MMA warpgroups.
-enum { BAR_RING_FREE = 1, BAR_CTILE = 2, BAR_FLAGS_R = 3, BAR_FLAGS_C = 4, BAR_DECIDE = 5, BAR_RED = 6, BAR_PART = 7 };
+enum { BAR_RING_FREE = 1, BAR_CTILE = 2, BAR_FLAGS_R = 3, BAR_FLAGS_C = 4, BAR_DECIDE = 5, BAR_RED = 6, BAR_PART = 7,
+       BAR_REPORT = 8 };
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -1925,6 +1934,37 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
 #endif
 }
 
+// The launch's report, written by its last CTA into mapped pinned host memory: every CTA,
+// after all its threads' C stores, counter atomics and events (barrier + fences), counts itself
+// done; the last one copies the counters and the first rep_events events, then (after a
+// system-scope fence) the call's sequence number to word 0, which the host polls instead of a
+// device-to-host copy and a stream synchronisation.  Layout: [seq | counters[CNT_N] |
+// events as EventDev].
+// (Called by each role after its last global write, and by ghost CTAs: the roles run with
+// different register budgets and must not re-converge, so each meets the others at barrier
+// BAR_REPORT from its own code path; thread 0 -- an MMA thread -- does the counting.)
+__device__ __forceinline__ void publish_report(const Params &P) {
+  __threadfence();
+  bar_sync(BAR_REPORT, NTHREADS);
+  if (threadIdx.x != 0) return;
+  const unsigned long long done = atomicAdd(&P.counters[CNT_DONE], 1ull);
+  if (done != (unsigned long long)gridDim.x - 1) return;
+  __threadfence();
+  volatile unsigned long long *h = P.host_rep;
+  unsigned long long cnt[CNT_N];
+#pragma unroll
+  for (int i = 0; i < CNT_N; ++i) cnt[i] = __ldcg(&P.counters[i]);
+#pragma unroll
+  for (int i = 0; i < CNT_N; ++i) h[1 + i] = cnt[i];
+  const long long nev = min((long long)cnt[CNT_EVENTS], min((long long)P.rep_events, P.ev_cap));
+  const unsigned long long *ev = reinterpret_cast<const unsigned long long *>(P.events);
+  constexpr int W = sizeof(EventDev) / 8;
+  for (long long q = 0; q < nev * W; ++q) h[1 + CNT_N + q] = __ldcg(ev + q);
+  __threadfence_system();
+  h[0] = P.rep_seq;
+  __threadfence_system();
+}
+
 template <bool AKM, bool BKM, bool FT>
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_abft_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -2060,16 +2100,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
   if (P.cluster2) cluster_sync_all();  // partners' mailbox barriers are initialised
-  if (ghost) return;
+  if (ghost) {
+    if (FT && P.host_rep) publish_report(P);
+    return;
+  }
 
   // The two roles never re-converge, so ptxas can give each its own register budget.
   if (is_cs_warp(x.warp)) {
     // K-major A with MN-major B (TT) needs 8 more registers in the protected DMMA loop.
     if (FT && AKM && !BKM) setmaxnreg_dec<REG_CS - 16>(); else setmaxnreg_dec<REG_CS>();
     checksum_role<AKM, BKM, FT>(tmA, tmB, P, x);
+    if (FT && P.host_rep) publish_report(P);
   } else {
     if (FT && AKM && !BKM) setmaxnreg_inc<REG_MMA + 8>(); else setmaxnreg_inc<REG_MMA>();
     mma_role<AKM, BKM, FT>(P, x);
+    if (FT && P.host_rep) publish_report(P);
   }
   // A sharing pair stays resident until the partner has made its last remote access.
   if (share) cluster_sync_all();
