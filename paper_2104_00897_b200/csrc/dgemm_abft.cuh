@@ -931,7 +931,8 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       const int p = AKM ? 2 * lane : lane;
       const int64_t pg = k0 + (int64_t)s * BK + p;
       double *dst = P.Ash + x.ti * P.ldash + pg;
-      FT_CHECK(x.ti < P.tiles_m && sg < P.nk && (pg >= k1 || pg + (AKM ? 1 : 0) < P.ldash));
+      // (pg + 1 is stored only when it is < k1 <= ldash: odd k leaves the pair's second slot out)
+      FT_CHECK(x.ti < P.tiles_m && sg < P.nk && k1 <= P.ldash && (pg >= k1 || pg < P.ldash));
       if (AKM) {
         if (lane < 8 && pg < k1) st_relaxed_gpu(dst, a0);
         if (lane < 8 && pg + 1 < k1) st_relaxed_gpu(dst + 1, a1);
@@ -1214,7 +1215,8 @@ __device__ __forceinline__ CheckOut check_decide(const Params &P, SmemTail &tl, 
     atomicAdd(&P.counters[CNT_DETECTED], 1ull);
     atomicAdd(&P.counters[multi ? CNT_RECOMPUTED : CNT_CORRECTED], 1ull);
     const unsigned long long slot = atomicAdd(&P.counters[CNT_EVENTS], 1ull);
-    FT_CHECK(fr >= 0 && fr < 128 && fc >= 0 && fc < 128);
+    // (a direction without flags keeps its sentinel: a checksum-lane fault flags one direction)
+    FT_CHECK((nfr == 0 || (fr >= 0 && fr < 128)) && (nfc == 0 || (fc >= 0 && fc < 128)));
     if ((long long)slot < P.ev_cap)
       P.events[slot] = multi ? EventDev{(long long)(x.i0 + P.ev_row_off), (long long)(x.j0 + P.ev_col_off), 2, t,
                                         nfr ? tl.dres[128 + fr] : 0.0, nfc ? tl.dres[fc] : 0.0}
