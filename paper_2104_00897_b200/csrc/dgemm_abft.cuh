@@ -88,6 +88,10 @@ struct Params {
   // and its stage maxima to part_max; the last split of a tile to finish (ticket) sums the
   // partials in split order (deterministic), verifies the whole C^f block and stores the tile.
   int ksplit;
+  // Encoder CTAs at the head of a few-wave protected launch (R22): blocks [0, enc_head) encode
+  // and publish e^T A_I of tile row b (b < tiles_m, when Ash) or B_J e of tile column b - tiles_m
+  // and compute nothing else; every tile then copies the published checksums.
+  int enc_head;
   int kcoop;  // 1: the splits of a tile are co-resident (cooperative launch): the S splits sum
               // one slice of the block each (distributed reduction) instead of the last one alone
   double *part;
@@ -813,6 +817,7 @@ struct Ctx {
   // dimension of a TMA box must start 16-byte aligned), so tile-local data row i sits in
   // staged row i + o (o = x0 & 1) and the checksum row/column takes the free row cr.
   int oa, ob, cra, crb;
+  int enc_only;  // 0: a tile; 1: encoder CTA of e^T A_I (tile row ti); 2: of B_J e (tile column tj)
 };
 
 // ---------------- checksum warpgroup: four encoder warps, each also its stages' TMA producer
@@ -872,8 +877,9 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
   // published stage if its flag is already set and otherwise encodes the stage itself.  The
   // flag and the published sums are fetched before the stage's TMA bytes are waited for, so
   // the L2 round trips overlap the TMA latency.
-  const bool a_pub = P.Ash && x.tj == 0, a_sub = P.Ash && x.tj != 0;
-  const bool b_pub = P.Bsh && x.ti == 0;
+  const bool a_pub = P.Ash && (P.enc_head ? x.enc_only == 1 : x.tj == 0);
+  const bool a_sub = P.Ash && (P.enc_head ? x.enc_only == 0 : x.tj != 0);
+  const bool b_pub = P.Bsh && (P.enc_head ? x.enc_only == 2 : x.ti == 0);
   struct PubA { bool ok; double a0, a1; uint32_t am; };
   // Relaxed loads of stage s's published e^T A_I words (not used until after the TMA wait).
   // Per attempt (the k range changes for a recompute): this lane's published words of the
@@ -950,7 +956,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
       for (int s = warp; s < nk && s < STAGES; s += N_ENC_WARPS) issue(s);
     // B_J e published by tile row 0 is copied per stage like e^T A_I.  Publication only
     // happens in launches without clusters, so a cluster pair (share) never copies.
-    const bool b_sub = P.Bsh && x.ti != 0;
+    const bool b_sub = P.Bsh && (P.enc_head ? x.enc_only == 0 : x.ti != 0);
     // Only the first attempt exchanges half encodes with the cluster partner: a recompute pass
     // (this tile alone) encodes its B_J e itself, bitwise the same checksum.
     const bool share = verify && tl.share && attempt == 0;
@@ -1007,7 +1013,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
         } else if ((FT_DEV_MODE(P) & 2) && !share) {
           // development: no encode (checksum rows zero)
         } else {
-         if (doA) {
+         if (doA && x.enc_only != 2) {  // (an encoder CTA handles its own operand only)
           enc_a(sA, s, pa_, a0, a1, amax_hi);  // e^T A_I over the 127 data rows
           if (AKM) {
             if (lane < 8) *reinterpret_cast<double2 *>(sA + offA) = make_double2(a0, a1);
@@ -1015,7 +1021,7 @@ __device__ __forceinline__ void checksum_role(const CUtensorMap &tmA, const CUte
             if (lane < 16) sA[offA] = a0;
           }
          }
-         if (doB) {
+         if (doB && x.enc_only != 1) {
           const int64_t sg = k0 / BK + s;  // global stage index
           if (bcopy) {  // B_J e of this stage as published by tile row 0
             if (lane < 16) sB[offB] = pb;
@@ -1495,7 +1501,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
   // 106 instead of 186 non-DMMA instructions per stage, tools/kloop_stats.py); the other
   // unprotected ones keep their single loop.
   constexpr bool SKIP = FT || (AKM && !BKM);
-  const bool active = FT ? (wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1))
+  const bool active = FT ? (!x.enc_only && wm * 64 < max(x.oa + x.bm_eff, x.cra + 1) && wn * 32 < max(x.ob + x.bn_eff, x.crb + 1))
                          : (!SKIP || (wm * 64 < x.bm_eff && wn * 32 < x.bn_eff));
   // Sliver tiles (the last tile row / column of a size that is not a multiple of 127): a warp
   // whose used rows (columns) of its 64 x 32 quarter fit in its first 2 m-tiles (n-tiles) -- 16
@@ -1556,7 +1562,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
       st_sv(ws, W_NEXT_STAGE, x.f_lo < x.f_hi ? P.faults[x.f_lo].stage - (attempt == 0 ? x.s0 : 0) : 0x7fffffff);
       // Stage index at which the next intermediate verification interval ends (Kc = KcS
       // stages); the last interval is checked after the k-loop, on the staged tile.
-      st_sv(ws, W_NEXT_CHECK, verify && t_done + 1 < P.T - 1 ? (t_done + 2) * max(1, (int)(P.Kc / BK)) : 0x7fffffff);
+      st_sv(ws, W_NEXT_CHECK, verify && !x.enc_only && t_done + 1 < P.T - 1 ? (t_done + 2) * max(1, (int)(P.Kc / BK)) : 0x7fffffff);
       st_sv(ws, W_FAILED, -1);
     }
     __syncwarp();
@@ -1804,7 +1810,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
 #ifdef FTBLAS_DEV_TIMELINE
     if (P.dev_prof && vt == 0 && attempt == 0) FT_TL(2) = (unsigned long long)clock64() - FT_TL(3);
 #endif
-    if (owner && verify && failed < 0 && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
+    if (owner && verify && failed < 0 && !x.enc_only && !(FT_DEV_MODE(P) & 1024)) {  // dev 1024: skip the last check (timing)
       // The last interval, verified before C is written, from the registers
       // (its first barrier is also the point where every MMA warp has drained its DMMA stream).
       const CheckOut co = check_unit<AKM, BKM, 2>(P, tl, acc, P.T - 1, P.k, mw, wm, wn, lane);
@@ -1862,6 +1868,7 @@ __device__ __forceinline__ void mma_role(const Params &P, const Ctx &x) {
     bar_sync(BAR_DECIDE, NTHREADS);  // encoders learn whether (and from where) to run again
     if (failed < 0) break;  // else out of the one-error model: recompute the unit (R6)
   }
+  if (FT && x.enc_only) return;  // an encoder CTA stores nothing
   // k-split: another split of this tile verifies and stores it (a recompute only ever runs in
   // the owner, so the ticket of its first attempt decides)
   if (P.ksplit > 1 && tl.ticket != P.ksplit - 1) return;
@@ -2017,10 +2024,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     ti_ = r0 + L;  // partial last tile column, its rows top to bottom
     tj_ = P.tiles_n - 1;
   };
-  const int Lg = (int)blockIdx.x / P.ksplit;  // tile in launch order (k-split: P.ksplit CTAs each)
+  const int E = FT ? P.enc_head : 0;
+  const int enc_b = (int)blockIdx.x;  // encoder CTAs first
+  x.enc_only = enc_b < E ? ((P.Ash && enc_b < P.tiles_m) ? 1 : 2) : 0;
+  const int bid = (int)blockIdx.x - E;
+  const int Lg = x.enc_only ? 0 : bid / P.ksplit;  // tile in launch order (k-split: P.ksplit CTAs each)
   const bool ghost = P.cluster2 && Lg >= P.total;  // pads an odd grid to whole clusters
   int ti, tj;
-  map_tile(ghost ? Lg - 1 : Lg, ti, tj);
+  if (x.enc_only == 1) {
+    ti = enc_b;
+    tj = 0;
+  } else if (x.enc_only == 2) {
+    ti = 0;
+    tj = enc_b - (P.Ash ? P.tiles_m : 0);
+  } else {
+    map_tile(ghost ? Lg - 1 : Lg, ti, tj);
+  }
   // Cluster pair (2c, 2c+1): share the B_J encode when both are real tiles of the same tile
   // column and interval (a band with an odd row count pairs across columns: no sharing).
   bool share = false;
@@ -2029,10 +2048,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     map_tile(Lg ^ 1, pti, ptj);
     share = ptj == tj;
   }
-  x.tile = ti + tj * P.tiles_m;  // fault bucket key
+  x.tile = x.enc_only ? -1 : ti + tj * P.tiles_m;  // fault bucket key (encoder CTAs: none)
   x.tile_slot = Lg;
   x.nk_all = (int)((P.k + BK - 1) / BK);
-  x.q = (int)blockIdx.x % P.ksplit;
+  x.q = x.enc_only ? 0 : bid % P.ksplit;
   x.s0 = (int)((int64_t)x.q * x.nk_all / P.ksplit);
   const int s1 = (int)((int64_t)(x.q + 1) * x.nk_all / P.ksplit);
   x.k0 = (int64_t)x.s0 * BK;

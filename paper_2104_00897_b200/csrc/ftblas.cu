@@ -638,6 +638,14 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   const bool fused_shared = tl_encode == FTBLAS_ENCODE_FUSED || tl_encode == FTBLAS_ENCODE_FUSED_WAIT;
   const bool ashare = ft && fused_shared && p.tiles_n > 1 && !one_wave;
   const bool bshare = ft && fused_shared && p.tiles_m > 1 && !one_wave;
+  // Launches of at most 3 waves: encoder CTAs at the head of the grid encode and publish every
+  // tile row's e^T A_I and tile column's B_J e (integer passes only, no DMMA: several times the
+  // DMMA pace), so no tile of the first wave waits for or repeats an encode (2048^3: the first
+  // wave ran at the encoding pace, 294 against 280.5 us per tile).  Longer launches keep the
+  // tile row / column 0 publishers (their extra cost is spread over many waves).
+  p.enc_head = 0;
+  if ((ashare || bshare) && p.ksplit == 1 && !p.cluster2 && (int64_t)p.ntiles <= 3 * (int64_t)num_sms())
+    p.enc_head = (ashare ? p.tiles_m : 0) + (bshare ? p.tiles_n : 0);
   const size_t nsg = (size_t)p.nk;  // global stages over the whole k
   // Scratch: [counters (64 B) | events | faults | prepass | hmA Ash | hmB Bsh]: the counters
   // zeroed, the publication region filled with 0xFF; counters and the first events are read
@@ -746,7 +754,7 @@ int dgemm_core(bool ft, const std::vector<ftblas_fault_t> &faults, char ta, char
   if (int e = make_tmap(&tmA, p.A, p.lda, akm, m, k)) return e;
   if (int e = make_tmap(&tmB, p.B, p.ldb, bkm, n, k)) return e;
   // One launch: every CTA verifies its tile online after every Kc updates (T checks).
-  const dim3 grid((unsigned)(p.ntiles * p.ksplit));  // 1-D: grouped raster in the kernel
+  const dim3 grid((unsigned)(p.ntiles * p.ksplit + p.enc_head));  // 1-D: grouped raster in the kernel
   const int lrc = ft ? dispatch<true>(akm, bkm, tmA, tmB, p, grid, st) : dispatch<false>(akm, bkm, tmA, tmB, p, grid, st);
   if (lrc) return lrc;
 
