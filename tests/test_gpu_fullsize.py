@@ -183,3 +183,23 @@ def test_few_wave_ksplit_parity(trans):
                         seed=77, faults=faults)
     rep, orep, _ = run_config(c, extra_units=12)
     assert (rep.detected, rep.corrected, rep.recomputed) == (5, 4, 1)
+
+
+@pytest.mark.parametrize("trans", ["NN", "TN"])
+def test_encoder_head_ctas_parity(trans):
+    """A two-wave protected launch (289 tiles, k = 512): encoder CTAs at the head of the grid
+    publish every tile row's e^T A_I and tile column's B_J e, and every tile -- those of tile
+    row / column 0 included -- copies them (R22).  Faults in tile row 0, tile column 0, the
+    corner and the interior, a two-fault unit, beta != 0: values, counters and events equal to
+    the oracle's on every fault unit + seeded units."""
+    m = n = 2048
+    k = 512
+    faults = [(3, 500, 100, 5.0),                        # tile row 0
+              (700, 2, 300, -3.0),                       # tile column 0
+              (0, 0, 0, 11.0),                           # tile (0, 0), first update
+              (2047, 2047, k, 1e3),                      # corner sliver, after the last update
+              (1000, 1000, 256, 2.5), (1001, 1010, 400, -6.0)]  # two faults in one unit
+    c = synth.make_case("enchead_" + trans, trans[0], trans[1], m, n, k, alpha=1.0, beta=0.5,
+                        seed=91, faults=faults)
+    rep, orep, _ = run_config(c, extra_units=12)
+    assert (rep.detected, rep.corrected, rep.recomputed) == (5, 4, 1)
