@@ -8,5 +8,5 @@ for f in $(ls tests/test_gpu_*.py); do
 done
 grep -E "passed|failed|error" gpurun_out/${TAG}_pytest.log
 timeout 900 python tools/quick_perf.py | tee gpurun_out/${TAG}_qp.jsonl
-BETA=0.5 SHAPES=2048x2048x2048NN,4096x4096x2048NN,1024x1024x1024NN,1536x1536x1536NN timeout 300 python tools/quick_perf.py | tee -a gpurun_out/${TAG}_qp.jsonl
-timeout 300 python tools/dev_timeline.py 2048 2048 2048 2>&1 | grep "^{" | tee gpurun_out/${TAG}_tl.jsonl
+SHAPES=16384x512x16384NN,16384x516x16384NN,32768x32768x8192NN timeout 300 python tools/quick_perf.py | tee -a gpurun_out/${TAG}_qp.jsonl
+TL_DUMP=gpurun_out/${TAG}_tl_c4b.npy timeout 300 python tools/dev_timeline.py 16384 512 16384 2>&1 | grep "^{" | tee gpurun_out/${TAG}_tl.jsonl
